@@ -1,0 +1,140 @@
+/*
+ * mosaic_b200.h — C ABI of the B200-native mask-only logits + remask hot path.
+ *
+ * This is the drop-in boundary for the reference's hot-path operator
+ * (`gather_gemm`, /root/reference/pkg/src/mosaic/kernel.py:62-86) and for the
+ * memory-only graph ops that surround it in the step template
+ * (`gather_logits` / `sample` / `commit`, mosaic/workload.py:287-315), plus the
+ * workspace reservation/commit it runs out of (mosaic/vmm.py:48-147).
+ *
+ * Conventions (every entry point):
+ *   - returns an int status: MOSAIC_OK (0) or one of the error codes below; the
+ *     Python host maps them onto the reference exception hierarchy
+ *     (mosaic/errors.py: InputError / CapacityError / ResourceError);
+ *     mosaic_last_error() returns a thread-local message for the last failure;
+ *   - all device buffers are caller-owned (arena views); nothing allocates
+ *     device memory except the arena functions;
+ *   - `stream` is a cudaStream_t passed as void* (0 = legacy default stream);
+ *     all kernels are enqueued asynchronously on it, no host synchronisation;
+ *   - element types: hidden states / LM-head weights are bf16 (uint16 bits),
+ *     indices int32, statistics fp32;
+ *   - a masked-row count may be given on the device (`m_dev`, int32, e.g. the
+ *     output of mosaic_mask_compact) so that a whole step can be enqueued or
+ *     graph-captured without a device->host round trip; when m_dev is NULL the
+ *     host value m_host is used. Buffers are sized for the capacity m_cap.
+ */
+#ifndef MOSAIC_B200_H_
+#define MOSAIC_B200_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#define MOSAIC_API __attribute__((visibility("default")))
+#else
+#define MOSAIC_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum mosaic_status {
+  MOSAIC_OK = 0,
+  MOSAIC_E_INPUT = 1,       /* malformed arguments  -> InputError     (errors.py:41-42) */
+  MOSAIC_E_CAPACITY = 2,    /* commit > reservation -> CapacityError  (errors.py:33-34) */
+  MOSAIC_E_RESOURCE = 3,    /* VA/physical alloc    -> ResourceError  (errors.py:29-30) */
+  MOSAIC_E_CUDA = 4,        /* CUDA runtime/driver failure                              */
+  MOSAIC_E_UNSUPPORTED = 5  /* shape the kernels do not support (e.g. d % 64 != 0)      */
+};
+
+/* ABI version (major*100 + minor) and the last error message of this thread. */
+MOSAIC_API int mosaic_abi_version(void);
+MOSAIC_API const char* mosaic_last_error(void);
+
+/* ---------------------------------------------------------------- K1 ------
+ * Mask compaction: idx_out[0..M) = ascending positions p with x[p] == mask_id,
+ * *m_out = M (device int32). Restates np.flatnonzero(x == MASK_ID); the
+ * reference takes mask_idx as a ready graph input (workload.py:199-200) and
+ * only validates it (kernel.py:42-49).
+ * `scratch` must hold mosaic_mask_compact_scratch_bytes(L) bytes.            */
+MOSAIC_API size_t mosaic_mask_compact_scratch_bytes(int64_t L);
+MOSAIC_API int mosaic_mask_compact(const int32_t* x, int64_t L, int32_t mask_id,
+                        int32_t* idx_out, int32_t* m_out,
+                        void* scratch, void* stream);
+
+/* ---------------------------------------------------------------- K2 ------
+ * Row gather: Hc[i, :] = H[src(idx[i]), :] for i < M, src(p) = p (shift=0) or
+ * max(p-1, 0) (shift=1, Dream's token-level shift, workload.py:295-303).
+ * Replaces the indirect panel fetch `H[rows, k0:k1]` of kernel.py:77.
+ * H: [n_rows, d] with row stride ld_h (elements); Hc: [m_cap, d] dense.
+ * d must be a multiple of 8 and ld_h too (16-byte rows).                    */
+MOSAIC_API int mosaic_gather_rows(const uint16_t* H, int64_t n_rows, int64_t ld_h, int64_t d,
+                       const int32_t* idx, const int32_t* m_dev, int64_t m_host,
+                       int64_t m_cap, int32_t shift, uint16_t* Hc, void* stream);
+
+/* ---------------------------------------------------------------- K3 ------
+ * Mask-only LM head with the fused softmax-statistics epilogue.
+ * For every row r < M of Hc [m_cap, d] and every vocab split s of the shard
+ * W [V_shard, d] (row-major, K-major for TMA/UMMA; the reference stores the
+ * transpose [d, V], kernel.py:26):
+ *   part_max[s*m_cap + r] = max_{v in split s} logit(r, v)
+ *   part_sum[s*m_cap + r] = sum_{v in split s} exp(logit(r, v) - part_max)
+ *   part_arg[s*m_cap + r] = v_offset + argmax (lowest index on ties)
+ * with logit(r, v) = <Hc[r, :], W[v, :]> in fp32 (tcgen05, bf16 operands).
+ * The [M, V] logits are never written. n_splits is chosen by
+ * mosaic_lmhead_plan() and the partial buffers hold n_splits*m_cap entries.
+ * d must be a multiple of 64, V_shard >= 1.                                  */
+MOSAIC_API int mosaic_lmhead_plan(int64_t m_cap, int64_t V_shard, int64_t d, int32_t* n_splits_out,
+                       int32_t* tiles_per_split_out);
+MOSAIC_API int mosaic_lmhead_stats(const uint16_t* Hc, int64_t m_cap, const int32_t* m_dev, int64_t m_host,
+                        const uint16_t* W, int64_t V_shard, int64_t d, int64_t v_offset,
+                        int32_t n_splits, float* part_max, float* part_sum, int32_t* part_arg,
+                        void* stream);
+
+/* Debug / parity path for the reference operator itself: out[r, v] =
+ * <Hc[r, :], W[v, :]> in fp32, row stride ldo. Materialises the logits like
+ * gather_gemm (kernel.py:68); the product path never calls it.               */
+MOSAIC_API int mosaic_lmhead_logits(const uint16_t* Hc, int64_t m_cap, const int32_t* m_dev, int64_t m_host,
+                         const uint16_t* W, int64_t V_shard, int64_t d,
+                         float* out, int64_t ldo, void* stream);
+
+/* ---------------------------------------------------------------- K4 ------
+ * Merge S partial triples per row (fixed ascending-s order; larger max wins,
+ * lower index on equal max), in layout [S][stride]. Any of the outputs may be
+ * NULL: (out_max, out_sum, out_arg) receive the merged triple (used before the
+ * cross-rank exchange); (token, lse, conf) the finalised sample:
+ * token = argmax, lse = max + ln(sum), conf = p(token) = 1/sum.
+ * Realises the memory-only `sample` op (workload.py:306-308).                */
+MOSAIC_API int mosaic_stats_merge(const float* in_max, const float* in_sum, const int32_t* in_arg,
+                       int32_t S, int64_t stride, const int32_t* m_dev, int64_t m_host,
+                       int64_t m_cap, float* out_max, float* out_sum, int32_t* out_arg,
+                       int32_t* token, float* lse, float* conf, void* stream);
+
+/* ---------------------------------------------------------------- K5 ------
+ * Low-confidence remasking commit (memory-only `commit` op, workload.py:315):
+ * among the M masked rows keep the k with the highest confidence (ties ->
+ * lower position pos[r]) and write x[pos[r]] = token[r] for them; the others
+ * stay masked. selected (optional, int32 [m_cap]) receives 1/0 per row.
+ * `scratch` must hold mosaic_remask_scratch_bytes() bytes. k is clamped to M. */
+MOSAIC_API size_t mosaic_remask_scratch_bytes(void);
+MOSAIC_API int mosaic_remask_commit(const float* conf, const int32_t* pos, const int32_t* token,
+                         const int32_t* m_dev, int64_t m_host, int64_t m_cap, int64_t k,
+                         int32_t* x, int32_t* selected, void* scratch, void* stream);
+
+/* ---------------------------------------------------------------- K7 ------
+ * Contiguous device workspace with lazy physical commitment (cuMem VMM):
+ * reserve a VA range once, map physical granules for the prefix
+ * [0, round_up(target, granularity)). Mirrors Workspace/reserve/commit_to of
+ * mosaic/vmm.py:48-147 with a `cuda` backend.                                */
+typedef struct mosaic_arena mosaic_arena;
+MOSAIC_API int mosaic_arena_reserve(int32_t device, uint64_t reserve_bytes, mosaic_arena** out);
+MOSAIC_API int mosaic_arena_commit(mosaic_arena* arena, uint64_t target_bytes);
+MOSAIC_API int mosaic_arena_info(const mosaic_arena* arena, uint64_t* base, uint64_t* reserved,
+                      uint64_t* committed, uint64_t* granularity);
+MOSAIC_API int mosaic_arena_release(mosaic_arena* arena);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* MOSAIC_B200_H_ */

@@ -1,0 +1,192 @@
+// K1 mask compaction and K2 masked-row gather.
+//
+// K1 restates np.flatnonzero(x == MASK_ID): the reference receives `mask_idx`
+// as a ready graph input (mosaic/workload.py:199-200) whose entries must be
+// unique and in range (mosaic/kernel.py:42-49); compaction makes them so by
+// construction and in ascending position order. Two passes over x (4 B/token):
+// a per-tile count and a write pass that rebuilds the tile's prefix from the
+// counts of the tiles before it, so the result is deterministic without atomics.
+//
+// K2 is the indirect panel fetch of gather_gemm (`a = H[rows, k0:k1]`,
+// mosaic/kernel.py:77) done once per masked row with 128-bit loads, one warp per
+// row, so the LM-head GEMM can stream a dense [M, d] operand through TMA.
+#include "common.cuh"
+
+namespace mosaic {
+namespace {
+
+constexpr int kThreads = 256;          // 8 warps
+constexpr int kRounds = 4;             // 4 rounds of 1024 tokens per tile
+constexpr int kTile = kThreads * 4 * kRounds;  // 4096 tokens per CTA
+
+__device__ __forceinline__ int4 load4(const int32_t* x, int64_t i, int64_t L) {
+  if (i + 3 < L && ((reinterpret_cast<uintptr_t>(x + i) & 15) == 0))
+    return __ldg(reinterpret_cast<const int4*>(x + i));
+  int4 v;
+  v.x = i + 0 < L ? __ldg(x + i + 0) : 0;
+  v.y = i + 1 < L ? __ldg(x + i + 1) : 0;
+  v.z = i + 2 < L ? __ldg(x + i + 2) : 0;
+  v.w = i + 3 < L ? __ldg(x + i + 3) : 0;
+  return v;
+}
+
+__device__ __forceinline__ uint32_t flags4(int4 v, int64_t i, int64_t L, int32_t mask_id) {
+  uint32_t f = 0;
+  f |= (i + 0 < L && v.x == mask_id) ? 1u : 0u;
+  f |= (i + 1 < L && v.y == mask_id) ? 2u : 0u;
+  f |= (i + 2 < L && v.z == mask_id) ? 4u : 0u;
+  f |= (i + 3 < L && v.w == mask_id) ? 8u : 0u;
+  return f;
+}
+
+__device__ __forceinline__ int block_sum(int v, int* red) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  if (lane == 0) red[warp] = v;
+  __syncthreads();
+  int t = 0;
+#pragma unroll
+  for (int w = 0; w < kThreads / 32; ++w) t += red[w];
+  __syncthreads();
+  return t;
+}
+
+__global__ void __launch_bounds__(kThreads) k1_count(const int32_t* __restrict__ x, int64_t L,
+                                                     int32_t mask_id, int32_t* __restrict__ counts) {
+  __shared__ int red[kThreads / 32];
+  const int64_t base = static_cast<int64_t>(blockIdx.x) * kTile;
+  int c = 0;
+#pragma unroll
+  for (int r = 0; r < kRounds; ++r) {
+    const int64_t i = base + r * (kThreads * 4) + threadIdx.x * 4;
+    c += __popc(flags4(load4(x, i, L), i, L, mask_id));
+  }
+  c = block_sum(c, red);
+  if (threadIdx.x == 0) counts[blockIdx.x] = c;
+}
+
+__global__ void __launch_bounds__(kThreads) k1_write(const int32_t* __restrict__ x, int64_t L,
+                                                     int32_t mask_id,
+                                                     const int32_t* __restrict__ counts,
+                                                     int32_t* __restrict__ idx_out,
+                                                     int32_t* __restrict__ m_out) {
+  __shared__ int red[kThreads / 32];
+  __shared__ int warp_excl[kThreads / 32 + 1];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  // prefix over the tiles before this one (fixed order -> deterministic)
+  int before = 0;
+  for (int j = threadIdx.x; j < static_cast<int>(blockIdx.x); j += kThreads) before += counts[j];
+  int offset = block_sum(before, red);
+
+  const int64_t base = static_cast<int64_t>(blockIdx.x) * kTile;
+#pragma unroll 1
+  for (int r = 0; r < kRounds; ++r) {
+    const int64_t i = base + r * (kThreads * 4) + threadIdx.x * 4;
+    const uint32_t f = flags4(load4(x, i, L), i, L, mask_id);
+    const int c = __popc(f);
+    int incl = c;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int n = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += n;
+    }
+    if (lane == 31) red[warp] = incl;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      int acc = 0;
+      for (int w = 0; w < kThreads / 32; ++w) {
+        warp_excl[w] = acc;
+        acc += red[w];
+      }
+      warp_excl[kThreads / 32] = acc;
+    }
+    __syncthreads();
+    int pos = offset + warp_excl[warp] + incl - c;
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+      if (f & (1u << j)) idx_out[pos++] = static_cast<int32_t>(i + j);
+    offset += warp_excl[kThreads / 32];
+    __syncthreads();
+  }
+  if (blockIdx.x == gridDim.x - 1 && threadIdx.x == 0) *m_out = offset;
+}
+
+// One warp per masked row; 16-byte vectors, UNROLL loads in flight per lane.
+template <int UNROLL>
+__global__ void __launch_bounds__(256) k2_gather(const int4* __restrict__ H, int64_t n_rows,
+                                                 int64_t ld_vec, int64_t d_vec,
+                                                 const int32_t* __restrict__ idx,
+                                                 const int32_t* __restrict__ m_dev, int64_t m_host,
+                                                 int64_t m_cap, int32_t shift,
+                                                 int4* __restrict__ Hc) {
+  const int64_t M = min(static_cast<int64_t>(load_count(m_dev, m_host)), m_cap);
+  const int lane = threadIdx.x & 31;
+  const int64_t warps = static_cast<int64_t>(gridDim.x) * (blockDim.x >> 5);
+  for (int64_t r = static_cast<int64_t>(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5);
+       r < M; r += warps) {
+    int64_t p = __ldg(idx + r);
+    if (shift) p = p > 0 ? p - 1 : 0;
+    if (p >= n_rows) p = n_rows - 1;  // validated on the host; clamp keeps the read in bounds
+    const int4* src = H + p * ld_vec;
+    int4* dst = Hc + r * d_vec;
+    int64_t c = lane;
+    for (; c + (UNROLL - 1) * 32 < d_vec; c += UNROLL * 32) {
+      int4 v[UNROLL];
+#pragma unroll
+      for (int u = 0; u < UNROLL; ++u) v[u] = __ldg(src + c + u * 32);
+#pragma unroll
+      for (int u = 0; u < UNROLL; ++u) dst[c + u * 32] = v[u];
+    }
+    for (; c < d_vec; c += 32) dst[c] = __ldg(src + c);
+  }
+}
+
+}  // namespace
+}  // namespace mosaic
+
+using namespace mosaic;
+
+extern "C" size_t mosaic_mask_compact_scratch_bytes(int64_t L) {
+  const int64_t tiles = L > 0 ? ceil_div(L, kTile) : 1;
+  return static_cast<size_t>(tiles) * sizeof(int32_t);
+}
+
+extern "C" int mosaic_mask_compact(const int32_t* x, int64_t L, int32_t mask_id, int32_t* idx_out,
+                                   int32_t* m_out, void* scratch, void* stream) {
+  MOSAIC_REQUIRE(L >= 0 && L < (int64_t(1) << 31), "sequence length %lld out of range",
+                 (long long)L);
+  MOSAIC_REQUIRE(m_out != nullptr && scratch != nullptr, "m_out and scratch are required");
+  MOSAIC_REQUIRE(L == 0 || (x != nullptr && idx_out != nullptr), "null x/idx_out");
+  cudaStream_t s = as_stream(stream);
+  if (L == 0) {
+    MOSAIC_CUDA(cudaMemsetAsync(m_out, 0, sizeof(int32_t), s));
+    return MOSAIC_OK;
+  }
+  const int tiles = static_cast<int>(ceil_div(L, kTile));
+  int32_t* counts = static_cast<int32_t*>(scratch);
+  k1_count<<<tiles, kThreads, 0, s>>>(x, L, mask_id, counts);
+  k1_write<<<tiles, kThreads, 0, s>>>(x, L, mask_id, counts, idx_out, m_out);
+  return check_launch("mosaic_mask_compact");
+}
+
+extern "C" int mosaic_gather_rows(const uint16_t* H, int64_t n_rows, int64_t ld_h, int64_t d,
+                                  const int32_t* idx, const int32_t* m_dev, int64_t m_host,
+                                  int64_t m_cap, int32_t shift, uint16_t* Hc, void* stream) {
+  MOSAIC_REQUIRE(d > 0 && d % 8 == 0, "d=%lld must be a positive multiple of 8", (long long)d);
+  MOSAIC_REQUIRE(ld_h >= d && ld_h % 8 == 0, "ld_h=%lld must be >= d and a multiple of 8",
+                 (long long)ld_h);
+  MOSAIC_REQUIRE(n_rows > 0, "hidden has no rows");
+  MOSAIC_REQUIRE((reinterpret_cast<uintptr_t>(H) & 15) == 0 && (reinterpret_cast<uintptr_t>(Hc) & 15) == 0,
+                 "H and Hc must be 16-byte aligned");
+  MOSAIC_REQUIRE(m_dev != nullptr || (m_host >= 0 && m_host <= m_cap), "m_host=%lld > m_cap=%lld",
+                 (long long)m_host, (long long)m_cap);
+  if (m_cap == 0) return MOSAIC_OK;
+  const int64_t rows_per_block = 8;
+  const int64_t want = ceil_div(m_cap, rows_per_block);
+  const int grid = static_cast<int>(want < num_sms() * 16 ? want : num_sms() * 16);
+  k2_gather<4><<<grid, 256, 0, as_stream(stream)>>>(
+      reinterpret_cast<const int4*>(H), n_rows, ld_h / 8, d / 8, idx, m_dev, m_host, m_cap, shift,
+      reinterpret_cast<int4*>(Hc));
+  return check_launch("mosaic_gather_rows");
+}

@@ -1,0 +1,403 @@
+// K3: mask-only LM head as a persistent, warp-specialised tcgen05 GEMM whose
+// epilogue folds each 128x256 FP32 accumulator tile into per-row online
+// softmax statistics (max, sum-exp, argmax) and never writes the logits.
+//
+// Reference counterpart: gather_gemm (mosaic/kernel.py:62-86) computes
+// logits[i, :] = H[mask_idx[i], :] @ W and materialises [m, V] (:68); the
+// `sample` op that consumes them is memory-only (mosaic/workload.py:306-308).
+// Here the gathered rows Hc (K2) and the vocab shard W [V, d] (K-major) stream
+// through TMA into a 4-stage shared-memory ring, one elected thread issues
+// tcgen05.mma (M=128, N=256, K=16, BF16 -> FP32 in TMEM), and four epilogue
+// warps drain a double-buffered TMEM accumulator with tcgen05.ld while the next
+// tile's MMAs run.
+//
+// Work decomposition: the vocab tiles (256 columns) are cut into n_splits
+// contiguous splits; a work unit is (m-block of 128 rows, split). Each CTA loops
+// over units u = blockIdx.x, blockIdx.x + gridDim.x, ... and keeps the per-row
+// statistics of the current unit in registers across the split's tiles, so the
+// only global output is one (max, sum, arg) triple per row and split. Units are
+// numbered m-fastest inside groups of `group_m` m-blocks, so the ~148 units in
+// flight at once share a handful of W tiles and m-blocks through L2.
+#include "common.cuh"
+
+namespace mosaic {
+namespace {
+
+constexpr int BM = 128;          // rows per tile (UMMA M)
+constexpr int BN = 256;          // vocab columns per tile (UMMA N)
+constexpr int BK = 64;           // K per stage: one 128-byte swizzle atom of bf16
+constexpr int UK = 16;           // K per tcgen05.mma (kind::f16)
+constexpr int STAGES = 4;
+constexpr int A_BYTES = BM * BK * 2;
+constexpr int B_BYTES = BN * BK * 2;
+constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+constexpr int NUM_ACC = 2;       // TMEM accumulator double buffer
+constexpr int TMEM_COLS = 512;   // 2 x 256 fp32 columns
+constexpr int kThreads = 192;    // warp0 TMA, warp1 MMA+TMEM, warps 2..5 epilogue
+constexpr int kEpiThreads = 128;
+constexpr uint32_t kIdesc = umma_idesc_bf16(BM, BN);
+constexpr int kSmemBytes = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
+constexpr int kMaxSplits = 64;
+constexpr float kLog2e = 1.4426950408889634f;
+
+struct Params {
+  const int32_t* m_dev;
+  int64_t m_host;
+  int64_t m_cap;
+  int64_t V;
+  int32_t K;
+  int32_t n_tiles;
+  int32_t tiles_per_split;
+  int32_t n_splits;
+  int32_t group_m;
+  int64_t v_offset;
+  float* part_max;
+  float* part_sum;
+  int32_t* part_arg;
+  float* out;   // logits (debug path)
+  int64_t ldo;
+};
+
+__device__ __forceinline__ void unit_coords(const Params& p, int m_blocks, int64_t u, int& mb,
+                                            int& s) {
+  const int64_t per_group = static_cast<int64_t>(p.group_m) * p.n_splits;
+  const int64_t g = u / per_group;
+  const int64_t rem = u - g * per_group;
+  const int64_t gm = min(static_cast<int64_t>(p.group_m), m_blocks - g * p.group_m);
+  s = static_cast<int>(rem / gm);
+  mb = static_cast<int>(g * p.group_m + rem % gm);
+}
+
+__device__ __forceinline__ float fast_exp2(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
+// 32 lanes x 32 consecutive fp32 columns of this warp's TMEM lane quarter.
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, float (&v)[32]) {
+  uint32_t r[32];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
+      "{%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, %15, "
+      "%16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31}, [%32];\n\t"
+      "tcgen05.wait::ld.sync.aligned;"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+        "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),
+        "=r"(r[14]), "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]),
+        "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]),
+        "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+      : "r"(taddr)
+      : "memory");
+#pragma unroll
+  for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
+}
+
+template <bool kStoreLogits>
+__global__ void __launch_bounds__(kThreads, 1)
+    k3_lmhead(const __grid_constant__ CUtensorMap tmap_a, const __grid_constant__ CUtensorMap tmap_b,
+              const Params p) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~static_cast<uintptr_t>(1023));
+  uint8_t* sA = smem;
+  uint8_t* sB = smem + STAGES * A_BYTES;
+  uint64_t* full = reinterpret_cast<uint64_t*>(sB + STAGES * B_BYTES);
+  uint64_t* empty = full + STAGES;
+  uint64_t* tfull = empty + STAGES;
+  uint64_t* tempty = tfull + NUM_ACC;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + NUM_ACC);
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const int64_t M = min(static_cast<int64_t>(load_count(p.m_dev, p.m_host)), p.m_cap);
+  const int m_blocks = static_cast<int>((M + BM - 1) / BM);
+  const int64_t units = static_cast<int64_t>(m_blocks) * p.n_splits;
+  const int k_blocks = p.K / BK;
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&tmap_a);
+    tma_prefetch_desc(&tmap_b);
+    for (int i = 0; i < STAGES; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&empty[i], 1);
+    }
+    for (int i = 0; i < NUM_ACC; ++i) {
+      mbar_init(&tfull[i], 1);
+      mbar_init(&tempty[i], kEpiThreads);
+    }
+    fence_mbar_init();
+  }
+  if (warp == 1) tmem_alloc(tmem_slot, TMEM_COLS);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0) {
+    // ------------------------------------------------------------ TMA producer
+    if (lane == 0) {
+      const uint64_t pol_a = policy_evict_last();    // re-read for every tile of the unit
+      const uint64_t pol_b = policy_evict_normal();  // shared by the m-blocks in flight
+      uint32_t stage = 0, phase = 0;
+      for (int64_t u = blockIdx.x; u < units; u += gridDim.x) {
+        int mb, s;
+        unit_coords(p, m_blocks, u, mb, s);
+        const int t0 = s * p.tiles_per_split;
+        const int t1 = min(t0 + p.tiles_per_split, p.n_tiles);
+        for (int t = t0; t < t1; ++t) {
+          for (int kb = 0; kb < k_blocks; ++kb) {
+            mbar_wait(&empty[stage], phase ^ 1);
+            mbar_arrive_expect_tx(&full[stage], STAGE_BYTES);
+            tma_load_2d(sA + stage * A_BYTES, &tmap_a, &full[stage], kb * BK, mb * BM, pol_a);
+            tma_load_2d(sB + stage * B_BYTES, &tmap_b, &full[stage], kb * BK, t * BN, pol_b);
+            if (++stage == STAGES) {
+              stage = 0;
+              phase ^= 1;
+            }
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ------------------------------------------------------------ MMA issuer
+    if (lane == 0) {
+      uint32_t stage = 0, phase = 0, acc = 0, acc_phase = 0;
+      for (int64_t u = blockIdx.x; u < units; u += gridDim.x) {
+        int mb, s;
+        unit_coords(p, m_blocks, u, mb, s);
+        const int t0 = s * p.tiles_per_split;
+        const int t1 = min(t0 + p.tiles_per_split, p.n_tiles);
+        for (int t = t0; t < t1; ++t) {
+          mbar_wait(&tempty[acc], acc_phase ^ 1);
+          tc_fence_after();
+          const uint32_t d_tmem = tmem_base + acc * BN;
+          for (int kb = 0; kb < k_blocks; ++kb) {
+            mbar_wait(&full[stage], phase);
+            tc_fence_after();
+            const uint32_t a0 = smem_u32(sA + stage * A_BYTES);
+            const uint32_t b0 = smem_u32(sB + stage * B_BYTES);
+#pragma unroll
+            for (int kk = 0; kk < BK / UK; ++kk)
+              umma_bf16(d_tmem, umma_desc_sw128(a0 + kk * UK * 2), umma_desc_sw128(b0 + kk * UK * 2),
+                        kIdesc, (kb | kk) != 0);
+            umma_commit(&empty[stage]);  // frees the smem slot when these MMAs retire
+            if (++stage == STAGES) {
+              stage = 0;
+              phase ^= 1;
+            }
+          }
+          umma_commit(&tfull[acc]);  // accumulator ready for the epilogue
+          if (++acc == NUM_ACC) {
+            acc = 0;
+            acc_phase ^= 1;
+          }
+        }
+      }
+    }
+  } else {
+    // ------------------------------------------------------------ epilogue
+    const int q = warp & 3;  // TMEM lane quarter accessible to this warp
+    const int row_local = q * 32 + lane;
+    uint32_t acc = 0, acc_phase = 0;
+    for (int64_t u = blockIdx.x; u < units; u += gridDim.x) {
+      int mb, s;
+      unit_coords(p, m_blocks, u, mb, s);
+      const int t0 = s * p.tiles_per_split;
+      const int t1 = min(t0 + p.tiles_per_split, p.n_tiles);
+      const int64_t row = static_cast<int64_t>(mb) * BM + row_local;
+      float run_max = -INFINITY, run_sum = 0.f;
+      int64_t run_arg = 0;
+      for (int t = t0; t < t1; ++t) {
+        mbar_wait(&tfull[acc], acc_phase);
+        tc_fence_after();
+        const uint32_t taddr = tmem_base + (static_cast<uint32_t>(q * 32) << 16) + acc * BN;
+        const int64_t col_base = static_cast<int64_t>(t) * BN;
+#pragma unroll 1
+        for (int c = 0; c < BN / 32; ++c) {
+          const int64_t col0 = col_base + c * 32;
+          if (col0 >= p.V) break;  // warp-uniform: vocab tail
+          float v[32];
+          tmem_ld32(taddr + c * 32, v);
+          if constexpr (kStoreLogits) {
+            if (row < M) {
+              float* dst = p.out + row * p.ldo + col0;
+#pragma unroll
+              for (int j = 0; j < 32; ++j)
+                if (col0 + j < p.V) dst[j] = v[j];
+            }
+          } else {
+            if (col0 + 32 > p.V) {
+#pragma unroll
+              for (int j = 0; j < 32; ++j)
+                if (col0 + j >= p.V) v[j] = -INFINITY;
+            }
+            float cmax = v[0];
+#pragma unroll
+            for (int j = 1; j < 32; ++j) cmax = fmaxf(cmax, v[j]);
+            if (cmax > run_max) {  // strict: earlier columns win ties
+              int jf = 31;
+#pragma unroll
+              for (int j = 31; j >= 0; --j)
+                if (v[j] == cmax) jf = j;
+              run_sum *= fast_exp2((run_max - cmax) * kLog2e);
+              run_max = cmax;
+              run_arg = col0 + jf;
+            }
+            const float mb2 = run_max * kLog2e;
+            float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
+#pragma unroll
+            for (int j = 0; j < 32; j += 4) {
+              s0 += fast_exp2(fmaf(v[j + 0], kLog2e, -mb2));
+              s1 += fast_exp2(fmaf(v[j + 1], kLog2e, -mb2));
+              s2 += fast_exp2(fmaf(v[j + 2], kLog2e, -mb2));
+              s3 += fast_exp2(fmaf(v[j + 3], kLog2e, -mb2));
+            }
+            run_sum += (s0 + s1) + (s2 + s3);
+          }
+        }
+        tc_fence_before();
+        mbar_arrive(&tempty[acc]);
+        if (++acc == NUM_ACC) {
+          acc = 0;
+          acc_phase ^= 1;
+        }
+      }
+      if constexpr (!kStoreLogits) {
+        if (row < M) {
+          const int64_t o = static_cast<int64_t>(s) * p.m_cap + row;
+          p.part_max[o] = run_max;
+          p.part_sum[o] = run_sum;
+          p.part_arg[o] = static_cast<int32_t>(p.v_offset + run_arg);
+        }
+      }
+    }
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc(tmem_base, TMEM_COLS);
+  }
+}
+
+using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                   const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                   const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                   CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+int encode_kmajor_bf16(CUtensorMap* map, const void* base, int64_t rows, int64_t K, int box_rows) {
+  static EncodeTiledFn fn = reinterpret_cast<EncodeTiledFn>(driver_fn("cuTensorMapEncodeTiled"));
+  if (!fn) return fail(MOSAIC_E_CUDA, "cuTensorMapEncodeTiled unavailable from the driver");
+  const cuuint64_t dims[2] = {static_cast<cuuint64_t>(K), static_cast<cuuint64_t>(rows)};
+  const cuuint64_t strides[1] = {static_cast<cuuint64_t>(K) * 2};
+  const cuuint32_t box[2] = {BK, static_cast<cuuint32_t>(box_rows)};
+  const cuuint32_t elem_strides[2] = {1, 1};
+  CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides,
+                  box, elem_strides, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(MOSAIC_E_CUDA, "cuTensorMapEncodeTiled failed (%d)", int(r));
+  return MOSAIC_OK;
+}
+
+void plan_splits(int64_t m_cap, int64_t V, int32_t* n_splits, int32_t* tps) {
+  const int64_t n_tiles = ceil_div(V, BN);
+  const int64_t m_blocks = ceil_div(m_cap > 0 ? m_cap : 1, BM);
+  const int64_t sms = num_sms();
+  int64_t best_cost = INT64_MAX, best_tps = n_tiles;
+  for (int64_t t = n_tiles; t >= 1; --t) {
+    const int64_t S = ceil_div(n_tiles, t);
+    if (S > kMaxSplits) break;
+    if (ceil_div(n_tiles, S) != t) continue;  // same split count as a larger t
+    const int64_t units = m_blocks * S;
+    const int64_t cost = ceil_div(units, sms) * t;  // tiles on the busiest CTA
+    if (cost < best_cost) {
+      best_cost = cost;
+      best_tps = t;
+    }
+  }
+  *tps = static_cast<int32_t>(best_tps);
+  *n_splits = static_cast<int32_t>(ceil_div(n_tiles, best_tps));
+}
+
+template <bool kStore>
+int launch(const uint16_t* Hc, int64_t m_cap, const int32_t* m_dev, int64_t m_host,
+           const uint16_t* W, int64_t V, int64_t d, Params p, void* stream) {
+  MOSAIC_REQUIRE(d > 0 && d % BK == 0, "d=%lld must be a positive multiple of %d", (long long)d, BK);
+  MOSAIC_REQUIRE(V >= 1 && V < (int64_t(1) << 31), "vocab shard %lld out of range", (long long)V);
+  MOSAIC_REQUIRE(m_cap >= 0 && m_cap < (int64_t(1) << 31), "m_cap out of range");
+  MOSAIC_REQUIRE(m_dev != nullptr || (m_host >= 0 && m_host <= m_cap), "m_host=%lld > m_cap=%lld",
+                 (long long)m_host, (long long)m_cap);
+  MOSAIC_REQUIRE((reinterpret_cast<uintptr_t>(Hc) & 15) == 0 && (reinterpret_cast<uintptr_t>(W) & 15) == 0,
+                 "Hc and W must be 16-byte aligned");
+  if (m_cap == 0) return MOSAIC_OK;
+  CUtensorMap ta, tb;
+  int st = encode_kmajor_bf16(&ta, Hc, m_cap, d, BM);
+  if (st) return st;
+  st = encode_kmajor_bf16(&tb, W, V, d, BN);
+  if (st) return st;
+  p.m_dev = m_dev;
+  p.m_host = m_host;
+  p.m_cap = m_cap;
+  p.V = V;
+  p.K = static_cast<int32_t>(d);
+  p.n_tiles = static_cast<int32_t>(ceil_div(V, BN));
+  if (p.group_m <= 0) p.group_m = 16;
+  auto kern = k3_lmhead<kStore>;
+  static bool attr_set = false;  // per template instantiation
+  if (!attr_set) {
+    MOSAIC_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes));
+    attr_set = true;
+  }
+  const int64_t units_cap = ceil_div(m_cap, BM) * p.n_splits;
+  const int grid = static_cast<int>(units_cap < num_sms() ? units_cap : num_sms());
+  kern<<<grid, kThreads, kSmemBytes, as_stream(stream)>>>(ta, tb, p);
+  return check_launch(kStore ? "mosaic_lmhead_logits" : "mosaic_lmhead_stats");
+}
+
+}  // namespace
+}  // namespace mosaic
+
+using namespace mosaic;
+
+extern "C" int mosaic_lmhead_plan(int64_t m_cap, int64_t V_shard, int64_t d, int32_t* n_splits_out,
+                                  int32_t* tiles_per_split_out) {
+  MOSAIC_REQUIRE(V_shard >= 1 && d >= 1, "empty shard");
+  MOSAIC_REQUIRE(n_splits_out && tiles_per_split_out, "null outputs");
+  plan_splits(m_cap, V_shard, n_splits_out, tiles_per_split_out);
+  return MOSAIC_OK;
+}
+
+extern "C" int mosaic_lmhead_stats(const uint16_t* Hc, int64_t m_cap, const int32_t* m_dev,
+                                   int64_t m_host, const uint16_t* W, int64_t V_shard, int64_t d,
+                                   int64_t v_offset, int32_t n_splits, float* part_max,
+                                   float* part_sum, int32_t* part_arg, void* stream) {
+  MOSAIC_REQUIRE(part_max && part_sum && part_arg, "null partial buffers");
+  const int64_t n_tiles = ceil_div(V_shard, BN);
+  MOSAIC_REQUIRE(n_splits >= 1 && n_splits <= n_tiles, "n_splits=%d not in [1, %lld]", n_splits,
+                 (long long)n_tiles);
+  Params p{};
+  p.tiles_per_split = static_cast<int32_t>(ceil_div(n_tiles, n_splits));
+  p.n_splits = static_cast<int32_t>(ceil_div(n_tiles, p.tiles_per_split));
+  MOSAIC_REQUIRE(p.n_splits == n_splits, "n_splits=%d does not tile %lld vocab tiles evenly; use mosaic_lmhead_plan",
+                 n_splits, (long long)n_tiles);
+  p.v_offset = v_offset;
+  p.part_max = part_max;
+  p.part_sum = part_sum;
+  p.part_arg = part_arg;
+  return launch<false>(Hc, m_cap, m_dev, m_host, W, V_shard, d, p, stream);
+}
+
+extern "C" int mosaic_lmhead_logits(const uint16_t* Hc, int64_t m_cap, const int32_t* m_dev,
+                                    int64_t m_host, const uint16_t* W, int64_t V_shard, int64_t d,
+                                    float* out, int64_t ldo, void* stream) {
+  MOSAIC_REQUIRE(out != nullptr && ldo >= V_shard, "bad logits output");
+  Params p{};
+  const int64_t n_tiles = ceil_div(V_shard, BN);
+  p.tiles_per_split = static_cast<int32_t>(n_tiles);
+  p.n_splits = 1;
+  p.out = out;
+  p.ldo = ldo;
+  return launch<true>(Hc, m_cap, m_dev, m_host, W, V_shard, d, p, stream);
+}

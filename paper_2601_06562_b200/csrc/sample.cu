@@ -1,0 +1,191 @@
+// K4 split/rank merge of the softmax-statistics triples, and K5 the
+// low-confidence remasking commit.
+//
+// Both realise ops that are memory-only in the reference template: `sample`
+// writes token_out/confidence [rows] (mosaic/workload.py:281-285,306-308) and
+// `commit` consumes them (mosaic/workload.py:315), with the per-step unmask
+// count coming from ScenarioConfig.masked_at (mosaic/workload.py:140-146).
+//
+// Merge rule (associative, applied in fixed ascending order so every rank and
+// every run produces the same bits):
+//   (m1,S1,a1) + (m2,S2,a2) = (max, S1 e^(m1-max) + S2 e^(m2-max),
+//                              a of the larger m, lower index on equal m).
+// Remask rule: keep the k masked rows with the highest confidence, ties broken
+// towards the lower sequence position. Implemented as an exact radix select on
+// the 64-bit key (conf bits << 32 | ~pos), unique per row, 8 passes of 8 bits.
+#include <cfloat>
+
+#include "common.cuh"
+
+namespace mosaic {
+namespace {
+
+__global__ void k4_merge(const float* __restrict__ in_max, const float* __restrict__ in_sum,
+                         const int32_t* __restrict__ in_arg, int32_t S, int64_t stride,
+                         const int32_t* __restrict__ m_dev, int64_t m_host, int64_t m_cap,
+                         float* __restrict__ out_max, float* __restrict__ out_sum,
+                         int32_t* __restrict__ out_arg, int32_t* __restrict__ token,
+                         float* __restrict__ lse, float* __restrict__ conf) {
+  const int64_t M = min(static_cast<int64_t>(load_count(m_dev, m_host)), m_cap);
+  for (int64_t r = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; r < M;
+       r += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    float m = -INFINITY, sum = 0.f;
+    int32_t arg = INT32_MAX;
+    for (int s = 0; s < S; ++s) {
+      const int64_t o = s * stride + r;
+      const float mi = in_max[o], si = in_sum[o];
+      const int32_t ai = in_arg[o];
+      if (mi > m) {
+        sum = sum * expf(m - mi) + si;
+        m = mi;
+        arg = ai;
+      } else if (mi == m) {
+        sum += si;
+        arg = min(arg, ai);
+      } else {
+        sum += si * expf(mi - m);
+      }
+    }
+    if (out_max) out_max[r] = m;
+    if (out_sum) out_sum[r] = sum;
+    if (out_arg) out_arg[r] = arg;
+    if (token) token[r] = arg;
+    if (lse) lse[r] = m + logf(sum);
+    if (conf) conf[r] = 1.f / sum;
+  }
+}
+
+struct SelectState {
+  unsigned long long prefix;
+  uint32_t k_rem;
+  uint32_t active;
+  uint32_t hist[256];
+};
+
+__device__ __forceinline__ unsigned long long remask_key(float c, int32_t pos) {
+  return (static_cast<unsigned long long>(__float_as_uint(c)) << 32) |
+         static_cast<unsigned long long>(~static_cast<uint32_t>(pos));
+}
+
+__global__ void k5_init(SelectState* st, const int32_t* __restrict__ m_dev, int64_t m_host,
+                        int64_t m_cap, int64_t k) {
+  const int64_t M = min(static_cast<int64_t>(load_count(m_dev, m_host)), m_cap);
+  const int64_t kk = k < M ? k : M;
+  if (threadIdx.x == 0) {
+    st->prefix = 0ull;
+    st->k_rem = static_cast<uint32_t>(kk > 0 ? kk : 0);
+    st->active = kk > 0 ? 1u : 0u;
+  }
+  st->hist[threadIdx.x] = 0u;
+}
+
+__global__ void __launch_bounds__(256) k5_hist(const float* __restrict__ conf,
+                                               const int32_t* __restrict__ pos,
+                                               const int32_t* __restrict__ m_dev, int64_t m_host,
+                                               int64_t m_cap, int pass, SelectState* st) {
+  __shared__ uint32_t h[256];
+  if (st->k_rem == 0) return;  // uniform across the grid
+  h[threadIdx.x] = 0u;
+  __syncthreads();
+  const int64_t M = min(static_cast<int64_t>(load_count(m_dev, m_host)), m_cap);
+  const unsigned long long prefix = st->prefix;
+  const int hi_shift = 64 - 8 * pass;  // bits already fixed: [hi_shift, 64)
+  const int lo_shift = 56 - 8 * pass;
+  for (int64_t r = blockIdx.x * 256ll + threadIdx.x; r < M; r += gridDim.x * 256ll) {
+    const unsigned long long key = remask_key(conf[r], pos[r]);
+    if (pass == 0 || (key >> hi_shift) == (prefix >> hi_shift))
+      atomicAdd(&h[(key >> lo_shift) & 255u], 1u);
+  }
+  __syncthreads();
+  if (h[threadIdx.x]) atomicAdd(&st->hist[threadIdx.x], h[threadIdx.x]);
+}
+
+__global__ void __launch_bounds__(256) k5_pick(SelectState* st, int pass) {
+  __shared__ uint32_t cum[256];
+  const int t = threadIdx.x;
+  const uint32_t k_rem = st->k_rem;
+  const uint32_t cnt = st->hist[255 - t];  // descending digit order
+  cum[t] = cnt;
+  __syncthreads();
+  for (int o = 1; o < 256; o <<= 1) {
+    const uint32_t add = t >= o ? cum[t - o] : 0u;
+    __syncthreads();
+    cum[t] += add;
+    __syncthreads();
+  }
+  if (k_rem > 0) {
+    const uint32_t incl = cum[t], above = incl - cnt;
+    if (above < k_rem && incl >= k_rem) {
+      st->prefix |= static_cast<unsigned long long>(255 - t) << (56 - 8 * pass);
+      st->k_rem = k_rem - above;
+    }
+  }
+  st->hist[255 - t] = 0u;
+}
+
+__global__ void __launch_bounds__(256) k5_commit(const float* __restrict__ conf,
+                                                 const int32_t* __restrict__ pos,
+                                                 const int32_t* __restrict__ token,
+                                                 const int32_t* __restrict__ m_dev, int64_t m_host,
+                                                 int64_t m_cap, const SelectState* st,
+                                                 int32_t* __restrict__ x,
+                                                 int32_t* __restrict__ selected) {
+  const int64_t M = min(static_cast<int64_t>(load_count(m_dev, m_host)), m_cap);
+  const bool active = st->active != 0u;
+  const unsigned long long thr = st->prefix;
+  for (int64_t r = blockIdx.x * 256ll + threadIdx.x; r < M; r += gridDim.x * 256ll) {
+    const int32_t p = pos[r];
+    const bool sel = active && remask_key(conf[r], p) >= thr;
+    if (sel) x[p] = token[r];
+    if (selected) selected[r] = sel ? 1 : 0;
+  }
+}
+
+int grid_for(int64_t n, int per_block) {
+  const int64_t want = ceil_div(n > 0 ? n : 1, per_block);
+  const int64_t cap = static_cast<int64_t>(num_sms()) * 8;
+  return static_cast<int>(want < cap ? want : cap);
+}
+
+}  // namespace
+}  // namespace mosaic
+
+using namespace mosaic;
+
+extern "C" int mosaic_stats_merge(const float* in_max, const float* in_sum, const int32_t* in_arg,
+                                  int32_t S, int64_t stride, const int32_t* m_dev, int64_t m_host,
+                                  int64_t m_cap, float* out_max, float* out_sum, int32_t* out_arg,
+                                  int32_t* token, float* lse, float* conf, void* stream) {
+  MOSAIC_REQUIRE(S >= 1, "need at least one partial, got S=%d", S);
+  MOSAIC_REQUIRE(stride >= m_cap, "partial stride %lld < m_cap %lld", (long long)stride,
+                 (long long)m_cap);
+  MOSAIC_REQUIRE(in_max && in_sum && in_arg, "null partial inputs");
+  MOSAIC_REQUIRE(m_dev != nullptr || (m_host >= 0 && m_host <= m_cap), "m_host > m_cap");
+  if (m_cap == 0) return MOSAIC_OK;
+  k4_merge<<<grid_for(m_cap, 256), 256, 0, as_stream(stream)>>>(
+      in_max, in_sum, in_arg, S, stride, m_dev, m_host, m_cap, out_max, out_sum, out_arg, token,
+      lse, conf);
+  return check_launch("mosaic_stats_merge");
+}
+
+extern "C" size_t mosaic_remask_scratch_bytes(void) { return sizeof(SelectState); }
+
+extern "C" int mosaic_remask_commit(const float* conf, const int32_t* pos, const int32_t* token,
+                                    const int32_t* m_dev, int64_t m_host, int64_t m_cap, int64_t k,
+                                    int32_t* x, int32_t* selected, void* scratch, void* stream) {
+  MOSAIC_REQUIRE(k >= 0, "negative unmask count %lld", (long long)k);
+  MOSAIC_REQUIRE(scratch != nullptr, "scratch required");
+  MOSAIC_REQUIRE(m_dev != nullptr || (m_host >= 0 && m_host <= m_cap), "m_host > m_cap");
+  if (m_cap == 0) return MOSAIC_OK;
+  MOSAIC_REQUIRE(conf && pos && token && x, "null inputs");
+  cudaStream_t s = as_stream(stream);
+  SelectState* st = static_cast<SelectState*>(scratch);
+  const int grid = grid_for(m_cap, 256);
+  k5_init<<<1, 256, 0, s>>>(st, m_dev, m_host, m_cap, k);
+  for (int pass = 0; pass < 8; ++pass) {
+    k5_hist<<<grid, 256, 0, s>>>(conf, pos, m_dev, m_host, m_cap, pass, st);
+    k5_pick<<<1, 256, 0, s>>>(st, pass);
+  }
+  k5_commit<<<grid, 256, 0, s>>>(conf, pos, token, m_dev, m_host, m_cap, st, x, selected);
+  return check_launch("mosaic_remask_commit");
+}

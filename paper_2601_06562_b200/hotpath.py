@@ -1,0 +1,257 @@
+"""Device-side hot path: torch-tensor wrappers over the C ABI and the fused
+mask-only logits + remask step.
+
+Each wrapper enqueues on the current torch CUDA stream (or an explicit one)
+and takes caller-owned output buffers, so a whole denoising step can run out
+of one preplanned workspace. Reference anchors:
+
+* K1 ``mask_compact``   — mask_idx graph input, mosaic/workload.py:199-200
+* K2 ``gather_rows``    — indirect row fetch, mosaic/kernel.py:77
+* K3 ``lmhead_stats``   — gather_gemm, mosaic/kernel.py:62-86 (fused, no [M,V])
+* K4 ``stats_merge``    — `sample` op, mosaic/workload.py:306-308
+* K5 ``remask_commit``  — `commit` op, mosaic/workload.py:315
+"""
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass
+from typing import Optional
+
+import torch
+
+from . import _native
+from .errors import InputError
+
+ALIGN = 256
+
+
+def _p(t: Optional[torch.Tensor]):
+    return None if t is None else ctypes.c_void_p(t.data_ptr())
+
+
+def _s(stream: Optional[torch.cuda.Stream]):
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return ctypes.c_void_p(s.cuda_stream)
+
+
+def _req(t: torch.Tensor, dtype: torch.dtype, name: str, ndim: int | None = None) -> None:
+    if not isinstance(t, torch.Tensor) or not t.is_cuda:
+        raise InputError(f"{name} must be a CUDA tensor")
+    if t.dtype != dtype:
+        raise InputError(f"{name} must be {dtype}, got {t.dtype}")
+    if ndim is not None and t.dim() != ndim:
+        raise InputError(f"{name} must be {ndim}-D, got shape {tuple(t.shape)}")
+    if not t.is_contiguous():
+        raise InputError(f"{name} must be contiguous")
+
+
+# ----------------------------------------------------------------- K1 / K2
+def mask_compact_scratch_bytes(L: int) -> int:
+    return int(_native.value("mosaic_mask_compact_scratch_bytes", L))
+
+
+def mask_compact(x: torch.Tensor, mask_id: int, idx_out: torch.Tensor, m_out: torch.Tensor,
+                 scratch: torch.Tensor, stream=None) -> None:
+    _req(x, torch.int32, "x", 1)
+    _req(idx_out, torch.int32, "idx_out", 1)
+    _req(m_out, torch.int32, "m_out")
+    if idx_out.numel() < x.numel():
+        raise InputError("idx_out must hold L entries")
+    if scratch.numel() * scratch.element_size() < mask_compact_scratch_bytes(x.numel()):
+        raise InputError("compaction scratch too small")
+    _native.call("mosaic_mask_compact", _p(x), x.numel(), int(mask_id), _p(idx_out), _p(m_out),
+                 _p(scratch), _s(stream))
+
+
+def gather_rows(hidden: torch.Tensor, idx: torch.Tensor, out: torch.Tensor, m_dev=None,
+                m_host: int = 0, shift: bool = False, stream=None) -> None:
+    if hidden.dtype != torch.bfloat16 or hidden.dim() != 2 or not hidden.is_cuda:
+        raise InputError("hidden must be a 2-D bf16 CUDA tensor")
+    if hidden.stride(1) != 1:
+        raise InputError("hidden rows must be contiguous")
+    _req(out, torch.bfloat16, "out", 2)
+    _req(idx, torch.int32, "idx", 1)
+    if out.shape[1] != hidden.shape[1]:
+        raise InputError("row width mismatch")
+    _native.call("mosaic_gather_rows", _p(hidden), hidden.shape[0], hidden.stride(0), hidden.shape[1],
+                 _p(idx), _p(m_dev), int(m_host), out.shape[0], int(bool(shift)), _p(out), _s(stream))
+
+
+# ----------------------------------------------------------------- K3
+def lmhead_plan(m_cap: int, v_shard: int, d: int) -> tuple[int, int]:
+    s = ctypes.c_int32()
+    t = ctypes.c_int32()
+    _native.call("mosaic_lmhead_plan", m_cap, v_shard, d, ctypes.byref(s), ctypes.byref(t))
+    return s.value, t.value
+
+
+def lmhead_stats(hc: torch.Tensor, weight: torch.Tensor, n_splits: int, part_max: torch.Tensor,
+                 part_sum: torch.Tensor, part_arg: torch.Tensor, m_dev=None, m_host: int = 0,
+                 v_offset: int = 0, stream=None) -> None:
+    _req(hc, torch.bfloat16, "hc", 2)
+    _req(weight, torch.bfloat16, "weight", 2)
+    m_cap, d = hc.shape
+    if weight.shape[1] != d:
+        raise InputError(f"weight is {tuple(weight.shape)}, expected [V, {d}]")
+    for t, dt, n in ((part_max, torch.float32, "part_max"), (part_sum, torch.float32, "part_sum"),
+                     (part_arg, torch.int32, "part_arg")):
+        _req(t, dt, n)
+        if t.numel() < n_splits * m_cap:
+            raise InputError(f"{n} must hold n_splits*m_cap entries")
+    _native.call("mosaic_lmhead_stats", _p(hc), m_cap, _p(m_dev), int(m_host), _p(weight),
+                 weight.shape[0], d, int(v_offset), int(n_splits), _p(part_max), _p(part_sum),
+                 _p(part_arg), _s(stream))
+
+
+def lmhead_logits(hc: torch.Tensor, weight: torch.Tensor, out: torch.Tensor, m_dev=None,
+                  m_host: int = 0, stream=None) -> None:
+    _req(hc, torch.bfloat16, "hc", 2)
+    _req(weight, torch.bfloat16, "weight", 2)
+    _req(out, torch.float32, "out", 2)
+    if out.shape[0] < hc.shape[0] or out.shape[1] < weight.shape[0]:
+        raise InputError("logits output too small")
+    _native.call("mosaic_lmhead_logits", _p(hc), hc.shape[0], _p(m_dev), int(m_host), _p(weight),
+                 weight.shape[0], hc.shape[1], _p(out), out.stride(0), _s(stream))
+
+
+# ----------------------------------------------------------------- K4 / K5
+def stats_merge(in_max, in_sum, in_arg, S: int, stride: int, m_cap: int, m_dev=None, m_host: int = 0,
+                out_max=None, out_sum=None, out_arg=None, token=None, lse=None, conf=None,
+                stream=None) -> None:
+    _native.call("mosaic_stats_merge", _p(in_max), _p(in_sum), _p(in_arg), int(S), int(stride),
+                 _p(m_dev), int(m_host), int(m_cap), _p(out_max), _p(out_sum), _p(out_arg),
+                 _p(token), _p(lse), _p(conf), _s(stream))
+
+
+def remask_scratch_bytes() -> int:
+    return int(_native.value("mosaic_remask_scratch_bytes"))
+
+
+def remask_commit(conf, pos, token, k: int, x, scratch, m_cap: int, m_dev=None, m_host: int = 0,
+                  selected=None, stream=None) -> None:
+    _native.call("mosaic_remask_commit", _p(conf), _p(pos), _p(token), _p(m_dev), int(m_host),
+                 int(m_cap), int(k), _p(x), _p(selected), _p(scratch), _s(stream))
+
+
+# ----------------------------------------------------------------- buffers
+class BufferLayout:
+    """Bump layout of named buffers inside one device block (256 B aligned)."""
+
+    def __init__(self) -> None:
+        self.entries: dict[str, tuple[int, tuple[int, ...], torch.dtype]] = {}
+        self.size = 0
+
+    def add(self, name: str, shape: tuple[int, ...], dtype: torch.dtype) -> None:
+        n = 1
+        for s in shape:
+            n *= s
+        nbytes = n * torch.empty((), dtype=dtype).element_size()
+        off = (self.size + ALIGN - 1) // ALIGN * ALIGN
+        self.entries[name] = (off, tuple(shape), dtype)
+        self.size = off + max(nbytes, 1)
+
+    def views(self, block: torch.Tensor) -> dict[str, torch.Tensor]:
+        if block.dtype != torch.uint8 or block.numel() < self.size:
+            raise InputError("buffer block too small for the layout")
+        out = {}
+        for name, (off, shape, dtype) in self.entries.items():
+            n = 1
+            for s in shape:
+                n *= s
+            nbytes = n * torch.empty((), dtype=dtype).element_size()
+            out[name] = block[off:off + nbytes].view(dtype).view(shape)
+        return out
+
+
+@dataclass
+class StepOutput:
+    m_dev: torch.Tensor       # [1] int32, masked rows this step
+    idx: torch.Tensor         # [m_cap] int32 masked positions (ascending), first M valid
+    token: torch.Tensor       # [m_cap] int32 argmax token per masked row
+    lse: torch.Tensor         # [m_cap] fp32 log-sum-exp
+    conf: torch.Tensor        # [m_cap] fp32 p(token)
+    selected: torch.Tensor    # [m_cap] int32 1 = unmasked this step
+
+
+class MaskOnlyHead:
+    """The fused mask-only logits + remask step on one vocab shard.
+
+    step(x, hidden, k): compact the masked positions of ``x`` (K1), gather their
+    hidden rows (K2), run the LM-head statistics GEMM over this rank's vocab
+    shard (K3), merge the splits (K4), combine the per-row triples across the
+    vocab-sharded ranks (all-gather over NCCL + K4 in rank order), and commit the
+    k most confident predictions into ``x`` in place (K5). ``[M, V]`` logits
+    never exist. Every rank of ``group`` ends with identical ``x``.
+    """
+
+    def __init__(self, weight_shard: torch.Tensor, *, seq_len: int, mask_id: int,
+                 vocab_offset: int = 0, m_cap: Optional[int] = None, shift: bool = False,
+                 group=None, block: Optional[torch.Tensor] = None):
+        _req(weight_shard, torch.bfloat16, "weight_shard", 2)
+        self.weight = weight_shard
+        self.v_shard, self.d = weight_shard.shape
+        self.vocab_offset = int(vocab_offset)
+        self.L = int(seq_len)
+        self.m_cap = int(m_cap if m_cap is not None else seq_len)
+        self.mask_id = int(mask_id)
+        self.shift = bool(shift)
+        self.group = group
+        self.world = 1
+        if group is not None:
+            import torch.distributed as dist
+            self.world = dist.get_world_size(group)
+        self.n_splits, self.tiles_per_split = lmhead_plan(self.m_cap, self.v_shard, self.d)
+        lay = BufferLayout()
+        m, S, P = self.m_cap, self.n_splits, self.world
+        lay.add("idx", (max(self.L, m),), torch.int32)
+        lay.add("m_dev", (1,), torch.int32)
+        lay.add("compact_scratch", (mask_compact_scratch_bytes(self.L),), torch.uint8)
+        lay.add("hc", (m, self.d), torch.bfloat16)
+        lay.add("part_max", (S, m), torch.float32)
+        lay.add("part_sum", (S, m), torch.float32)
+        lay.add("part_arg", (S, m), torch.int32)
+        if P > 1:
+            lay.add("local", (3, m), torch.float32)     # merged (max, sum, arg-bits) of this shard
+            lay.add("gathered", (P, 3, m), torch.float32)
+        lay.add("token", (m,), torch.int32)
+        lay.add("lse", (m,), torch.float32)
+        lay.add("conf", (m,), torch.float32)
+        lay.add("selected", (m,), torch.int32)
+        lay.add("remask_scratch", (remask_scratch_bytes(),), torch.uint8)
+        self.layout = lay
+        if block is None:
+            block = torch.empty(lay.size, dtype=torch.uint8, device=weight_shard.device)
+        self.block = block
+        self.buf = lay.views(block)
+
+    @property
+    def workspace_bytes(self) -> int:
+        return self.layout.size
+
+    def step(self, x: torch.Tensor, hidden: torch.Tensor, k: int, stream=None) -> StepOutput:
+        b = self.buf
+        _req(x, torch.int32, "x", 1)
+        if x.numel() != self.L or hidden.shape[0] != self.L or hidden.shape[1] != self.d:
+            raise InputError("x/hidden do not match the configured sequence length / width")
+        m_dev = b["m_dev"]
+        mask_compact(x, self.mask_id, b["idx"], m_dev, b["compact_scratch"], stream)
+        gather_rows(hidden, b["idx"], b["hc"], m_dev=m_dev, shift=self.shift, stream=stream)
+        lmhead_stats(b["hc"], self.weight, self.n_splits, b["part_max"], b["part_sum"],
+                     b["part_arg"], m_dev=m_dev, v_offset=self.vocab_offset, stream=stream)
+        m, S = self.m_cap, self.n_splits
+        if self.world == 1:
+            stats_merge(b["part_max"], b["part_sum"], b["part_arg"], S, m, m, m_dev=m_dev,
+                        token=b["token"], lse=b["lse"], conf=b["conf"], stream=stream)
+        else:
+            import torch.distributed as dist
+            loc = b["local"]
+            stats_merge(b["part_max"], b["part_sum"], b["part_arg"], S, m, m, m_dev=m_dev,
+                        out_max=loc[0], out_sum=loc[1], out_arg=loc[2].view(torch.int32),
+                        stream=stream)
+            g = b["gathered"]
+            dist.all_gather_into_tensor(g.view(-1), loc.view(-1), group=self.group)
+            stats_merge(g[0, 0], g[0, 1], g[0, 2].view(torch.int32), self.world, 3 * m, m,
+                        m_dev=m_dev, token=b["token"], lse=b["lse"], conf=b["conf"], stream=stream)
+        remask_commit(b["conf"], b["idx"], b["token"], int(k), x, b["remask_scratch"], m,
+                      m_dev=m_dev, selected=b["selected"], stream=stream)
+        return StepOutput(m_dev, b["idx"][:m], b["token"], b["lse"], b["conf"], b["selected"])

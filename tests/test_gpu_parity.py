@@ -1,0 +1,299 @@
+"""GPU parity of every hot-path kernel against the CPU oracle, through the C ABI.
+
+Tolerances (north_star): indices / remask selections bit-exact; argmax tokens
+exact wherever the oracle's top-1 margin exceeds 1e-3; lse and confidence
+within 1e-3 relative (BF16 operands, FP32 accumulation). Materialised logits
+(debug path of gather_gemm) within 2e-3 absolute + 1e-3 relative of the fp64
+oracle on the same bf16-rounded operands.
+"""
+import numpy as np
+import pytest
+import torch
+
+import mosaic_oracle as orc
+from conftest import GOLDEN
+
+pytestmark = pytest.mark.gpu
+
+LSE_REL = 1e-3
+CONF_REL = 1e-3
+MARGIN = 1e-3
+
+
+@pytest.fixture(scope="module")
+def dev(native_lib):
+    return torch.device("cuda", 0)
+
+
+def bf16_tensor(a, dev):
+    return torch.from_numpy(np.asarray(a, dtype=np.float32)).to(dev).to(torch.bfloat16)
+
+
+def as_f64(t):
+    return t.float().cpu().numpy().astype(np.float64)
+
+
+# ----------------------------------------------------------------------- K1
+@pytest.mark.parametrize("L,layout", [(1, "all"), (3, "none"), (4097, "scattered"), (2048, "suffix"),
+                                      (32768, "suffix"), (32768, "scattered"), (131075, "scattered"),
+                                      (1 << 20, "scattered"), (5000, "all"), (5000, "none")])
+def test_mask_compact(dev, L, layout):
+    from paper_2601_06562_b200 import hotpath
+
+    rng = np.random.default_rng(L)
+    mask_id = 126336
+    x = rng.integers(0, 126000, size=L).astype(np.int32)
+    if layout == "all":
+        x[:] = mask_id
+    elif layout == "suffix":
+        x[L // 2:] = mask_id
+    elif layout == "scattered":
+        x[rng.random(L) < 0.37] = mask_id
+    xd = torch.from_numpy(x).to(dev)
+    idx = torch.full((L,), -7, dtype=torch.int32, device=dev)
+    m = torch.zeros(1, dtype=torch.int32, device=dev)
+    scratch = torch.empty(hotpath.mask_compact_scratch_bytes(L), dtype=torch.uint8, device=dev)
+    hotpath.mask_compact(xd, mask_id, idx, m, scratch)
+    want = orc.mask_compact(x, mask_id)
+    assert int(m.item()) == want.size
+    assert np.array_equal(idx[: want.size].cpu().numpy(), want)
+
+
+# ----------------------------------------------------------------------- K2
+@pytest.mark.parametrize("shift", [False, True])
+@pytest.mark.parametrize("n,d,m", [(17, 8, 5), (2048, 256, 1024), (4096, 4096, 1000), (300, 3584, 300)])
+def test_gather_rows_bitexact(dev, n, d, m, shift):
+    from paper_2601_06562_b200 import hotpath
+
+    g = torch.Generator().manual_seed(n + d)
+    H = torch.randn(n, d, generator=g).to(torch.bfloat16).to(dev)
+    idx_np = np.sort(np.random.default_rng(m).choice(n, size=m, replace=False)).astype(np.int32)
+    idx = torch.from_numpy(idx_np).to(dev)
+    out = torch.zeros(m + 3, d, dtype=torch.bfloat16, device=dev)
+    hotpath.gather_rows(H, idx, out, m_host=m, shift=shift)
+    src = orc.source_rows(idx_np, shift)
+    assert torch.equal(out[:m].cpu(), H.cpu()[torch.from_numpy(src)])
+    assert torch.count_nonzero(out[m:].float()) == 0
+
+
+# ----------------------------------------------------------------------- K3 (materialised, parity path)
+def test_gather_gemm_golden_cases(dev):
+    """The reference's own gather_gemm outputs (tests/golden) reproduced by the
+    GPU path within bf16 tolerance."""
+    from paper_2601_06562_b200 import GatherGemmProblem, gather_gemm
+
+    kg = np.load(GOLDEN / "kernel_golden.npz")
+    cases = sorted({k.split("_")[0] for k in kg.files if k.startswith("rand")})
+    for c in cases:
+        h, w, idx = kg[c + "_hidden"], kg[c + "_weight"], kg[c + "_idx"]
+        out, scratch = gather_gemm(GatherGemmProblem(h, w, tuple(int(i) for i in idx)))
+        ref = orc.gemm_reference(orc.bf16_round(h)[idx], orc.bf16_round(w))
+        assert out.shape == kg[c + "_out"].shape
+        assert np.allclose(out, ref, rtol=1e-5, atol=1e-4), c
+        # and against the reference's own (unrounded) result at bf16 input precision
+        assert np.allclose(out, kg[c + "_out"], rtol=2e-2, atol=0.2), c
+        assert scratch.within_bound
+    # bf16-representable case: same operands on both sides
+    out, _ = gather_gemm(GatherGemmProblem(kg["bf16case_hidden"], kg["bf16case_weight"],
+                                           tuple(int(i) for i in kg["bf16case_idx"])))
+    assert np.allclose(out, kg["bf16case_out"], rtol=1e-5, atol=1e-4)
+
+
+@pytest.mark.parametrize("m,d,V", [(1, 64, 1), (128, 64, 256), (129, 128, 257), (300, 256, 8192 + 77),
+                                   (1000, 4096, 3000), (257, 3584, 1000)])
+def test_lmhead_logits_vs_oracle(dev, m, d, V):
+    from paper_2601_06562_b200 import hotpath
+
+    rng = np.random.default_rng(m * 7 + V)
+    Hc = orc.bf16_round(rng.standard_normal((m, d)))
+    W = orc.bf16_round(rng.standard_normal((V, d)) * 0.02)
+    out = torch.full((m, V), float("nan"), dtype=torch.float32, device=dev)
+    hotpath.lmhead_logits(bf16_tensor(Hc, dev), bf16_tensor(W, dev), out, m_host=m)
+    ref = orc.logits_f64(Hc, W)
+    got = out.cpu().numpy().astype(np.float64)
+    assert np.all(np.isfinite(got))
+    assert np.allclose(got, ref, rtol=1e-3, atol=2e-3 * max(1.0, np.abs(ref).max() / 10))
+
+
+# ----------------------------------------------------------------------- K3 + K4 (fused statistics)
+def _stats_case(dev, m, d, V, seed, scale=0.02, n_splits=None, v_offset=0):
+    from paper_2601_06562_b200 import hotpath
+
+    rng = np.random.default_rng(seed)
+    Hc = orc.bf16_round(rng.standard_normal((m, d)))
+    W = orc.bf16_round(rng.standard_normal((V, d)) * scale)
+    S = n_splits or hotpath.lmhead_plan(m, V, d)[0]
+    pm = torch.empty(S, m, device=dev)
+    ps = torch.empty(S, m, device=dev)
+    pa = torch.empty(S, m, dtype=torch.int32, device=dev)
+    hotpath.lmhead_stats(bf16_tensor(Hc, dev), bf16_tensor(W, dev), S, pm, ps, pa, m_host=m,
+                         v_offset=v_offset)
+    return Hc, W, S, pm, ps, pa
+
+
+def _check_final(ref, token, lse, conf):
+    ok_margin = ref["margin"] > MARGIN
+    assert np.array_equal(token[ok_margin], ref["arg"][ok_margin])
+    assert orc.isclose_rel(lse, ref["lse"], LSE_REL)
+    assert orc.isclose_rel(conf, ref["conf"], CONF_REL)
+
+
+@pytest.mark.parametrize("m,d,V", [(1, 64, 300), (1024, 256, 8192), (333, 4096, 126464 // 8 + 5),
+                                   (2048, 4096, 126464), (700, 3584, 19008)])
+def test_lmhead_stats_vs_oracle(dev, m, d, V):
+    from paper_2601_06562_b200 import hotpath
+
+    Hc, W, S, pm, ps, pa = _stats_case(dev, m, d, V, seed=m + V)
+    token = torch.empty(m, dtype=torch.int32, device=dev)
+    lse = torch.empty(m, device=dev)
+    conf = torch.empty(m, device=dev)
+    hotpath.stats_merge(pm, ps, pa, S, m, m, m_host=m, token=token, lse=lse, conf=conf)
+    ref = orc.softmax_stats(orc.logits_f64(Hc, W))
+    _check_final(ref, token.cpu().numpy(), as_f64(lse), as_f64(conf))
+    # every split triple against the oracle on its own column range
+    tiles = -(-V // 256)
+    tps = -(-tiles // S)
+    bounds = [min(V, s * tps * 256) for s in range(S)] + [V]
+    parts = orc.split_stats(orc.logits_f64(Hc, W), bounds)
+    for s, (mx, sm, ar) in enumerate(parts):
+        assert orc.isclose_rel(pm[s].cpu().numpy(), mx, 1e-4) or np.allclose(pm[s].cpu().numpy(), mx, atol=1e-4)
+        assert orc.isclose_rel(ps[s].cpu().numpy(), sm, 1e-3)
+
+
+def test_argmax_tie_lowest_index(dev):
+    """Duplicate vocab rows produce exactly tied logits; the lowest id must win,
+    inside a tile, across tiles and across splits."""
+    from paper_2601_06562_b200 import hotpath
+
+    rng = np.random.default_rng(9)
+    m, d, V = 256, 128, 2048
+    Hc = orc.bf16_round(rng.standard_normal((m, d)))
+    W = orc.bf16_round(rng.standard_normal((V, d)) * 0.01)
+    star = orc.bf16_round(rng.standard_normal(d))
+    for col in (5, 200, 700, 1800):  # same tile, other tile, other split
+        W[col] = star
+    Hc[:, :] = orc.bf16_round(np.outer(np.ones(m), star) + 0.01 * rng.standard_normal((m, d)))
+    for S in (1, 2, 8):
+        pm = torch.empty(S, m, device=dev)
+        ps = torch.empty(S, m, device=dev)
+        pa = torch.empty(S, m, dtype=torch.int32, device=dev)
+        hotpath.lmhead_stats(bf16_tensor(Hc, dev), bf16_tensor(W, dev), S, pm, ps, pa, m_host=m)
+        token = torch.empty(m, dtype=torch.int32, device=dev)
+        hotpath.stats_merge(pm, ps, pa, S, m, m, m_host=m, token=token)
+        assert (token.cpu().numpy() == 5).all(), S
+
+
+def test_vocab_shards_merge_equals_unsharded(dev):
+    """P-way vocab sharding emulated on one GPU: each shard runs K3 with its
+    vocab offset, K4 merges splits per shard, then K4 merges shards in rank
+    order — the exact data flow of the NCCL path minus the all-gather."""
+    from paper_2601_06562_b200 import hotpath
+
+    m, d, V, P = 512, 1024, 126464 // 16, 4
+    rng = np.random.default_rng(11)
+    Hc = orc.bf16_round(rng.standard_normal((m, d)))
+    W = orc.bf16_round(rng.standard_normal((V, d)) * 0.02)
+    Hd = bf16_tensor(Hc, dev)
+    edges = [r * V // P for r in range(P + 1)]
+    gathered = torch.empty(P, 3, m, device=dev)
+    for r in range(P):
+        Wr = bf16_tensor(W[edges[r]:edges[r + 1]], dev)
+        S = hotpath.lmhead_plan(m, Wr.shape[0], d)[0]
+        pm = torch.empty(S, m, device=dev)
+        ps = torch.empty(S, m, device=dev)
+        pa = torch.empty(S, m, dtype=torch.int32, device=dev)
+        hotpath.lmhead_stats(Hd, Wr, S, pm, ps, pa, m_host=m, v_offset=edges[r])
+        g = gathered[r]
+        hotpath.stats_merge(pm, ps, pa, S, m, m, m_host=m, out_max=g[0], out_sum=g[1],
+                            out_arg=g[2].view(torch.int32))
+    token = torch.empty(m, dtype=torch.int32, device=dev)
+    lse = torch.empty(m, device=dev)
+    conf = torch.empty(m, device=dev)
+    hotpath.stats_merge(gathered[0, 0], gathered[0, 1], gathered[0, 2].view(torch.int32), P, 3 * m, m,
+                        m_host=m, token=token, lse=lse, conf=conf)
+    ref = orc.softmax_stats(orc.logits_f64(Hc, W))
+    _check_final(ref, token.cpu().numpy(), as_f64(lse), as_f64(conf))
+
+
+# ----------------------------------------------------------------------- K5
+@pytest.mark.parametrize("M,k", [(1, 1), (10, 0), (10, 10), (10, 25), (1024, 32), (16384, 256),
+                                 (65536, 683), (524288, 8192)])
+def test_remask_commit_bitexact(dev, M, k):
+    from paper_2601_06562_b200 import hotpath
+
+    rng = np.random.default_rng(M + k)
+    L = 2 * M + 5
+    pos = np.sort(rng.choice(L, size=M, replace=False)).astype(np.int32)
+    conf = (rng.random(M) * 1e-2).astype(np.float32)
+    conf[rng.random(M) < 0.2] = np.float32(0.004)  # heavy exact ties
+    token = rng.integers(0, 1000, size=M).astype(np.int32)
+    x = np.full(L, 99999, dtype=np.int32)
+    xd = torch.from_numpy(x).to(dev)
+    sel = torch.full((M,), -1, dtype=torch.int32, device=dev)
+    scratch = torch.empty(hotpath.remask_scratch_bytes(), dtype=torch.uint8, device=dev)
+    hotpath.remask_commit(torch.from_numpy(conf).to(dev), torch.from_numpy(pos).to(dev),
+                          torch.from_numpy(token).to(dev), k, xd, scratch, M, m_host=M, selected=sel)
+    want = orc.remask_select(conf, pos, k)
+    assert np.array_equal(sel.cpu().numpy().astype(bool), want)
+    assert np.array_equal(xd.cpu().numpy(), orc.commit(x, pos, token, want))
+
+
+# ----------------------------------------------------------------------- fused step
+@pytest.mark.parametrize("L,d,V,ratio,shift", [(2048, 256, 8192, 0.5, False), (2048, 256, 8192, 0.5, True),
+                                               (4096, 1024, 32000, 0.3, False)])
+def test_mask_only_head_step_vs_oracle(dev, L, d, V, ratio, shift):
+    from paper_2601_06562_b200 import MaskOnlyHead
+
+    rng = np.random.default_rng(L + d)
+    mask_id = V - 1
+    x = rng.integers(0, V - 1, size=L).astype(np.int32)
+    x[rng.random(L) < ratio] = mask_id
+    H = orc.bf16_round(rng.standard_normal((L, d)))
+    W = orc.bf16_round(rng.standard_normal((V, d)) * 0.05)
+    head = MaskOnlyHead(bf16_tensor(W, dev), seq_len=L, mask_id=mask_id, shift=shift)
+    xd = torch.from_numpy(x).to(dev)
+    k = 37
+    out = head.step(xd, bf16_tensor(H, dev), k)
+    torch.cuda.synchronize()
+    ref = orc.step(x, H, W, mask_id, k, shift=shift)
+    M = int(out.m_dev.item())
+    assert M == ref["idx"].size
+    assert np.array_equal(out.idx[:M].cpu().numpy(), ref["idx"])
+    token = out.token[:M].cpu().numpy()
+    _check_final(ref, token, as_f64(out.lse[:M]), as_f64(out.conf[:M]))
+    # selection: bit-exact given the device confidences; vs the fp64 oracle up to near-ties
+    sel = out.selected[:M].cpu().numpy().astype(bool)
+    assert np.array_equal(sel, orc.remask_select(out.conf[:M].cpu().numpy(), ref["idx"], k))
+    near = orc.near_tie_rows(ref["conf"], k)
+    assert np.array_equal(sel[~near], ref["selected"][~near])
+    # committed sequence: every unmasked position carries the oracle argmax
+    xo = xd.cpu().numpy()
+    assert (xo == mask_id).sum() == M - k
+    for r in np.flatnonzero(sel):
+        if ref["margin"][r] > MARGIN:
+            assert xo[ref["idx"][r]] == ref["arg"][r]
+
+
+# ----------------------------------------------------------------------- arena
+def test_arena_commit_grow_shrink(dev):
+    from paper_2601_06562_b200 import vmm
+
+    ws = vmm.reserve(1 << 30, backend="cuda")
+    try:
+        g = ws.page_size
+        ws.commit_to(3 * g + 5)
+        assert ws.committed_bytes == 4 * g
+        t = ws.view(0, (4 * g,), torch.uint8)
+        t.fill_(7)
+        ws.commit_to(2 * g)
+        assert ws.committed_bytes == 2 * g
+        assert int(ws.view(0, (2 * g,), torch.uint8).sum().item()) == 7 * 2 * g
+        ws.commit_to(6 * g)
+        ws.view(2 * g, (4 * g,), torch.uint8).fill_(1)
+        assert int(ws.view(0, (2 * g,), torch.uint8).sum().item()) == 7 * 2 * g
+        from paper_2601_06562_b200.errors import CapacityError
+
+        with pytest.raises(CapacityError):
+            ws.commit_to(ws.reserved_bytes + 1)
+    finally:
+        ws.close()
