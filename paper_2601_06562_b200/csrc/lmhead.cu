@@ -18,27 +18,39 @@
 // only global output is one (max, sum, arg) triple per row and split. Units are
 // numbered m-fastest inside groups of `group_m` m-blocks, so the ~148 units in
 // flight at once share a handful of W tiles and m-blocks through L2.
+#include <cstdlib>
+
 #include "common.cuh"
 
 namespace mosaic {
 namespace {
 
-constexpr int BM = 128;          // rows per tile (UMMA M)
+constexpr int BM = 128;          // accumulator rows per CTA (TMEM lanes)
 constexpr int BN = 256;          // vocab columns per tile (UMMA N)
 constexpr int BK = 64;           // K per stage: one 128-byte swizzle atom of bf16
 constexpr int UK = 16;           // K per tcgen05.mma (kind::f16)
-constexpr int STAGES = 4;
-constexpr int A_BYTES = BM * BK * 2;
-constexpr int B_BYTES = BN * BK * 2;
-constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
 constexpr int NUM_ACC = 2;       // TMEM accumulator double buffer
 constexpr int TMEM_COLS = 512;   // 2 x 256 fp32 columns
 constexpr int kThreads = 192;    // warp0 TMA, warp1 MMA+TMEM, warps 2..5 epilogue
-constexpr int kEpiThreads = 128;
-constexpr uint32_t kIdesc = umma_idesc_bf16(BM, BN);
-constexpr int kSmemBytes = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
+constexpr int kEpiWarps = 4;
 constexpr int kMaxSplits = 64;
 constexpr float kLog2e = 1.4426950408889634f;
+
+// Per cta_group configuration. CG = 2 pairs two SMs on one 256 x 256 tile
+// (tcgen05.mma.cta_group::2): each CTA stages half of the rows (A) and half of
+// the vocab columns (B) of every K step, so shared-memory and L2 traffic per
+// FLOP drop by a third against CG = 1 and the ring can be 6 stages deep.
+template <int CG>
+struct Cfg {
+  static constexpr int ROWS = BM * CG;             // tile rows (UMMA M)
+  static constexpr int B_ROWS = BN / CG;           // vocab rows staged per CTA
+  static constexpr int A_BYTES = BM * BK * 2;
+  static constexpr int B_BYTES = B_ROWS * BK * 2;
+  static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+  static constexpr int STAGES = CG == 1 ? 4 : 6;
+  static constexpr int SMEM = STAGES * STAGE_BYTES + 1024 + 256;
+  static constexpr uint32_t IDESC = umma_idesc_bf16(ROWS, BN);
+};
 
 struct Params {
   const int32_t* m_dev;
@@ -93,65 +105,76 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, float (&v)[32]) {
   for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
 }
 
-template <bool kStoreLogits>
+template <int CG, bool kStoreLogits>
 __global__ void __launch_bounds__(kThreads, 1)
     k3_lmhead(const __grid_constant__ CUtensorMap tmap_a, const __grid_constant__ CUtensorMap tmap_b,
               const Params p) {
+  using C = Cfg<CG>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~static_cast<uintptr_t>(1023));
   uint8_t* sA = smem;
-  uint8_t* sB = smem + STAGES * A_BYTES;
-  uint64_t* full = reinterpret_cast<uint64_t*>(sB + STAGES * B_BYTES);
-  uint64_t* empty = full + STAGES;
-  uint64_t* tfull = empty + STAGES;
+  uint8_t* sB = smem + C::STAGES * C::A_BYTES;
+  uint64_t* full = reinterpret_cast<uint64_t*>(sB + C::STAGES * C::B_BYTES);
+  uint64_t* empty = full + C::STAGES;
+  uint64_t* tfull = empty + C::STAGES;
   uint64_t* tempty = tfull + NUM_ACC;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + NUM_ACC);
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
+  const uint32_t rank = CG == 2 ? cluster_ctarank() : 0u;  // position in the SM pair
+  const int64_t cluster = blockIdx.x / CG;
+  const int64_t n_clusters = gridDim.x / CG;
   const int64_t M = min(static_cast<int64_t>(load_count(p.m_dev, p.m_host)), p.m_cap);
-  const int m_blocks = static_cast<int>((M + BM - 1) / BM);
+  const int m_blocks = static_cast<int>((M + C::ROWS - 1) / C::ROWS);
   const int64_t units = static_cast<int64_t>(m_blocks) * p.n_splits;
   const int k_blocks = p.K / BK;
 
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&tmap_a);
     tma_prefetch_desc(&tmap_b);
-    for (int i = 0; i < STAGES; ++i) {
+    for (int i = 0; i < C::STAGES; ++i) {
       mbar_init(&full[i], 1);
       mbar_init(&empty[i], 1);
     }
     for (int i = 0; i < NUM_ACC; ++i) {
       mbar_init(&tfull[i], 1);
-      mbar_init(&tempty[i], kEpiThreads);
+      mbar_init(&tempty[i], kEpiWarps * CG);  // one arrive per epilogue warp of the pair
     }
     fence_mbar_init();
   }
-  if (warp == 1) tmem_alloc(tmem_slot, TMEM_COLS);
+  if (warp == 1) tmem_alloc<CG>(tmem_slot, TMEM_COLS);
   tc_fence_before();
-  __syncthreads();
+  if constexpr (CG == 2) cluster_sync(); else __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
 
   if (warp == 0) {
-    // ------------------------------------------------------------ TMA producer
+    // ------------------------------------------------------------ TMA producer (both CTAs)
     if (lane == 0) {
       const uint64_t pol_a = policy_evict_last();    // re-read for every tile of the unit
       const uint64_t pol_b = policy_evict_normal();  // shared by the m-blocks in flight
       uint32_t stage = 0, phase = 0;
-      for (int64_t u = blockIdx.x; u < units; u += gridDim.x) {
+      for (int64_t u = cluster; u < units; u += n_clusters) {
         int mb, s;
         unit_coords(p, m_blocks, u, mb, s);
         const int t0 = s * p.tiles_per_split;
         const int t1 = min(t0 + p.tiles_per_split, p.n_tiles);
+        const int a_row = mb * C::ROWS + rank * BM;
         for (int t = t0; t < t1; ++t) {
+          const int b_row = t * BN + rank * C::B_ROWS;
           for (int kb = 0; kb < k_blocks; ++kb) {
             mbar_wait(&empty[stage], phase ^ 1);
-            mbar_arrive_expect_tx(&full[stage], STAGE_BYTES);
-            tma_load_2d(sA + stage * A_BYTES, &tmap_a, &full[stage], kb * BK, mb * BM, pol_a);
-            tma_load_2d(sB + stage * B_BYTES, &tmap_b, &full[stage], kb * BK, t * BN, pol_b);
-            if (++stage == STAGES) {
+            if (rank == 0) mbar_arrive_expect_tx(&full[stage], C::STAGE_BYTES * CG);
+            if constexpr (CG == 1) {
+              tma_load_2d(sA + stage * C::A_BYTES, &tmap_a, &full[stage], kb * BK, a_row, pol_a);
+              tma_load_2d(sB + stage * C::B_BYTES, &tmap_b, &full[stage], kb * BK, b_row, pol_b);
+            } else {
+              tma_load_2d_cg2(sA + stage * C::A_BYTES, &tmap_a, &full[stage], kb * BK, a_row, pol_a);
+              tma_load_2d_cg2(sB + stage * C::B_BYTES, &tmap_b, &full[stage], kb * BK, b_row, pol_b);
+            }
+            if (++stage == C::STAGES) {
               stage = 0;
               phase ^= 1;
             }
@@ -160,34 +183,35 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
     }
   } else if (warp == 1) {
-    // ------------------------------------------------------------ MMA issuer
-    if (lane == 0) {
+    // ------------------------------------------------------------ MMA issuer (pair leader)
+    if (lane == 0 && rank == 0) {
       uint32_t stage = 0, phase = 0, acc = 0, acc_phase = 0;
-      for (int64_t u = blockIdx.x; u < units; u += gridDim.x) {
+      for (int64_t u = cluster; u < units; u += n_clusters) {
         int mb, s;
         unit_coords(p, m_blocks, u, mb, s);
         const int t0 = s * p.tiles_per_split;
         const int t1 = min(t0 + p.tiles_per_split, p.n_tiles);
         for (int t = t0; t < t1; ++t) {
-          mbar_wait(&tempty[acc], acc_phase ^ 1);
+          if constexpr (CG == 2) mbar_wait_cluster(&tempty[acc], acc_phase ^ 1);
+          else mbar_wait(&tempty[acc], acc_phase ^ 1);
           tc_fence_after();
           const uint32_t d_tmem = tmem_base + acc * BN;
           for (int kb = 0; kb < k_blocks; ++kb) {
             mbar_wait(&full[stage], phase);
             tc_fence_after();
-            const uint32_t a0 = smem_u32(sA + stage * A_BYTES);
-            const uint32_t b0 = smem_u32(sB + stage * B_BYTES);
+            const uint32_t a0 = smem_u32(sA + stage * C::A_BYTES);
+            const uint32_t b0 = smem_u32(sB + stage * C::B_BYTES);
 #pragma unroll
             for (int kk = 0; kk < BK / UK; ++kk)
-              umma_bf16(d_tmem, umma_desc_sw128(a0 + kk * UK * 2), umma_desc_sw128(b0 + kk * UK * 2),
-                        kIdesc, (kb | kk) != 0);
-            umma_commit(&empty[stage]);  // frees the smem slot when these MMAs retire
-            if (++stage == STAGES) {
+              umma_bf16<CG>(d_tmem, umma_desc_sw128(a0 + kk * UK * 2),
+                            umma_desc_sw128(b0 + kk * UK * 2), C::IDESC, (kb | kk) != 0);
+            umma_commit<CG>(&empty[stage]);  // frees the smem slot(s) when these MMAs retire
+            if (++stage == C::STAGES) {
               stage = 0;
               phase ^= 1;
             }
           }
-          umma_commit(&tfull[acc]);  // accumulator ready for the epilogue
+          umma_commit<CG>(&tfull[acc]);  // accumulator ready for the epilogue(s)
           if (++acc == NUM_ACC) {
             acc = 0;
             acc_phase ^= 1;
@@ -196,16 +220,18 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
     }
   } else {
-    // ------------------------------------------------------------ epilogue
+    // ------------------------------------------------------------ epilogue (both CTAs)
     const int q = warp & 3;  // TMEM lane quarter accessible to this warp
     const int row_local = q * 32 + lane;
+    // tempty lives in the pair leader: arrive locally or through the cluster window
+    const uint32_t tempty_addr0 = CG == 2 ? mapa_shared(smem_u32(&tempty[0]), 0) : smem_u32(&tempty[0]);
     uint32_t acc = 0, acc_phase = 0;
-    for (int64_t u = blockIdx.x; u < units; u += gridDim.x) {
+    for (int64_t u = cluster; u < units; u += n_clusters) {
       int mb, s;
       unit_coords(p, m_blocks, u, mb, s);
       const int t0 = s * p.tiles_per_split;
       const int t1 = min(t0 + p.tiles_per_split, p.n_tiles);
-      const int64_t row = static_cast<int64_t>(mb) * BM + row_local;
+      const int64_t row = static_cast<int64_t>(mb) * C::ROWS + rank * BM + row_local;
       float run_max = -INFINITY, run_sum = 0.f;
       int64_t run_arg = 0;
       for (int t = t0; t < t1; ++t) {
@@ -257,7 +283,11 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
         }
         tc_fence_before();
-        mbar_arrive(&tempty[acc]);
+        __syncwarp();
+        if (lane == 0) {
+          if constexpr (CG == 2) mbar_arrive_cluster(tempty_addr0 + acc * 8);
+          else mbar_arrive(&tempty[acc]);
+        }
         if (++acc == NUM_ACC) {
           acc = 0;
           acc_phase ^= 1;
@@ -275,10 +305,10 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
 
   tc_fence_before();
-  __syncthreads();
+  if constexpr (CG == 2) cluster_sync(); else __syncthreads();
   if (warp == 1) {
     tc_fence_after();
-    tmem_dealloc(tmem_base, TMEM_COLS);
+    tmem_dealloc<CG>(tmem_base, TMEM_COLS);
   }
 }
 
@@ -301,17 +331,35 @@ int encode_kmajor_bf16(CUtensorMap* map, const void* base, int64_t rows, int64_t
   return MOSAIC_OK;
 }
 
+int cta_group_for(int64_t m_cap) {
+  static int forced = [] {
+    const char* e = getenv("MOSAIC_CTA_GROUP");
+    return e ? atoi(e) : 0;
+  }();
+  if (forced == 1 || forced == 2) return forced;
+  return m_cap > BM ? 2 : 1;  // a lone 128-row block would leave half a pair idle
+}
+
+int group_m_default() {
+  static int g = [] {
+    const char* e = getenv("MOSAIC_GROUP_M");
+    return e ? atoi(e) : 0;
+  }();
+  return g;
+}
+
 void plan_splits(int64_t m_cap, int64_t V, int32_t* n_splits, int32_t* tps) {
+  const int cg = cta_group_for(m_cap);
   const int64_t n_tiles = ceil_div(V, BN);
-  const int64_t m_blocks = ceil_div(m_cap > 0 ? m_cap : 1, BM);
-  const int64_t sms = num_sms();
+  const int64_t m_blocks = ceil_div(m_cap > 0 ? m_cap : 1, BM * cg);
+  const int64_t workers = num_sms() / cg;
   int64_t best_cost = INT64_MAX, best_tps = n_tiles;
   for (int64_t t = n_tiles; t >= 1; --t) {
     const int64_t S = ceil_div(n_tiles, t);
     if (S > kMaxSplits) break;
     if (ceil_div(n_tiles, S) != t) continue;  // same split count as a larger t
     const int64_t units = m_blocks * S;
-    const int64_t cost = ceil_div(units, sms) * t;  // tiles on the busiest CTA
+    const int64_t cost = ceil_div(units, workers) * t;  // tiles on the busiest SM (pair)
     if (cost < best_cost) {
       best_cost = cost;
       best_tps = t;
@@ -319,6 +367,35 @@ void plan_splits(int64_t m_cap, int64_t V, int32_t* n_splits, int32_t* tps) {
   }
   *tps = static_cast<int32_t>(best_tps);
   *n_splits = static_cast<int32_t>(ceil_div(n_tiles, best_tps));
+}
+
+template <int CG, bool kStore>
+int launch_cg(const CUtensorMap& ta, const CUtensorMap& tb, const Params& p, int64_t m_cap,
+              cudaStream_t stream) {
+  using C = Cfg<CG>;
+  auto kern = k3_lmhead<CG, kStore>;
+  static bool attr_set = false;  // per instantiation
+  if (!attr_set) {
+    MOSAIC_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
+    attr_set = true;
+  }
+  const int64_t units_cap = ceil_div(m_cap, C::ROWS) * p.n_splits;
+  const int64_t workers = num_sms() / CG;
+  const int64_t clusters = units_cap < workers ? units_cap : workers;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(static_cast<unsigned>(clusters * CG));
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = C::SMEM;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = CG;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  MOSAIC_CUDA(cudaLaunchKernelEx(&cfg, kern, ta, tb, p));
+  return MOSAIC_OK;
 }
 
 template <bool kStore>
@@ -332,10 +409,11 @@ int launch(const uint16_t* Hc, int64_t m_cap, const int32_t* m_dev, int64_t m_ho
   MOSAIC_REQUIRE((reinterpret_cast<uintptr_t>(Hc) & 15) == 0 && (reinterpret_cast<uintptr_t>(W) & 15) == 0,
                  "Hc and W must be 16-byte aligned");
   if (m_cap == 0) return MOSAIC_OK;
+  const int cg = cta_group_for(m_cap);
   CUtensorMap ta, tb;
   int st = encode_kmajor_bf16(&ta, Hc, m_cap, d, BM);
   if (st) return st;
-  st = encode_kmajor_bf16(&tb, W, V, d, BN);
+  st = encode_kmajor_bf16(&tb, W, V, d, BN / cg);
   if (st) return st;
   p.m_dev = m_dev;
   p.m_host = m_host;
@@ -343,16 +421,10 @@ int launch(const uint16_t* Hc, int64_t m_cap, const int32_t* m_dev, int64_t m_ho
   p.V = V;
   p.K = static_cast<int32_t>(d);
   p.n_tiles = static_cast<int32_t>(ceil_div(V, BN));
-  if (p.group_m <= 0) p.group_m = 16;
-  auto kern = k3_lmhead<kStore>;
-  static bool attr_set = false;  // per template instantiation
-  if (!attr_set) {
-    MOSAIC_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes));
-    attr_set = true;
-  }
-  const int64_t units_cap = ceil_div(m_cap, BM) * p.n_splits;
-  const int grid = static_cast<int>(units_cap < num_sms() ? units_cap : num_sms());
-  kern<<<grid, kThreads, kSmemBytes, as_stream(stream)>>>(ta, tb, p);
+  if (p.group_m <= 0) p.group_m = group_m_default() > 0 ? group_m_default() : (cg == 2 ? 8 : 16);
+  st = cg == 2 ? launch_cg<2, kStore>(ta, tb, p, m_cap, as_stream(stream))
+               : launch_cg<1, kStore>(ta, tb, p, m_cap, as_stream(stream));
+  if (st) return st;
   return check_launch(kStore ? "mosaic_lmhead_logits" : "mosaic_lmhead_stats");
 }
 
