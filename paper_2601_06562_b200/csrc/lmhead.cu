@@ -62,6 +62,7 @@ struct Params {
   int32_t tiles_per_split;
   int32_t n_splits;
   int32_t group_m;
+  int32_t policy;   // L2 policy of (A, B) loads: 0 = (evict_normal, evict_normal), 1 = (evict_last, evict_normal), 2 = (evict_normal, evict_first)
   int64_t v_offset;
   float* part_max;
   float* part_sum;
@@ -153,8 +154,10 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (warp == 0) {
     // ------------------------------------------------------------ TMA producer (both CTAs)
     if (lane == 0) {
-      const uint64_t pol_a = policy_evict_last();    // re-read for every tile of the unit
-      const uint64_t pol_b = policy_evict_normal();  // shared by the m-blocks in flight
+      // A is re-read for every tile of a unit and by the units of its m-group;
+      // a W tile is shared by the m-blocks in flight at the same moment.
+      const uint64_t pol_a = p.policy == 1 ? policy_evict_last() : policy_evict_normal();
+      const uint64_t pol_b = p.policy == 2 ? policy_evict_first() : policy_evict_normal();
       uint32_t stage = 0, phase = 0;
       for (int64_t u = cluster; u < units; u += n_clusters) {
         int mb, s;
@@ -340,6 +343,11 @@ int cta_group_for(int64_t m_cap) {
   return m_cap > BM ? 2 : 1;  // a lone 128-row block would leave half a pair idle
 }
 
+int env_int(const char* name, int fallback) {
+  const char* e = getenv(name);
+  return e ? atoi(e) : fallback;
+}
+
 int group_m_default() {
   static int g = [] {
     const char* e = getenv("MOSAIC_GROUP_M");
@@ -421,7 +429,9 @@ int launch(const uint16_t* Hc, int64_t m_cap, const int32_t* m_dev, int64_t m_ho
   p.V = V;
   p.K = static_cast<int32_t>(d);
   p.n_tiles = static_cast<int32_t>(ceil_div(V, BN));
-  if (p.group_m <= 0) p.group_m = group_m_default() > 0 ? group_m_default() : (cg == 2 ? 8 : 16);
+  if (p.group_m <= 0) p.group_m = group_m_default() > 0 ? group_m_default() : 16;
+  static const int policy = env_int("MOSAIC_L2_POLICY", 0);
+  p.policy = policy;
   st = cg == 2 ? launch_cg<2, kStore>(ta, tb, p, m_cap, as_stream(stream))
                : launch_cg<1, kStore>(ta, tb, p, m_cap, as_stream(stream));
   if (st) return st;
