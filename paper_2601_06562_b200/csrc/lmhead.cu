@@ -430,7 +430,7 @@ int launch(const uint16_t* Hc, int64_t m_cap, const int32_t* m_dev, int64_t m_ho
   p.K = static_cast<int32_t>(d);
   p.n_tiles = static_cast<int32_t>(ceil_div(V, BN));
   if (p.group_m <= 0) p.group_m = group_m_default() > 0 ? group_m_default() : 16;
-  static const int policy = env_int("MOSAIC_L2_POLICY", 0);
+  static const int policy = env_int("MOSAIC_L2_POLICY", 1);  // measured best: A evict_last
   p.policy = policy;
   st = cg == 2 ? launch_cg<2, kStore>(ta, tb, p, m_cap, as_stream(stream))
                : launch_cg<1, kStore>(ta, tb, p, m_cap, as_stream(stream));
