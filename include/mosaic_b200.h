@@ -122,6 +122,12 @@ MOSAIC_API int mosaic_remask_commit(const float* conf, const int32_t* pos, const
                          const int32_t* m_dev, int64_t m_host, int64_t m_cap, int64_t k,
                          int32_t* x, int32_t* selected, void* scratch, void* stream);
 
+/* ---------------------------------------------------------------- K6 ------
+ * Fused SwiGLU of one FFN chunk, in place: up[i] = silu(gate[i]) * up[i],
+ * bf16, n elements (the in-place `glu` op of the chunked FFN loop,
+ * workload.py:249-259). gate/up 16-byte aligned.                              */
+MOSAIC_API int mosaic_swiglu(const uint16_t* gate, uint16_t* up, int64_t n, void* stream);
+
 /* ---------------------------------------------------------------- K7 ------
  * Contiguous device workspace with lazy physical commitment (cuMem VMM):
  * reserve a VA range once, map physical granules for the prefix

@@ -1,0 +1,355 @@
+"""Numeric step executor: runs an instantiated step graph on the B200 with every
+activation at its planned offset inside one cuMem arena.
+
+The reference plans a denoising step but never executes it (the step loop
+mosaic/workload.py:349-399 stops at the memory trace). Here
+``StepExecutor.run`` walks ``ConcreteGraph.ops`` in order and dispatches on
+``OpInstance.kind``; each tensor instance is a zero-copy view of the arena at
+the offset ``plan_first_fit`` gave its storage group, so in-place pairs share
+storage, chunk instances live exactly where the plan put them, and the step
+allocates nothing per op. Graph inputs (token ids, mask indices, weights)
+live outside the workspace, as in the reference (mosaic/liveness.py:52-53).
+
+Op kinds (mosaic/workload.py:179-316, plus the fused-logits kinds):
+
+* embed / matmul / fused_attention / add / alloc — model forward (cuBLAS and
+  PyTorch SDPA; not the hot path);
+* ffn_up / ffn_gate / glu (K6) / activation / ffn_down / chunk_write — the
+  lazily chunked FFN, rows [i*ceil(L/K_FFN), ...) per iteration;
+* gather (K2) / lmhead_stats (K3) / sample (K4) / commit (K5) — the fused
+  mask-only logits + remask hot path (``logits_mode="fused"``);
+* gather_logits / logits / shift / chunk_write / sample — the reference's
+  materialising modes (``mask_only`` / ``eager``), executed with cuBLAS and
+  fp32 softmax as the dense-logits baseline.
+"""
+from __future__ import annotations
+
+import math
+from typing import Optional
+
+import torch
+import torch.nn.functional as F
+
+from . import hotpath
+from .errors import InputError
+from .graph import ConcreteGraph, InstKey
+from .liveness import LifetimeTable, analyze
+from .planner import MemoryPlan, plan_first_fit
+from .vmm import Workspace
+from .workload import ModelConfig
+
+_INT32_TENSORS = {"token_out", "token_ids", "mask_idx"}
+
+
+class RandomDLLM:
+    """Random-init weights of a :class:`ModelConfig` on one device (bf16), in the
+    template's graph-input layout. The LM head is stored [V, d] (K-major for
+    K3); the reference's [d, V] is the same matrix transposed.
+
+    ``distinct_layers`` limits how many layer weight sets are materialised;
+    layer i uses set ``i % distinct_layers`` (the context sweep allocates all
+    of them to charge the full weight footprint)."""
+
+    def __init__(self, cfg: ModelConfig, device, seed: int = 0, distinct_layers: Optional[int] = None,
+                 vocab_shard: tuple[int, int] | None = None):
+        if cfg.moe is not None:
+            raise InputError("MoE expert execution is not implemented in the executor yet")
+        if cfg.element_size != 2:
+            raise InputError("the executor runs bf16 models (element_size=2)")
+        self.cfg = cfg
+        g = torch.Generator(device=device).manual_seed(seed)
+        d, f, V = cfg.d_model, cfg.d_ff, cfg.vocab_size
+        out_scale = 1.0 / math.sqrt(2 * cfg.n_layers)
+
+        def w(*shape, scale=0.02):
+            return (torch.randn(shape, generator=g, device=device, dtype=torch.float32) * scale).to(torch.bfloat16)
+
+        self.w_embed = w(V, d, scale=1.0)
+        n_sets = cfg.n_layers if distinct_layers is None else max(1, min(distinct_layers, cfg.n_layers))
+        self.layers = []
+        for _ in range(n_sets):
+            lw = {"w_qkv": w(d, 3 * d), "w_attn_out": w(d, d, scale=0.02 * out_scale),
+                  "w_up": w(d, f), "w_down": w(f, d, scale=0.02 * out_scale)}
+            if cfg.gated_ffn:
+                lw["w_gate"] = w(d, f)
+            self.layers.append(lw)
+        v0, v1 = vocab_shard or (0, V)
+        self.vocab_offset = v0
+        self.w_vocab = w(v1 - v0, d)  # [V_shard, d]
+
+    def layer(self, i: int) -> dict:
+        return self.layers[i % len(self.layers)]
+
+    def nbytes(self) -> int:
+        n = self.w_embed.numel() + self.w_vocab.numel()
+        for lw in self.layers:
+            n += sum(t.numel() for t in lw.values())
+        return 2 * n
+
+
+def _rows(n_total: int, trips: int, it: Optional[int]) -> tuple[int, int]:
+    if it is None:
+        return 0, n_total
+    per = -(-n_total // trips)
+    r0 = min(it * per, n_total)
+    return r0, min(r0 + per, n_total)
+
+
+class StepExecutor:
+    """Executes step graphs of one model inside one :class:`Workspace` (cuda)."""
+
+    def __init__(self, model: RandomDLLM, workspace: Workspace, mask_id: int, exec_layers: Optional[int] = None):
+        if workspace.backend != "cuda":
+            raise InputError("the executor needs a cuda workspace")
+        self.model = model
+        self.cfg = model.cfg
+        self.ws = workspace
+        self.mask_id = int(mask_id)
+        self.shift = self.cfg.shift_mode != "none"
+        self.exec_layers = exec_layers  # execute only the first n layers (context sweep)
+        dev = torch.device("cuda", workspace.device)
+        self.device = dev
+        self._side: dict[int, dict] = {}
+
+    # ---------------------------------------------------------------- buffers
+    def _side_buffers(self, L: int) -> dict:
+        """Graph inputs outside the workspace: mask indices, their count and the
+        K1/K5 scratch (mosaic/liveness.py:52-53 excludes graph inputs)."""
+        if L not in self._side:
+            self._side = {L: {
+                "mask_idx": torch.empty(L, dtype=torch.int32, device=self.device),
+                "m_dev": torch.zeros(1, dtype=torch.int32, device=self.device),
+                "compact": torch.empty(hotpath.mask_compact_scratch_bytes(L), dtype=torch.uint8, device=self.device),
+                "remask": torch.empty(hotpath.remask_scratch_bytes(), dtype=torch.uint8, device=self.device),
+            }}
+        return self._side[L]
+
+    def _views(self, g: ConcreteGraph, table: LifetimeTable, plan: MemoryPlan) -> dict[InstKey, torch.Tensor]:
+        offset = plan.offsets()
+        views: dict[InstKey, torch.Tensor] = {}
+        t = g.template
+        for grp in table.groups:
+            base = offset[grp.id]
+            for key in grp.members:
+                tid = key[0]
+                shape = t.instance_shape(tid, g.bindings)
+                es = t.tensor(tid).element_size
+                if es == 2:
+                    dtype = torch.bfloat16
+                elif tid in _INT32_TENSORS:
+                    dtype = torch.int32
+                else:
+                    dtype = torch.float32
+                if 0 in shape:
+                    views[key] = torch.empty(shape, dtype=dtype, device=self.device)
+                else:
+                    views[key] = self.ws.view(base, shape, dtype)
+        return views
+
+    # ---------------------------------------------------------------- run
+    def plan(self, g: ConcreteGraph) -> tuple[LifetimeTable, MemoryPlan]:
+        table = analyze(g)
+        return table, plan_first_fit(table)
+
+    def run(self, g: ConcreteGraph, x: torch.Tensor, k_unmask: int,
+            table: Optional[LifetimeTable] = None, plan: Optional[MemoryPlan] = None,
+            keep: tuple[str, ...] = ()) -> dict:
+        """Execute one step; ``x`` (int32 [L] on device) is updated in place.
+        Returns timing/memory measurements and the instances named in ``keep``
+        (copied out of the arena before they can be overwritten)."""
+        if table is None or plan is None:
+            table, plan = self.plan(g)
+        if plan.workspace_size > self.ws.committed_bytes:
+            self.ws.commit_to(plan.workspace_size)
+        b = g.bindings
+        L, M = b["L"], b["M"]
+        if x.dtype != torch.int32 or x.numel() != L:
+            raise InputError("x must be int32 [L]")
+        side = self._side_buffers(L)
+        views = self._views(g, table, plan)
+        kept: dict[str, torch.Tensor] = {}
+        start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        start.record()
+        # K1: masked positions (graph input mask_idx) of the current sequence
+        hotpath.mask_compact(x, self.mask_id, side["mask_idx"], side["m_dev"], side["compact"])
+        mask_idx = side["mask_idx"][:M]
+        skip_layers = set()
+        if self.exec_layers is not None:
+            skip_layers = {f"l{i}." for i in range(self.exec_layers, self.cfg.n_layers)}
+        for op in g.ops:
+            if skip_layers and op.op_id[:op.op_id.find(".") + 1] in skip_layers:
+                continue
+            self._dispatch(op, g, views, x, mask_idx, side, k_unmask)
+            for key in op.outputs:
+                if key[0] in keep:
+                    kept[key[0] if key[1] is None else f"{key[0]}@{key[1]}"] = views[key].clone()
+            if op.kind == "sample" and "token_out" in keep:
+                kept["token_out"] = views[("token_out", None)].clone()
+                kept["confidence"] = views[("confidence", None)].clone()
+        end.record()
+        end.synchronize()
+        return {"ms": start.elapsed_time(end), "workspace_bytes": plan.workspace_size,
+                "committed_bytes": self.ws.committed_bytes, "ops": len(g.ops), "kept": kept}
+
+    # ---------------------------------------------------------------- ops
+    def _dispatch(self, op, g: ConcreteGraph, v, x, mask_idx, side, k_unmask: int) -> None:
+        kind = op.kind
+        b = g.bindings
+        L, M = b["L"], b["M"]
+        cfg = self.cfg
+        d = cfg.d_model
+        if kind == "embed":
+            torch.index_select(self.model.w_embed, 0, x, out=v[op.outputs[0]])
+        elif kind == "matmul":
+            self._matmul(op, v)
+        elif kind == "fused_attention":
+            q, k, vv = (v[key] for key in op.inputs)
+            H = cfg.n_heads
+            dh = d // H
+            qh, kh, vh = (t.view(L, H, dh).transpose(0, 1).unsqueeze(0) for t in (q, k, vv))
+            o = F.scaled_dot_product_attention(qh, kh, vh, is_causal=False)  # bidirectional dLLM attention
+            v[op.outputs[0]].view(L, H, dh).copy_(o.squeeze(0).transpose(0, 1))
+        elif kind == "add":
+            a, c = (v[key] for key in op.inputs)
+            torch.add(a, c, out=v[op.outputs[0]])
+        elif kind == "alloc":
+            out = v[op.outputs[0]]
+            if op.outputs[0][0].endswith("ffn_acc"):
+                out.zero_()
+        elif kind in ("ffn_up", "ffn_gate"):
+            layer = self._layer(op.op_id)
+            r0, r1 = _rows(L, b["K_FFN"], op.iteration)
+            w = layer["w_up" if kind == "ffn_up" else "w_gate"]
+            torch.matmul(v[op.inputs[0]][r0:r1], w, out=v[op.outputs[0]][: r1 - r0])
+        elif kind == "glu":
+            r0, r1 = _rows(L, b["K_FFN"], op.iteration)
+            up, gate = v[op.inputs[0]], v[op.inputs[1]]
+            hotpath.swiglu_(gate[: r1 - r0], up[: r1 - r0])  # act shares storage with up (in place)
+        elif kind == "activation":
+            r0, r1 = _rows(L, b["K_FFN"], op.iteration)
+            up = v[op.inputs[0]][: r1 - r0]
+            up.copy_(F.silu(up))
+        elif kind == "ffn_down":
+            layer = self._layer(op.op_id)
+            r0, r1 = _rows(L, b["K_FFN"], op.iteration)
+            torch.matmul(v[op.inputs[0]][: r1 - r0], layer["w_down"], out=v[op.outputs[0]][: r1 - r0])
+        elif kind == "chunk_write":
+            src, dst = op.inputs
+            if src[0] == "logits":  # shift_mode=concat: logits chunk -> logits_all rows
+                r0, r1 = _rows(M if cfg.logits_mode == "mask_only" else L, b["K_logits"], op.iteration)
+            else:
+                r0, r1 = _rows(L, b["K_FFN"], op.iteration)
+            v[dst][r0:r1].copy_(v[src][: r1 - r0])
+        elif kind == "gather":  # K2, fused mode
+            r0, r1 = _rows(M, b["K_logits"], op.iteration)
+            if r1 > r0:
+                hotpath.gather_rows(v[op.inputs[0]], mask_idx[r0:r1], v[op.outputs[0]], m_host=r1 - r0,
+                                    shift=self.shift)
+        elif kind == "lmhead_stats":  # K3
+            r0, r1 = _rows(M, b["K_logits"], op.iteration)
+            hc, buf = v[op.inputs[0]], v[op.outputs[0]]
+            cap = hc.shape[0]
+            S, _ = hotpath.lmhead_plan(cap, self.model.w_vocab.shape[0], d)
+            if 3 * S > buf.shape[1]:
+                raise InputError(f"K3 wants {S} splits but the template reserved {buf.shape[1] // 3}")
+            flat = buf.view(-1)
+            pm, ps = flat[: S * cap].view(S, cap), flat[S * cap: 2 * S * cap].view(S, cap)
+            pa = flat[2 * S * cap: 3 * S * cap].view(torch.int32).view(S, cap)
+            if r1 > r0:
+                hotpath.lmhead_stats(hc, self.model.w_vocab, S, pm, ps, pa, m_host=r1 - r0,
+                                     v_offset=self.model.vocab_offset)
+            self._last_splits = S
+        elif kind == "sample":
+            self._sample(op, g, v)
+        elif kind == "gather_logits":  # reference mask-only: materialised [rows, V]
+            r0, r1 = _rows(M, b["K_logits"], op.iteration)
+            rows = mask_idx[r0:r1].long()
+            if self.shift:
+                rows = (rows - 1).clamp_min(0)
+            h = v[op.inputs[0]]
+            torch.matmul(h.index_select(0, rows), self.model.w_vocab.t(), out=v[op.outputs[0]][: r1 - r0])
+        elif kind == "logits":  # reference eager: all L rows
+            r0, r1 = _rows(L, b["K_logits"], op.iteration)
+            h = v[op.inputs[0]]
+            src = h[r0:r1] if not self.shift else h.index_select(
+                0, (torch.arange(r0, r1, device=h.device) - 1).clamp_min(0))
+            torch.matmul(src, self.model.w_vocab.t(), out=v[op.outputs[0]][: r1 - r0])
+        elif kind == "shift":
+            pass  # the shift was applied as a row remap when the logits were produced
+        elif kind == "commit":
+            tok, conf = v[op.inputs[0]], v[op.inputs[1]]
+            if cfg.logits_mode == "eager":  # rows are all positions: pick the masked ones
+                tok = tok.index_select(0, mask_idx.long())
+                conf = conf.index_select(0, mask_idx.long())
+            hotpath.remask_commit(conf[:M].contiguous(), mask_idx, tok[:M].contiguous(), k_unmask, x,
+                                  side["remask"], M, m_host=M)
+        else:
+            raise InputError(f"no executor for op kind {kind!r} ({op.label})")
+
+    def _layer(self, op_id: str) -> dict:
+        return self.model.layer(int(op_id[1:op_id.index(".")]))
+
+    def _matmul(self, op, v) -> None:
+        name = op.op_id.split(".", 1)[1]
+        lw = self._layer(op.op_id)
+        d = self.cfg.d_model
+        src = v[op.inputs[0]]
+        if name in ("q_proj", "k_proj", "v_proj"):
+            j = "qkv".index(name[0])
+            w = lw["w_qkv"][:, j * d:(j + 1) * d]
+        elif name == "attn_proj":
+            w = lw["w_attn_out"]
+        else:
+            raise InputError(f"unsupported matmul {op.op_id}")  # materialised attention scores
+        torch.matmul(src, w, out=v[op.outputs[0]])
+
+    def _sample(self, op, g: ConcreteGraph, v) -> None:
+        b = g.bindings
+        cfg = self.cfg
+        L, M = b["L"], b["M"]
+        if cfg.logits_mode == "fused":  # K4 over the K3 partial triples
+            src = v[op.inputs[0]]
+            r0, r1 = _rows(M, b["K_logits"], op.iteration)
+            if r1 <= r0:
+                return
+            cap = src.shape[0]
+            S = self._last_splits
+            flat = src.view(-1)
+            pm, ps = flat[: S * cap], flat[S * cap: 2 * S * cap]
+            pa = flat[2 * S * cap: 3 * S * cap].view(torch.int32)
+            tok, conf = v[op.inputs[1]], v[op.inputs[2]]
+            hotpath.stats_merge(pm, ps, pa, S, cap, cap, m_host=r1 - r0, token=tok[r0:r1], conf=conf[r0:r1])
+            return
+        # reference modes: fp32 softmax statistics of materialised bf16 logits
+        if len(op.outputs) == 2:  # concat: sample over logits_all after the loop
+            z = v[op.inputs[0]]
+            tok, conf = v[op.outputs[0]], v[op.outputs[1]]
+            r0, r1 = 0, z.shape[0]
+        else:
+            z, tok, conf = (v[key] for key in op.inputs)
+            rows = M if cfg.logits_mode == "mask_only" else L
+            r0, r1 = _rows(rows, b["K_logits"], op.iteration)
+            z = z[: r1 - r0]
+        zf = z.float()
+        mx, arg = zf.max(dim=1)
+        lse = torch.logsumexp(zf, dim=1)
+        tok[r0:r1] = arg.to(torch.int32) + self.model.vocab_offset
+        conf[r0:r1] = torch.exp(mx - lse)
+
+
+def reference_forward(model: RandomDLLM, x: torch.Tensor) -> torch.Tensor:
+    """Plain-PyTorch forward of the same model (no arena, no chunking): the
+    final hidden states [L, d], used as the executor's numerics reference."""
+    cfg = model.cfg
+    L, d, H = x.numel(), cfg.d_model, cfg.n_heads
+    h = model.w_embed.index_select(0, x)
+    for i in range(cfg.n_layers):
+        lw = model.layer(i)
+        q, k, v = (h @ lw["w_qkv"][:, j * d:(j + 1) * d] for j in range(3))
+        qh, kh, vh = (t.view(L, H, d // H).transpose(0, 1).unsqueeze(0) for t in (q, k, v))
+        a = F.scaled_dot_product_attention(qh, kh, vh).squeeze(0).transpose(0, 1).reshape(L, d)
+        h = h + a @ lw["w_attn_out"]
+        up = h @ lw["w_up"]
+        act = F.silu((h @ lw["w_gate"]).float()).mul(up.float()).to(torch.bfloat16) if cfg.gated_ffn else F.silu(up)
+        h = h + act @ lw["w_down"]
+    return h

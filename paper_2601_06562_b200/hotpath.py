@@ -133,6 +133,17 @@ def remask_commit(conf, pos, token, k: int, x, scratch, m_cap: int, m_dev=None, 
                  int(m_cap), int(k), _p(x), _p(selected), _p(scratch), _s(stream))
 
 
+# ----------------------------------------------------------------- K6
+def swiglu_(gate: torch.Tensor, up: torch.Tensor, stream=None) -> torch.Tensor:
+    """In place: up = silu(gate) * up (bf16), the chunked FFN's `glu` op."""
+    _req(gate, torch.bfloat16, "gate")
+    _req(up, torch.bfloat16, "up")
+    if gate.numel() != up.numel():
+        raise InputError("gate/up size mismatch")
+    _native.call("mosaic_swiglu", _p(gate), _p(up), up.numel(), _s(stream))
+    return up
+
+
 # ----------------------------------------------------------------- buffers
 class BufferLayout:
     """Bump layout of named buffers inside one device block (256 B aligned)."""
