@@ -39,6 +39,7 @@ from .vmm import Workspace
 from .workload import ModelConfig
 
 _INT32_TENSORS = {"token_out", "token_ids", "mask_idx"}
+ATTN_BLOCK = 32768  # query rows per attention call
 
 
 class RandomDLLM:
@@ -166,6 +167,8 @@ class StepExecutor:
         if x.dtype != torch.int32 or x.numel() != L:
             raise InputError("x must be int32 [L]")
         side = self._side_buffers(L)
+        kinds = {op.kind for op in g.ops}  # the graph, not the model config, fixes the logits mode
+        self._mode = "fused" if "lmhead_stats" in kinds else ("mask_only" if "gather_logits" in kinds else "eager")
         views = self._views(g, table, plan)
         kept: dict[str, torch.Tensor] = {}
         start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -207,8 +210,13 @@ class StepExecutor:
             H = cfg.n_heads
             dh = d // H
             qh, kh, vh = (t.view(L, H, dh).transpose(0, 1).unsqueeze(0) for t in (q, k, vv))
-            o = F.scaled_dot_product_attention(qh, kh, vh, is_causal=False)  # bidirectional dLLM attention
-            v[op.outputs[0]].view(L, H, dh).copy_(o.squeeze(0).transpose(0, 1))
+            out = v[op.outputs[0]].view(L, H, dh)
+            # bidirectional dLLM attention, query-blocked so the library's output
+            # temporary stays bounded ([ATTN_BLOCK, d]) at million-token contexts
+            for q0 in range(0, L, ATTN_BLOCK):
+                q1 = min(q0 + ATTN_BLOCK, L)
+                o = F.scaled_dot_product_attention(qh[:, :, q0:q1], kh, vh, is_causal=False)
+                out[q0:q1].copy_(o.squeeze(0).transpose(0, 1))
         elif kind == "add":
             a, c = (v[key] for key in op.inputs)
             torch.add(a, c, out=v[op.outputs[0]])
@@ -236,7 +244,7 @@ class StepExecutor:
         elif kind == "chunk_write":
             src, dst = op.inputs
             if src[0] == "logits":  # shift_mode=concat: logits chunk -> logits_all rows
-                r0, r1 = _rows(M if cfg.logits_mode == "mask_only" else L, b["K_logits"], op.iteration)
+                r0, r1 = _rows(M if self._mode == "mask_only" else L, b["K_logits"], op.iteration)
             else:
                 r0, r1 = _rows(L, b["K_FFN"], op.iteration)
             v[dst][r0:r1].copy_(v[src][: r1 - r0])
@@ -278,7 +286,7 @@ class StepExecutor:
             pass  # the shift was applied as a row remap when the logits were produced
         elif kind == "commit":
             tok, conf = v[op.inputs[0]], v[op.inputs[1]]
-            if cfg.logits_mode == "eager":  # rows are all positions: pick the masked ones
+            if self._mode == "eager":  # rows are all positions: pick the masked ones
                 tok = tok.index_select(0, mask_idx.long())
                 conf = conf.index_select(0, mask_idx.long())
             hotpath.remask_commit(conf[:M].contiguous(), mask_idx, tok[:M].contiguous(), k_unmask, x,
@@ -307,7 +315,7 @@ class StepExecutor:
         b = g.bindings
         cfg = self.cfg
         L, M = b["L"], b["M"]
-        if cfg.logits_mode == "fused":  # K4 over the K3 partial triples
+        if self._mode == "fused":  # K4 over the K3 partial triples
             src = v[op.inputs[0]]
             r0, r1 = _rows(M, b["K_logits"], op.iteration)
             if r1 <= r0:
@@ -327,7 +335,7 @@ class StepExecutor:
             r0, r1 = 0, z.shape[0]
         else:
             z, tok, conf = (v[key] for key in op.inputs)
-            rows = M if cfg.logits_mode == "mask_only" else L
+            rows = M if self._mode == "mask_only" else L
             r0, r1 = _rows(rows, b["K_logits"], op.iteration)
             z = z[: r1 - r0]
         zf = z.float()
