@@ -263,27 +263,50 @@ def gpu_main(args):
     # --------------------------------------------------------------- e2e: host buffers
     e2e = None
     if not args.no_e2e:
+        # Host-resident inputs (pinned), results read back every step. Steps are
+        # pipelined: the H2D copy of step i+1 runs on a copy stream into the
+        # other half of a double buffer while step i computes.
         xh = x0.cpu().pin_memory()
         Hh = H.cpu().pin_memory()
         xo = torch.empty_like(xh).pin_memory()
-        Hd = torch.empty_like(H)
-        xd = torch.empty_like(x0)
+        Hd = [torch.empty_like(H), torch.empty_like(H)]
+        xd = [torch.empty_like(x0), torch.empty_like(x0)]
+        copy_s = torch.cuda.Stream(device=dev)
+        ready = [torch.cuda.Event(), torch.cuda.Event()]
+        done = [torch.cuda.Event(), torch.cuda.Event()]
 
-        def e2e_step():
-            xd.copy_(xh, non_blocking=True)
-            Hd.copy_(Hh, non_blocking=True)
-            head.step(xd, Hd, k)
-            xo.copy_(xd, non_blocking=True)
+        def issue_copy(i, after=None):
+            b = i % 2
+            with torch.cuda.stream(copy_s):
+                if after is not None:
+                    copy_s.wait_event(after)
+                if i >= 2:
+                    copy_s.wait_event(done[b])  # buffer b free again
+                xd[b].copy_(xh, non_blocking=True)
+                Hd[b].copy_(Hh, non_blocking=True)
+                ready[b].record(copy_s)
 
-        for _ in range(3):
-            e2e_step()
+        def run(i):
+            b = i % 2
+            stream.wait_event(ready[b])
+            head.step(xd[b], Hd[b], k)
+            xo.copy_(xd[b], non_blocking=True)  # D2H of the step's result
+            done[b].record(stream)
+
+        def pipeline(n, start_event=None):
+            issue_copy(0, after=start_event)
+            for i in range(n):
+                if i + 1 < n:
+                    issue_copy(i + 1)
+                run(i)
+
+        pipeline(3)
         torch.cuda.synchronize()
         if world > 1:
             dist.barrier()
         s2, e2 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         s2.record(stream)
-        for _ in range(args.steps):
-            e2e_step()
+        pipeline(args.steps, start_event=s2)
         e2.record(stream)
         torch.cuda.synchronize()
         t2 = torch.tensor([s2.elapsed_time(e2)], device=dev, dtype=torch.float64)
@@ -291,7 +314,9 @@ def gpu_main(args):
             dist.all_reduce(t2, op=dist.ReduceOp.MAX)
         e2e = {"value": M * args.steps / (float(t2[0]) / 1e3), "unit": "masked tokens/s",
                "h2d_bytes_per_step": xh.numel() * 4 + Hh.numel() * 2,
-               "d2h_bytes_per_step": xo.numel() * 4}
+               "d2h_bytes_per_step": xo.numel() * 4,
+               "note": "pinned host H and x copied in every step (double-buffered copy stream overlapping the "
+                       "previous step's compute); updated x read back every step"}
 
     peaks = json.loads((ROOT / "MEASURED_PEAKS.json").read_text()) if (ROOT / "MEASURED_PEAKS.json").exists() else {}
     peak = peaks.get("bf16_tflops", 1590.0)
@@ -330,7 +355,7 @@ def gpu_main(args):
         "clocks": clocks.summary(),
         "e2e": e2e,
         "workspace_bytes": head.workspace_bytes,
-        "peak_activation_gb": torch.cuda.max_memory_allocated(dev) / 1e9 - (W.numel() * 2 + H.numel() * 2) / 1e9,
+        **context_fields(),
     }
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cpu = run_cpu_reference(steps=2, warmup=0)
@@ -340,6 +365,29 @@ def gpu_main(args):
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
+
+
+def context_fields() -> dict:
+    """Peak activation and max context of the full LLaDA-8B step (fused logits +
+    lazy chunking, first-fit arena): planned here in ~1 s with the graph planner;
+    the measured on-device sweep (bench_context.py) is read from profiles/."""
+    from paper_2601_06562_b200 import chunker, workload
+
+    cfg = workload.ModelConfig("llada_8b", 32, D, 12288, 32, VOCAB, 2, 16 * 2 ** 30, True, "fused", "none")
+    t = workload.build_layer_template(cfg)
+    peak = chunker.evaluate_peak(t, {"L": SEQ, "M": round(MASK_RATIO * SEQ)}, chunker.ChunkConfig(1, 1))
+    dense = chunker.evaluate_peak(workload.build_layer_template(
+        workload.ModelConfig("llada_8b", 32, D, 12288, 32, VOCAB, 2, 16 * 2 ** 30, True, "eager", "none")),
+        {"L": SEQ, "M": round(MASK_RATIO * SEQ)}, chunker.ChunkConfig(1, 1))
+    out = {"peak_activation_gb": peak.total_peak / 1e9, "peak_activation_gb_dense_logits_plan": dense.total_peak / 1e9}
+    sweep = ROOT / "profiles" / "r01_context_sweep.json"
+    if sweep.exists():
+        d = json.loads(sweep.read_text())
+        out["max_seq_len"] = d.get("pipeline_lmax_measured")
+        out["max_seq_len_planned"] = d.get("planned_lmax", {}).get("fused_chunking")
+        out["max_seq_len_dense_baseline"] = d.get("baseline_lmax")
+        out["max_seq_len_source"] = "profiles/r01_context_sweep.json (bench_context.py on one B200)"
+    return out
 
 
 def reference_main(args):

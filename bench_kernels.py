@@ -1,0 +1,118 @@
+"""Per-kernel throughput at the BASELINE.json shapes (one B200), CUDA events on
+the launching stream, inputs larger than L2 where the shape allows.
+
+    python bench_kernels.py [--out gpurun_out/kernels.json]
+
+K1/K2/K6 are reported as achieved HBM GB/s of algorithmic bytes against the
+measured copy bandwidth; K3 as TFLOP/s against the measured bf16 peak; K4/K5
+as latency.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import sys
+from pathlib import Path
+
+import torch
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+
+def timeit(fn, iters=20, warmup=3):
+    for _ in range(warmup):
+        fn()
+    torch.cuda.synchronize()
+    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    s.record()
+    for _ in range(iters):
+        fn()
+    e.record()
+    e.synchronize()
+    return s.elapsed_time(e) / iters
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--out", default="gpurun_out/kernels.json")
+    args = ap.parse_args()
+    from paper_2601_06562_b200 import _build, hotpath
+
+    _build.build()
+    dev = torch.device("cuda", 0)
+    peaks = json.loads((ROOT / "MEASURED_PEAKS.json").read_text()) if (ROOT / "MEASURED_PEAKS.json").exists() else {}
+    hbm = peaks.get("hbm_gbs", 6650.0)
+    tf = peaks.get("bf16_tflops", 1590.0)
+    out = {"peaks": {"hbm_gbs": hbm, "bf16_tflops": tf}}
+    g = torch.Generator(device=dev).manual_seed(0)
+
+    # K1 ---------------------------------------------------------------------
+    for L in (32768, 1 << 20, 1 << 22):
+        x = torch.randint(0, 1000, (L,), generator=g, device=dev, dtype=torch.int32)
+        x[L // 2:] = 999999
+        idx = torch.empty(L, dtype=torch.int32, device=dev)
+        m = torch.zeros(1, dtype=torch.int32, device=dev)
+        sc = torch.empty(hotpath.mask_compact_scratch_bytes(L), dtype=torch.uint8, device=dev)
+        ms = timeit(lambda: hotpath.mask_compact(x, 999999, idx, m, sc))
+        byts = 2 * 4 * L + 4 * (L // 2)  # x read twice + indices written
+        out[f"k1_compact_L{L}"] = {"ms": ms, "GBps": byts / ms / 1e6, "frac_hbm": byts / ms / 1e6 / hbm}
+
+    # K2 ---------------------------------------------------------------------
+    for name, L, d in (("llada", 32768, 4096), ("dream", 131072, 3584)):
+        M = L // 2
+        H = torch.randn(L, d, generator=g, device=dev).to(torch.bfloat16)
+        idx = torch.arange(L - M, L, device=dev, dtype=torch.int32)
+        hc = torch.empty(M, d, device=dev, dtype=torch.bfloat16)
+        ms = timeit(lambda: hotpath.gather_rows(H, idx, hc, m_host=M))
+        byts = 2 * 2 * M * d + 4 * M
+        out[f"k2_gather_{name}"] = {"ms": ms, "GBps": byts / ms / 1e6, "frac_hbm": byts / ms / 1e6 / hbm}
+        del H, hc
+
+    # K3 + K4 ----------------------------------------------------------------
+    for name, M, d, V in (("llada", 16384, 4096, 126464), ("dream", 65536, 3584, 152064),
+                          ("moe", 32768, 2048, 126464), ("tiny", 1024, 256, 8192),
+                          ("llada_shard8", 16384, 4096, 126464 // 8)):
+        hc = torch.randn(M, d, generator=g, device=dev).to(torch.bfloat16)
+        W = (torch.randn(V, d, generator=g, device=dev) * 0.02).to(torch.bfloat16)
+        S, tps = hotpath.lmhead_plan(M, V, d)
+        pm = torch.empty(S, M, device=dev)
+        ps = torch.empty(S, M, device=dev)
+        pa = torch.empty(S, M, device=dev, dtype=torch.int32)
+        it = 5 if M * V > 1e9 else 50
+        ms = timeit(lambda: hotpath.lmhead_stats(hc, W, S, pm, ps, pa, m_host=M), iters=it)
+        flops = 2.0 * M * d * V
+        tok = torch.empty(M, device=dev, dtype=torch.int32)
+        conf = torch.empty(M, device=dev)
+        lse = torch.empty(M, device=dev)
+        ms4 = timeit(lambda: hotpath.stats_merge(pm, ps, pa, S, M, M, m_host=M, token=tok, lse=lse, conf=conf))
+        out[f"k3_lmhead_{name}"] = {"M": M, "d": d, "V": V, "splits": S, "tiles_per_split": tps, "ms": ms,
+                                    "TFLOPs": flops / ms / 1e9, "frac_bf16_peak": flops / ms / 1e9 / tf,
+                                    "k4_merge_ms": ms4}
+        del hc, W
+
+    # K5 ---------------------------------------------------------------------
+    for M, k in ((16384, 256), (65536, 683), (524288, 8192)):
+        conf = torch.rand(M, generator=g, device=dev)
+        pos = torch.arange(M, device=dev, dtype=torch.int32)
+        tok = torch.zeros(M, device=dev, dtype=torch.int32)
+        x = torch.zeros(M, device=dev, dtype=torch.int32)
+        sc = torch.empty(hotpath.remask_scratch_bytes(), dtype=torch.uint8, device=dev)
+        ms = timeit(lambda: hotpath.remask_commit(conf, pos, tok, k, x, sc, M, m_host=M))
+        out[f"k5_remask_M{M}_k{k}"] = {"ms": ms}
+
+    # K6 ---------------------------------------------------------------------
+    for name, rows, f in (("llada_chunk", 32768, 12288), ("dream_chunk", 32768, 18944)):
+        gate = torch.randn(rows, f, generator=g, device=dev).to(torch.bfloat16)
+        up = torch.randn(rows, f, generator=g, device=dev).to(torch.bfloat16)
+        ms = timeit(lambda: hotpath.swiglu_(gate, up))
+        byts = 3 * 2 * rows * f
+        out[f"k6_swiglu_{name}"] = {"ms": ms, "GBps": byts / ms / 1e6, "frac_hbm": byts / ms / 1e6 / hbm}
+        del gate, up
+    print(json.dumps(out, indent=1))
+    Path(args.out).parent.mkdir(parents=True, exist_ok=True)
+    Path(args.out).write_text(json.dumps(out, indent=1) + "\n")
+
+
+if __name__ == "__main__":
+    main()

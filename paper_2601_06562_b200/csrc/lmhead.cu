@@ -62,6 +62,7 @@ struct Params {
   int32_t tiles_per_split;
   int32_t n_splits;
   int32_t group_m;
+  int32_t epilogue;  // 0 = skip the statistics math (power/overlap experiments only)
   int32_t policy;   // L2 policy of (A, B) loads: 0 = (evict_normal, evict_normal), 1 = (evict_last, evict_normal), 2 = (evict_normal, evict_first)
   int64_t v_offset;
   float* part_max;
@@ -245,7 +246,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll 1
         for (int c = 0; c < BN / 32; ++c) {
           const int64_t col0 = col_base + c * 32;
-          if (col0 >= p.V) break;  // warp-uniform: vocab tail
+          if (col0 >= p.V || !p.epilogue) break;  // warp-uniform: vocab tail
           float v[32];
           tmem_ld32(taddr + c * 32, v);
           if constexpr (kStoreLogits) {
@@ -432,6 +433,8 @@ int launch(const uint16_t* Hc, int64_t m_cap, const int32_t* m_dev, int64_t m_ho
   if (p.group_m <= 0) p.group_m = group_m_default() > 0 ? group_m_default() : 16;
   static const int policy = env_int("MOSAIC_L2_POLICY", 1);  // measured best: A evict_last
   p.policy = policy;
+  static const int epilogue = env_int("MOSAIC_K3_EPILOGUE", 1);
+  p.epilogue = epilogue;
   st = cg == 2 ? launch_cg<2, kStore>(ta, tb, p, m_cap, as_stream(stream))
                : launch_cg<1, kStore>(ta, tb, p, m_cap, as_stream(stream));
   if (st) return st;
