@@ -128,6 +128,30 @@ MOSAIC_API int mosaic_remask_commit(const float* conf, const int32_t* pos, const
  * workload.py:249-259). gate/up 16-byte aligned.                              */
 MOSAIC_API int mosaic_swiglu(const uint16_t* gate, uint16_t* up, int64_t n, void* stream);
 
+/* ---------------------------------------------------------------- K8/K9 ---
+ * MoE expert routing and combine for the chunked expert FFN (BASELINE
+ * configs[3]). The reference models MoE only as a top_k multiplier on the FFN
+ * chunk rows (mosaic/workload.py:195,238-253); these realise the routing those
+ * rows stand for.
+ * mosaic_moe_route: for each of `rows` router-logit rows (fp32, stride ld):
+ *   top_k experts by (logit desc, expert asc), weights = softmax over the
+ *   selected logits; assignments are ordered (expert, row, j) ascending:
+ *   disp_row[p] = row_base + row of dispatch slot p (and disp_w[p], optional),
+ *   comb_pos[row*top_k + j] = p, comb_w[row*top_k + j] = weight,
+ *   expert_off[0..E] = segment offsets (device int32, E+1 entries).
+ * `scratch` holds mosaic_moe_route_scratch_bytes(rows, E) bytes. E <= 256,
+ * top_k <= 16.
+ * mosaic_moe_combine: out[r, :] = sum_j comb_w[r*k+j] * src[comb_pos[r*k+j], :]
+ *   (bf16 in/out, fp32 accumulation in ascending j), d % 8 == 0.             */
+MOSAIC_API size_t mosaic_moe_route_scratch_bytes(int64_t rows, int32_t n_experts);
+MOSAIC_API int mosaic_moe_route(const float* logits, int64_t ld, int64_t rows, int32_t n_experts,
+                     int32_t top_k, int32_t row_base, int32_t* disp_row, float* disp_w,
+                     int32_t* comb_pos, float* comb_w, int32_t* expert_off, void* scratch,
+                     void* stream);
+MOSAIC_API int mosaic_moe_combine(const uint16_t* src, int64_t ld_src, const int32_t* comb_pos,
+                       const float* comb_w, int64_t rows, int32_t top_k, int64_t d,
+                       uint16_t* out, int64_t ld_out, void* stream);
+
 /* ---------------------------------------------------------------- K7 ------
  * Contiguous device workspace with lazy physical commitment (cuMem VMM):
  * reserve a VA range once, map physical granules for the prefix

@@ -51,6 +51,16 @@ SIGNATURES: dict[str, tuple[object, list[object]]] = {
          c_void_p, c_void_p],
     ),
     "mosaic_swiglu": (c_int, [c_void_p, c_void_p, c_int64, c_void_p]),
+    "mosaic_moe_route_scratch_bytes": (c_size_t, [c_int64, c_int32]),
+    "mosaic_moe_route": (
+        c_int,
+        [c_void_p, c_int64, c_int64, c_int32, c_int32, c_int32, c_void_p, c_void_p, c_void_p, c_void_p,
+         c_void_p, c_void_p, c_void_p],
+    ),
+    "mosaic_moe_combine": (
+        c_int,
+        [c_void_p, c_int64, c_void_p, c_void_p, c_int64, c_int32, c_int64, c_void_p, c_int64, c_void_p],
+    ),
     "mosaic_arena_reserve": (c_int, [c_int32, c_uint64, POINTER(c_void_p)]),
     "mosaic_arena_commit": (c_int, [c_void_p, c_uint64]),
     "mosaic_arena_info": (c_int, [c_void_p, _u64p, _u64p, _u64p, _u64p]),

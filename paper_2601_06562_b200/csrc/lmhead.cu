@@ -18,6 +18,7 @@
 // only global output is one (max, sum, arg) triple per row and split. Units are
 // numbered m-fastest inside groups of `group_m` m-blocks, so the ~148 units in
 // flight at once share a handful of W tiles and m-blocks through L2.
+#include <algorithm>
 #include <cstdlib>
 
 #include "common.cuh"
@@ -363,6 +364,12 @@ void plan_splits(int64_t m_cap, int64_t V, int32_t* n_splits, int32_t* tps) {
   const int64_t m_blocks = ceil_div(m_cap > 0 ? m_cap : 1, BM * cg);
   const int64_t workers = num_sms() / cg;
   int64_t best_cost = INT64_MAX, best_tps = n_tiles;
+  static const int forced_tps = env_int("MOSAIC_K3_TPS", 0);  // schedule experiments only
+  if (forced_tps > 0 && ceil_div(n_tiles, std::min<int64_t>(forced_tps, n_tiles)) <= kMaxSplits) {
+    *tps = static_cast<int32_t>(std::min<int64_t>(forced_tps, n_tiles));
+    *n_splits = static_cast<int32_t>(ceil_div(n_tiles, *tps));
+    return;
+  }
   for (int64_t t = n_tiles; t >= 1; --t) {
     const int64_t S = ceil_div(n_tiles, t);
     if (S > kMaxSplits) break;

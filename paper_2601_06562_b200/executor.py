@@ -38,7 +38,7 @@ from .planner import MemoryPlan, plan_first_fit
 from .vmm import Workspace
 from .workload import ModelConfig
 
-_INT32_TENSORS = {"token_out", "token_ids", "mask_idx"}
+_INT32_TENSORS = {"token_out", "token_ids", "mask_idx", "route_row", "route_pos", "expert_off"}
 ATTN_BLOCK = 32768  # query rows per attention call
 
 
@@ -53,8 +53,9 @@ class RandomDLLM:
 
     def __init__(self, cfg: ModelConfig, device, seed: int = 0, distinct_layers: Optional[int] = None,
                  vocab_shard: tuple[int, int] | None = None):
-        if cfg.moe is not None:
-            raise InputError("MoE expert execution is not implemented in the executor yet")
+        if cfg.moe is not None and cfg.logits_mode != "fused":
+            raise InputError("MoE models execute through the fused template (logits_mode='fused'), "
+                             "whose FFN block carries the expert routing")
         if cfg.element_size != 2:
             raise InputError("the executor runs bf16 models (element_size=2)")
         self.cfg = cfg
@@ -68,11 +69,18 @@ class RandomDLLM:
         self.w_embed = w(V, d, scale=1.0)
         n_sets = cfg.n_layers if distinct_layers is None else max(1, min(distinct_layers, cfg.n_layers))
         self.layers = []
+        E = cfg.moe.n_experts if cfg.moe else None
         for _ in range(n_sets):
-            lw = {"w_qkv": w(d, 3 * d), "w_attn_out": w(d, d, scale=0.02 * out_scale),
-                  "w_up": w(d, f), "w_down": w(f, d, scale=0.02 * out_scale)}
-            if cfg.gated_ffn:
-                lw["w_gate"] = w(d, f)
+            lw = {"w_qkv": w(d, 3 * d), "w_attn_out": w(d, d, scale=0.02 * out_scale)}
+            if E is None:
+                lw.update(w_up=w(d, f), w_down=w(f, d, scale=0.02 * out_scale))
+                if cfg.gated_ffn:
+                    lw["w_gate"] = w(d, f)
+            else:  # experts stacked [E, d, f] / [E, f, d]; router [d, E]
+                lw.update(w_router=w(d, E, scale=1.0 / math.sqrt(d)), w_up=w(E, d, f),
+                          w_down=w(E, f, d, scale=0.02 * out_scale))
+                if cfg.gated_ffn:
+                    lw["w_gate"] = w(E, d, f)
             self.layers.append(lw)
         v0, v1 = vocab_shard or (0, V)
         self.vocab_offset = v0
@@ -123,6 +131,9 @@ class StepExecutor:
                 "compact": torch.empty(hotpath.mask_compact_scratch_bytes(L), dtype=torch.uint8, device=self.device),
                 "remask": torch.empty(hotpath.remask_scratch_bytes(), dtype=torch.uint8, device=self.device),
             }}
+            if self.cfg.moe is not None:  # K8 per-CTA expert histogram (graph-input-like scratch)
+                self._side[L]["route"] = torch.empty(
+                    hotpath.moe_route_scratch_bytes(L, self.cfg.moe.n_experts), dtype=torch.uint8, device=self.device)
         return self._side[L]
 
     def _views(self, g: ConcreteGraph, table: LifetimeTable, plan: MemoryPlan) -> dict[InstKey, torch.Tensor]:
@@ -137,7 +148,7 @@ class StepExecutor:
                 es = t.tensor(tid).element_size
                 if es == 2:
                     dtype = torch.bfloat16
-                elif tid in _INT32_TENSORS:
+                elif tid.rsplit(".", 1)[-1] in _INT32_TENSORS:
                     dtype = torch.int32
                 else:
                     dtype = torch.float32
@@ -224,6 +235,8 @@ class StepExecutor:
             out = v[op.outputs[0]]
             if op.outputs[0][0].endswith("ffn_acc"):
                 out.zero_()
+        elif kind.startswith("moe_") or (self.cfg.moe is not None and kind in ("ffn_up", "ffn_gate", "ffn_down")):
+            self._moe(op, g, v, side)
         elif kind in ("ffn_up", "ffn_gate"):
             layer = self._layer(op.op_id)
             r0, r1 = _rows(L, b["K_FFN"], op.iteration)
@@ -231,11 +244,12 @@ class StepExecutor:
             torch.matmul(v[op.inputs[0]][r0:r1], w, out=v[op.outputs[0]][: r1 - r0])
         elif kind == "glu":
             r0, r1 = _rows(L, b["K_FFN"], op.iteration)
+            n = (r1 - r0) * (cfg.moe.top_k if cfg.moe else 1)
             up, gate = v[op.inputs[0]], v[op.inputs[1]]
-            hotpath.swiglu_(gate[: r1 - r0], up[: r1 - r0])  # act shares storage with up (in place)
+            hotpath.swiglu_(gate[:n], up[:n])  # act shares storage with up (in place)
         elif kind == "activation":
             r0, r1 = _rows(L, b["K_FFN"], op.iteration)
-            up = v[op.inputs[0]][: r1 - r0]
+            up = v[op.inputs[0]][: (r1 - r0) * (cfg.moe.top_k if cfg.moe else 1)]
             up.copy_(F.silu(up))
         elif kind == "ffn_down":
             layer = self._layer(op.op_id)
@@ -291,6 +305,44 @@ class StepExecutor:
                 conf = conf.index_select(0, mask_idx.long())
             hotpath.remask_commit(conf[:M].contiguous(), mask_idx, tok[:M].contiguous(), k_unmask, x,
                                   side["remask"], M, m_host=M)
+        else:
+            raise InputError(f"no executor for op kind {kind!r} ({op.label})")
+
+    def _moe(self, op, g: ConcreteGraph, v, side) -> None:
+        """The MoE FFN chunk (workload._moe_ffn_block): K8 routing, K2 dispatch
+        gather, per-expert cuBLAS GEMMs on the expert segments, K9 combine."""
+        cfg = self.cfg
+        E, k = cfg.moe.n_experts, cfg.moe.top_k
+        L = g.bindings["L"]
+        r0, r1 = _rows(L, g.bindings["K_FFN"], op.iteration)
+        n = r1 - r0
+        kind = op.kind
+        if n <= 0:
+            if kind == "moe_route":
+                v[op.outputs[3]].zero_()
+                self._moe_off = [0] * (E + 1)
+            return
+        lw = self._layer(op.op_id)
+        if kind == "moe_router":
+            h = v[op.inputs[0]]
+            torch.mm(h[r0:r1], lw["w_router"], out_dtype=torch.float32, out=v[op.outputs[0]][:n])
+        elif kind == "moe_route":
+            rrow, rpos, rw, off = (v[key] for key in op.outputs)
+            hotpath.moe_route(v[op.inputs[0]][:n], k, rrow, rpos, rw, off, side["route"], row_base=r0)
+            self._moe_off = off.tolist()  # segment bounds for the per-expert GEMMs (host sync)
+        elif kind == "moe_dispatch":
+            h, rrow = (v[key] for key in op.inputs)
+            hotpath.gather_rows(h, rrow, v[op.outputs[0]][: n * k], m_host=n * k)
+        elif kind in ("ffn_up", "ffn_gate", "ffn_down"):
+            src, out = v[op.inputs[0]], v[op.outputs[0]]
+            w = lw["w_up" if kind == "ffn_up" else "w_gate" if kind == "ffn_gate" else "w_down"]
+            off = self._moe_off
+            for e in range(E):
+                if off[e + 1] > off[e]:
+                    torch.matmul(src[off[e]:off[e + 1]], w[e], out=out[off[e]:off[e + 1]])
+        elif kind == "moe_combine":
+            src, rpos, rw, acc = (v[key] for key in op.inputs)
+            hotpath.moe_combine(src[: n * k], rpos, rw, k, acc[r0:r1])
         else:
             raise InputError(f"no executor for op kind {kind!r} ({op.label})")
 
@@ -357,7 +409,31 @@ def reference_forward(model: RandomDLLM, x: torch.Tensor) -> torch.Tensor:
         qh, kh, vh = (t.view(L, H, d // H).transpose(0, 1).unsqueeze(0) for t in (q, k, v))
         a = F.scaled_dot_product_attention(qh, kh, vh).squeeze(0).transpose(0, 1).reshape(L, d)
         h = h + a @ lw["w_attn_out"]
+        if cfg.moe is not None:
+            h = h + _moe_reference(cfg, lw, h)
+            continue
         up = h @ lw["w_up"]
         act = F.silu((h @ lw["w_gate"]).float()).mul(up.float()).to(torch.bfloat16) if cfg.gated_ffn else F.silu(up)
         h = h + act @ lw["w_down"]
     return h
+
+
+def _moe_reference(cfg: ModelConfig, lw: dict, h: torch.Tensor) -> torch.Tensor:
+    """Plain-PyTorch MoE FFN with the routing rule of K8: top-k by (logit desc,
+    expert asc) over fp32 router logits, softmax over the selected logits,
+    per-expert SwiGLU FFN, weighted fp32 sum."""
+    E, k = cfg.moe.n_experts, cfg.moe.top_k
+    logits = torch.mm(h, lw["w_router"], out_dtype=torch.float32)
+    vals, idx = torch.sort(logits, dim=1, descending=True, stable=True)
+    sel, wts = idx[:, :k], torch.softmax(vals[:, :k], dim=1)
+    out = torch.zeros(h.shape, dtype=torch.float32, device=h.device)
+    for e in range(E):
+        rows, j = (sel == e).nonzero(as_tuple=True)
+        if rows.numel() == 0:
+            continue
+        x = h.index_select(0, rows)
+        up = x @ lw["w_up"][e]
+        act = F.silu((x @ lw["w_gate"][e]).float()).mul(up.float()).to(torch.bfloat16) if cfg.gated_ffn \
+            else F.silu(up)
+        out.index_add_(0, rows, wts[rows, j].unsqueeze(1) * (act @ lw["w_down"][e]).float())
+    return out.to(torch.bfloat16)

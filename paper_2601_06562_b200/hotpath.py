@@ -144,6 +144,47 @@ def swiglu_(gate: torch.Tensor, up: torch.Tensor, stream=None) -> torch.Tensor:
     return up
 
 
+# ----------------------------------------------------------------- K8 / K9 (MoE FFN)
+def moe_route_scratch_bytes(rows: int, n_experts: int) -> int:
+    return int(_native.value("mosaic_moe_route_scratch_bytes", rows, n_experts))
+
+
+def moe_route(logits: torch.Tensor, top_k: int, disp_row: torch.Tensor, comb_pos: torch.Tensor,
+              comb_w: torch.Tensor, expert_off: torch.Tensor, scratch: torch.Tensor, row_base: int = 0,
+              disp_w: Optional[torch.Tensor] = None, stream=None) -> None:
+    """Top-k routing of router logits [rows, E] (fp32) and the stable
+    (expert, row, j) dispatch order; see include/mosaic_b200.h K8."""
+    if logits.dtype != torch.float32 or logits.dim() != 2 or logits.stride(1) != 1 or not logits.is_cuda:
+        raise InputError("router logits must be a 2-D fp32 CUDA tensor with contiguous rows")
+    rows, E = logits.shape
+    n = rows * int(top_k)
+    for t, dt, name in ((disp_row, torch.int32, "disp_row"), (comb_pos, torch.int32, "comb_pos"),
+                        (comb_w, torch.float32, "comb_w"), (expert_off, torch.int32, "expert_off")):
+        _req(t, dt, name)
+    if disp_row.numel() < n or comb_pos.numel() < n or comb_w.numel() < n or expert_off.numel() < E + 1:
+        raise InputError("routing outputs too small")
+    if scratch.numel() * scratch.element_size() < moe_route_scratch_bytes(rows, E):
+        raise InputError("routing scratch too small")
+    _native.call("mosaic_moe_route", _p(logits), logits.stride(0), rows, E, int(top_k), int(row_base),
+                 _p(disp_row), _p(disp_w), _p(comb_pos), _p(comb_w), _p(expert_off), _p(scratch), _s(stream))
+
+
+def moe_combine(src: torch.Tensor, comb_pos: torch.Tensor, comb_w: torch.Tensor, top_k: int,
+                out: torch.Tensor, stream=None) -> None:
+    """out[r] = sum_j comb_w[r, j] * src[comb_pos[r, j]] (bf16, fp32 math)."""
+    if src.dtype != torch.bfloat16 or src.dim() != 2 or src.stride(1) != 1:
+        raise InputError("src must be 2-D bf16 with contiguous rows")
+    if out.dtype != torch.bfloat16 or out.dim() != 2 or out.stride(1) != 1 or out.shape[1] != src.shape[1]:
+        raise InputError("out must be 2-D bf16 [rows, d] with contiguous rows")
+    _req(comb_pos, torch.int32, "comb_pos")
+    _req(comb_w, torch.float32, "comb_w")
+    rows = out.shape[0]
+    if comb_pos.numel() < rows * top_k or comb_w.numel() < rows * top_k:
+        raise InputError("combine tables too small")
+    _native.call("mosaic_moe_combine", _p(src), src.stride(0), _p(comb_pos), _p(comb_w), rows, int(top_k),
+                 src.shape[1], _p(out), out.stride(0), _s(stream))
+
+
 # ----------------------------------------------------------------- buffers
 class BufferLayout:
     """Bump layout of named buffers inside one device block (256 B aligned)."""

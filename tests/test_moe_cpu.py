@@ -1,0 +1,101 @@
+"""CPU checks of the MoE expert-FFN extension: the routing restatement in the
+oracle (closed form; UNPINNED by the reference, which has no routing) and the
+executable MoE template registered through the reference's graph API."""
+from dataclasses import replace
+
+import numpy as np
+import pytest
+
+import mosaic_oracle as orc
+
+
+def test_route_closed_form_small():
+    z = np.array([[0.0, 2.0, 1.0, 2.0],   # tie 1 vs 3 -> 1 first
+                  [5.0, -1.0, 5.0, 5.0]])  # three-way tie -> 0, 2
+    r = orc.moe_route(z, 2)
+    assert r["experts"].tolist() == [[1, 3], [0, 2]]
+    # dispatch order (expert, row, j): e0 <- (1,0); e1 <- (0,0); e2 <- (1,1); e3 <- (0,1)
+    assert r["disp_row"].tolist() == [1, 0, 1, 0]
+    assert r["comb_pos"].tolist() == [[1, 3], [0, 2]]
+    assert r["expert_off"].tolist() == [0, 1, 2, 3, 4]
+    assert np.allclose(r["comb_w"], 0.5)
+
+
+@pytest.mark.parametrize("rows,E,k", [(50, 8, 2), (200, 64, 8), (17, 5, 5)])
+def test_route_properties(rows, E, k):
+    rng = np.random.default_rng(rows)
+    z = rng.standard_normal((rows, E))
+    r = orc.moe_route(z, k, row_base=100)
+    assert np.allclose(r["comb_w"].sum(axis=1), 1.0)
+    assert np.all(np.diff(r["comb_w"], axis=1) <= 1e-15)  # weights follow logit order
+    off = r["expert_off"]
+    assert off[0] == 0 and off[-1] == rows * k and np.all(np.diff(off) >= 0)
+    # every (row, j) lands in its expert's segment, rows ascending inside a segment
+    for e in range(E):
+        seg = r["disp_row"][off[e]:off[e + 1]]
+        assert np.all(np.diff(seg) > 0)
+    pos = r["comb_pos"]
+    assert sorted(pos.reshape(-1).tolist()) == list(range(rows * k))
+    assert np.array_equal(r["disp_row"][pos] - 100, np.repeat(np.arange(rows)[:, None], k, axis=1))
+    for rr in range(rows):
+        for j in range(k):
+            e = r["experts"][rr, j]
+            assert off[e] <= pos[rr, j] < off[e + 1]
+
+
+def test_combine_closed_form():
+    src = np.arange(12, dtype=np.float64).reshape(6, 2)
+    pos = np.array([[5, 0], [2, 3], [1, 4]])
+    w = np.array([[0.5, 0.5], [1.0, 0.0], [0.25, 0.75]])
+    out = orc.moe_combine(src, pos, w)
+    assert out.tolist() == [[5.0, 6.0], [4.0, 5.0], [6.5, 7.5]]
+
+
+def test_moe_template_registers_routing_in_the_ffn_loop():
+    from paper_2601_06562_b200 import chunker, workload
+
+    cfg = workload.toy_configs()["tiny_moe"]
+    t = workload.build_layer_template(cfg)
+    g = t.instantiate({"L": 2048, "M": 1024, "K_logits": 1, "K_FFN": 4})
+    kinds = [op.kind for op in g.ops if op.op_id.startswith("l0.")]
+    assert kinds.count("moe_route") == 4 and kinds.count("moe_combine") == 4
+    # chunk tensors scale with ceil(L/K) * top_k rows
+    assert t.instance_shape("l0.xin", g.bindings) == (512 * 2, 256)
+    assert t.instance_shape("l0.up", g.bindings) == (512 * 2, 128)
+    assert t.instance_shape("l0.expert_off", g.bindings) == (9,)
+    # the search chunks the MoE FFN when it is the bottleneck
+    peak1 = chunker.evaluate_peak(t, {"L": 8192, "M": 4096}, chunker.ChunkConfig(1, 1))
+    assert peak1.bottleneck == "ffn"
+    budget = (peak1.total_peak + peak1.non_chunkable_peak) // 2  # above the attention floor
+    out = chunker.search_bottleneck(t, {"L": 8192, "M": 4096}, budget)
+    assert out.config.k_ffn > 1 and out.reason == "fits"
+
+
+def test_moe_template_first_fit_is_tight_and_in_place():
+    from paper_2601_06562_b200 import liveness, planner, workload
+
+    cfg = workload.toy_configs()["tiny_moe"]
+    g = workload.build_layer_template(cfg).instantiate({"L": 4096, "M": 2048, "K_logits": 2, "K_FFN": 3})
+    table = liveness.analyze(g)
+    plan = planner.plan_first_fit(table)
+    planner.validate(plan, table)
+    assert plan.workspace_size == liveness.max_live(table)
+    grp = {m: gr.id for gr in table.groups for m in gr.members}
+    assert grp[("l0.down_e", 0)] == grp[("l0.xin", 0)]   # down writes over the dispatch rows
+    assert grp[("l0.act", 1)] == grp[("l0.up", 1)]
+
+
+def test_reference_modes_keep_the_reference_moe_template():
+    """mask_only/eager MoE templates stay the reference's (plans pinned to it);
+    the executor refuses them rather than guessing a routing."""
+    import torch
+
+    from paper_2601_06562_b200 import workload
+    from paper_2601_06562_b200.errors import InputError
+    from paper_2601_06562_b200.executor import RandomDLLM
+
+    cfg = replace(workload.toy_configs()["tiny_moe"], logits_mode="mask_only")
+    ops = {op.kind for op in workload.build_layer_template(cfg).ops}
+    assert "moe_route" not in ops and "ffn_up" in ops
+    with pytest.raises(InputError):
+        RandomDLLM(cfg, torch.device("cpu"))
