@@ -207,6 +207,10 @@ def gpu_main(args):
     x0[SEQ - M:] = MASK_ID
     x = x0.clone()
 
+    persist = int(os.environ.get("MOSAIC_L2_PERSIST_MB", "0")) << 20
+    if persist:
+        from paper_2601_06562_b200 import hotpath as _hp
+        _hp.l2_persisting_limit(persist)
     head = MaskOnlyHead(W, seq_len=SEQ, mask_id=MASK_ID, vocab_offset=v0, m_cap=M, group=group)
     stream = torch.cuda.current_stream()
     launches_per_step = 23

@@ -52,6 +52,21 @@ enum mosaic_status {
 MOSAIC_API int mosaic_abi_version(void);
 MOSAIC_API const char* mosaic_last_error(void);
 
+/* L2 set-aside for persisting (evict_last) lines on the current device:
+ * min(bytes, device maximum); *applied_out receives the limit now in force.
+ * K3 keeps its A operand evict_last, so the set-aside decides whether the
+ * gathered rows survive the LM-head weight stream in L2. Device-global.     */
+MOSAIC_API int mosaic_l2_persisting_limit(int64_t bytes, int64_t* applied_out);
+
+/* Native first-fit planner (host): groups given in placement order (the
+ * reference's def asc, size desc, id asc; mosaic/planner.py:107-142) with
+ * byte sizes and inclusive live intervals [def_idx, last_idx]; offsets_out[i]
+ * = lowest multiple of `alignment` that collides with no earlier-placed,
+ * lifetime-overlapping group; *workspace_out = max(offset + size).          */
+MOSAIC_API int mosaic_first_fit(int64_t n, const int64_t* sizes, const int64_t* def_idx,
+                     const int64_t* last_idx, int64_t alignment, int64_t* offsets_out,
+                     int64_t* workspace_out);
+
 /* ---------------------------------------------------------------- K1 ------
  * Mask compaction: idx_out[0..M) = ascending positions p with x[p] == mask_id,
  * *m_out = M (device int32). Restates np.flatnonzero(x == MASK_ID); the

@@ -23,6 +23,8 @@ _u64p = POINTER(c_uint64)
 SIGNATURES: dict[str, tuple[object, list[object]]] = {
     "mosaic_abi_version": (c_int, []),
     "mosaic_last_error": (c_char_p, []),
+    "mosaic_first_fit": (c_int, [c_int64, c_void_p, c_void_p, c_void_p, c_int64, c_void_p, POINTER(c_int64)]),
+    "mosaic_l2_persisting_limit": (c_int, [c_int64, POINTER(c_int64)]),
     "mosaic_mask_compact_scratch_bytes": (c_size_t, [c_int64]),
     "mosaic_mask_compact": (c_int, [c_void_p, c_int64, c_int32, c_void_p, c_void_p, c_void_p, c_void_p]),
     "mosaic_gather_rows": (

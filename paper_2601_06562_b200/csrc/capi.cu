@@ -64,3 +64,21 @@ void* driver_fn(const char* name) {
 extern "C" int mosaic_abi_version(void) { return 100; }
 
 extern "C" const char* mosaic_last_error(void) { return mosaic::g_last_error.c_str(); }
+
+// L2 set-aside for persisting accesses (the evict_last class of createpolicy /
+// access-policy windows). K3 marks its A operand (the gathered masked rows,
+// re-read once per vocab tile) evict_last; without a set-aside the hint has no
+// reserved capacity to protect those lines from the streamed LM-head weights.
+extern "C" int mosaic_l2_persisting_limit(int64_t bytes, int64_t* applied_out) {
+  int dev = 0;
+  MOSAIC_CUDA(cudaGetDevice(&dev));
+  int max_bytes = 0;
+  MOSAIC_CUDA(cudaDeviceGetAttribute(&max_bytes, cudaDevAttrMaxPersistingL2CacheSize, dev));
+  size_t want = bytes < 0 ? 0 : static_cast<size_t>(bytes);
+  if (want > static_cast<size_t>(max_bytes)) want = static_cast<size_t>(max_bytes);
+  MOSAIC_CUDA(cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, want));
+  size_t got = 0;
+  MOSAIC_CUDA(cudaDeviceGetLimit(&got, cudaLimitPersistingL2CacheSize));
+  if (applied_out) *applied_out = static_cast<int64_t>(got);
+  return MOSAIC_OK;
+}

@@ -370,14 +370,28 @@ void plan_splits(int64_t m_cap, int64_t V, int32_t* n_splits, int32_t* tps) {
     *n_splits = static_cast<int32_t>(ceil_div(n_tiles, *tps));
     return;
   }
+  // Pass 1: the least busiest-pair load (tiles). Pass 2: among loads within
+  // 0.5% of it, the unit length closest to kPreferTps tiles -- measured on B200
+  // (profiles/r01b_k3_schedule_sweep.txt): ~13-tile units keep the m-group's
+  // rows and the shared LM-head tiles L2-resident best, which lowers DRAM
+  // traffic and with it the power-capped clock penalty.
+  constexpr int64_t kPreferTps = 13;
+  auto cost_of = [&](int64_t t) { return ceil_div(m_blocks * ceil_div(n_tiles, t), workers) * t; };
   for (int64_t t = n_tiles; t >= 1; --t) {
     const int64_t S = ceil_div(n_tiles, t);
     if (S > kMaxSplits) break;
     if (ceil_div(n_tiles, S) != t) continue;  // same split count as a larger t
-    const int64_t units = m_blocks * S;
-    const int64_t cost = ceil_div(units, workers) * t;  // tiles on the busiest SM (pair)
-    if (cost < best_cost) {
-      best_cost = cost;
+    best_cost = std::min(best_cost, cost_of(t));
+  }
+  int64_t best_dist = INT64_MAX;
+  for (int64_t t = n_tiles; t >= 1; --t) {
+    const int64_t S = ceil_div(n_tiles, t);
+    if (S > kMaxSplits) break;
+    if (ceil_div(n_tiles, S) != t) continue;
+    if (cost_of(t) * 1000 > best_cost * 1005) continue;
+    const int64_t dist = t > kPreferTps ? t - kPreferTps : kPreferTps - t;
+    if (dist < best_dist) {
+      best_dist = dist;
       best_tps = t;
     }
   }

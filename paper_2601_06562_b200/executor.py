@@ -165,10 +165,12 @@ class StepExecutor:
 
     def run(self, g: ConcreteGraph, x: torch.Tensor, k_unmask: int,
             table: Optional[LifetimeTable] = None, plan: Optional[MemoryPlan] = None,
-            keep: tuple[str, ...] = ()) -> dict:
+            keep: tuple[str, ...] = (), profile: bool = False) -> dict:
         """Execute one step; ``x`` (int32 [L] on device) is updated in place.
         Returns timing/memory measurements and the instances named in ``keep``
-        (copied out of the arena before they can be overwritten)."""
+        (copied out of the arena before they can be overwritten). With
+        ``profile`` every op is bracketed by CUDA events on the current stream
+        and the result carries device milliseconds per op kind."""
         if table is None or plan is None:
             table, plan = self.plan(g)
         if plan.workspace_size > self.ws.committed_bytes:
@@ -190,10 +192,18 @@ class StepExecutor:
         skip_layers = set()
         if self.exec_layers is not None:
             skip_layers = {f"l{i}." for i in range(self.exec_layers, self.cfg.n_layers)}
+        marks = []
         for op in g.ops:
             if skip_layers and op.op_id[:op.op_id.find(".") + 1] in skip_layers:
                 continue
+            if profile:
+                e0 = torch.cuda.Event(enable_timing=True)
+                e0.record()
             self._dispatch(op, g, views, x, mask_idx, side, k_unmask)
+            if profile:
+                e1 = torch.cuda.Event(enable_timing=True)
+                e1.record()
+                marks.append((op.kind, e0, e1))
             for key in op.outputs:
                 if key[0] in keep:
                     kept[key[0] if key[1] is None else f"{key[0]}@{key[1]}"] = views[key].clone()
@@ -202,8 +212,12 @@ class StepExecutor:
                 kept["confidence"] = views[("confidence", None)].clone()
         end.record()
         end.synchronize()
+        by_kind: dict[str, float] = {}
+        for kind, e0, e1 in marks:
+            by_kind[kind] = by_kind.get(kind, 0.0) + e0.elapsed_time(e1)
         return {"ms": start.elapsed_time(end), "workspace_bytes": plan.workspace_size,
-                "committed_bytes": self.ws.committed_bytes, "ops": len(g.ops), "kept": kept}
+                "committed_bytes": self.ws.committed_bytes, "ops": len(g.ops), "kept": kept,
+                "ms_by_kind": by_kind}
 
     # ---------------------------------------------------------------- ops
     def _dispatch(self, op, g: ConcreteGraph, v, x, mask_idx, side, k_unmask: int) -> None:

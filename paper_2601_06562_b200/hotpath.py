@@ -45,6 +45,14 @@ def _req(t: torch.Tensor, dtype: torch.dtype, name: str, ndim: int | None = None
         raise InputError(f"{name} must be contiguous")
 
 
+def l2_persisting_limit(nbytes: int) -> int:
+    """Reserve up to ``nbytes`` of L2 for persisting (evict_last) lines on the
+    current device; returns the limit in force."""
+    got = ctypes.c_int64()
+    _native.call("mosaic_l2_persisting_limit", int(nbytes), ctypes.byref(got))
+    return got.value
+
+
 # ----------------------------------------------------------------- K1 / K2
 def mask_compact_scratch_bytes(L: int) -> int:
     return int(_native.value("mosaic_mask_compact_scratch_bytes", L))

@@ -31,6 +31,15 @@ def pytest_collection_modifyitems(config, items):
             item.add_marker(skip)
 
 
+@pytest.fixture(scope="session", autouse=True)
+def _built_library():
+    """The control plane's first-fit planner and every kernel live in the
+    in-tree C-ABI library; build it (no-op when fresh) before any test."""
+    from paper_2601_06562_b200 import _build
+
+    _build.build()
+
+
 @pytest.fixture(scope="session")
 def native_lib():
     from paper_2601_06562_b200 import _build, _native
