@@ -91,6 +91,28 @@ def main():
                                     "k4_merge_ms": ms4}
         del hc, W
 
+    # K3 gather mode (gather4 A operand straight from H; K2 and Hc disappear)
+    for name, L, d, V, layout in (("llada", 32768, 4096, 126464, "suffix"), ("llada_scattered", 32768, 4096, 126464,
+                                                                             "scattered")):
+        M = L // 2
+        H = torch.randn(L, d, generator=g, device=dev).to(torch.bfloat16)
+        W = (torch.randn(V, d, generator=g, device=dev) * 0.02).to(torch.bfloat16)
+        idx = (torch.arange(L - M, L, device=dev) if layout == "suffix" else
+               torch.randperm(L, generator=g, device=dev)[:M].sort().values).to(torch.int32)
+        S, tps = hotpath.lmhead_plan(M, V, d)
+        pm = torch.empty(S, M, device=dev)
+        ps = torch.empty(S, M, device=dev)
+        pa = torch.empty(S, M, device=dev, dtype=torch.int32)
+        ms = timeit(lambda: hotpath.lmhead_stats_gather(H, idx, W, S, pm, ps, pa, M, m_host=M), iters=5)
+        hc = torch.empty(M, d, device=dev, dtype=torch.bfloat16)
+        ms_sep = timeit(lambda: (hotpath.gather_rows(H, idx, hc, m_host=M),
+                                 hotpath.lmhead_stats(hc, W, S, pm, ps, pa, m_host=M)), iters=5)
+        flops = 2.0 * M * d * V
+        out[f"k3_gather_{name}"] = {"M": M, "d": d, "V": V, "splits": S, "ms": ms, "TFLOPs": flops / ms / 1e9,
+                                    "frac_bf16_peak": flops / ms / 1e9 / tf, "k2_plus_k3_ms": ms_sep,
+                                    "hc_bytes_saved": M * d * 2}
+        del H, W, hc
+
     # K5 ---------------------------------------------------------------------
     for M, k in ((16384, 256), (65536, 683), (524288, 8192)):
         conf = torch.rand(M, generator=g, device=dev)

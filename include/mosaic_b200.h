@@ -107,6 +107,17 @@ MOSAIC_API int mosaic_lmhead_stats(const uint16_t* Hc, int64_t m_cap, const int3
                         int32_t n_splits, float* part_max, float* part_sum, int32_t* part_arg,
                         void* stream);
 
+/* Gather mode of K3 -- the paper's gather-GEMM with no intermediate buffer:
+ * the A rows are read straight from the hidden states H [n_rows, d] (row
+ * stride ld_h elements) at the masked positions idx[0..M) (src(p) = p, or
+ * max(p-1, 0) with shift = 1) by TMA tile::gather4, so K2 and the [m_cap, d]
+ * compacted buffer disappear. Outputs as mosaic_lmhead_stats.                */
+MOSAIC_API int mosaic_lmhead_stats_gather(const uint16_t* H, int64_t n_rows, int64_t ld_h, const int32_t* idx,
+                               int32_t shift, int64_t m_cap, const int32_t* m_dev, int64_t m_host,
+                               const uint16_t* W, int64_t V_shard, int64_t d, int64_t v_offset,
+                               int32_t n_splits, float* part_max, float* part_sum, int32_t* part_arg,
+                               void* stream);
+
 /* Debug / parity path for the reference operator itself: out[r, v] =
  * <Hc[r, :], W[v, :]> in fp32, row stride ldo. Materialises the logits like
  * gather_gemm (kernel.py:68); the product path never calls it.               */

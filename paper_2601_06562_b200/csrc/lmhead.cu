@@ -49,7 +49,7 @@ struct Cfg {
   static constexpr int B_BYTES = B_ROWS * BK * 2;
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
   static constexpr int STAGES = CG == 1 ? 4 : 6;
-  static constexpr int SMEM = STAGES * STAGE_BYTES + 1024 + 256;
+  static constexpr int SMEM = STAGES * STAGE_BYTES + 1024 + 256 + BM * 4;  // + gather row indices
   static constexpr uint32_t IDESC = umma_idesc_bf16(ROWS, BN);
 };
 
@@ -71,6 +71,8 @@ struct Params {
   int32_t* part_arg;
   float* out;   // logits (debug path)
   int64_t ldo;
+  const int32_t* idx;  // gather mode: masked positions, A rows are H[src(idx[r])]
+  int32_t shift;       // gather mode: src(p) = max(p - 1, 0) (Dream token shift)
 };
 
 __device__ __forceinline__ void unit_coords(const Params& p, int m_blocks, int64_t u, int& mb,
@@ -108,7 +110,33 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, float (&v)[32]) {
   for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
 }
 
-template <int CG, bool kStoreLogits>
+// 2-D TMA gather of four K-major rows (64 bf16 columns each) by row index,
+// 128-byte swizzled like a plain box load; with CG == 2 the transaction bytes
+// complete on the pair leader's mbarrier.
+template <int CG>
+__device__ __forceinline__ void tma_gather4(void* smem_dst, const void* tmap, uint64_t* bar, int32_t col,
+                                            int4 rows, uint64_t policy) {
+  if constexpr (CG == 1)
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.tile::gather4.mbarrier::complete_tx::bytes.L2::cache_hint"
+        " [%0], [%1, {%3, %4, %5, %6, %7}], [%2], %8;" ::"r"(smem_u32(smem_dst)),
+        "l"(reinterpret_cast<uint64_t>(tmap)), "r"(smem_u32(bar)), "r"(col), "r"(rows.x), "r"(rows.y), "r"(rows.z),
+        "r"(rows.w), "l"(policy)
+        : "memory");
+  else
+    asm volatile(
+        "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.tile::gather4.mbarrier::complete_tx::bytes"
+        ".L2::cache_hint [%0], [%1, {%3, %4, %5, %6, %7}], [%2], %8;" ::"r"(smem_u32(smem_dst)),
+        "l"(reinterpret_cast<uint64_t>(tmap)), "r"(smem_u32(bar) & 0xFEFFFFFFu), "r"(col), "r"(rows.x),
+        "r"(rows.y), "r"(rows.z), "r"(rows.w), "l"(policy)
+        : "memory");
+}
+
+// kGather: the A operand is not a compacted [m, d] buffer but the hidden
+// states H themselves, fetched row by row with TMA gather4 at the masked
+// positions idx[] -- the gather-GEMM of the paper with no intermediate
+// buffer (K2 is skipped entirely).
+template <int CG, bool kStoreLogits, bool kGather = false>
 __global__ void __launch_bounds__(kThreads, 1)
     k3_lmhead(const __grid_constant__ CUtensorMap tmap_a, const __grid_constant__ CUtensorMap tmap_b,
               const Params p) {
@@ -123,6 +151,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* tfull = empty + C::STAGES;
   uint64_t* tempty = tfull + NUM_ACC;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + NUM_ACC);
+  int32_t* sidx = reinterpret_cast<int32_t*>(smem + C::STAGES * C::STAGE_BYTES + 256);  // gather rows
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -155,29 +184,54 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   if (warp == 0) {
     // ------------------------------------------------------------ TMA producer (both CTAs)
-    if (lane == 0) {
-      // A is re-read for every tile of a unit and by the units of its m-group;
-      // a W tile is shared by the m-blocks in flight at the same moment.
-      const uint64_t pol_a = p.policy == 1 ? policy_evict_last() : policy_evict_normal();
-      const uint64_t pol_b = p.policy == 2 ? policy_evict_first() : policy_evict_normal();
-      uint32_t stage = 0, phase = 0;
-      for (int64_t u = cluster; u < units; u += n_clusters) {
-        int mb, s;
-        unit_coords(p, m_blocks, u, mb, s);
-        const int t0 = s * p.tiles_per_split;
-        const int t1 = min(t0 + p.tiles_per_split, p.n_tiles);
-        const int a_row = mb * C::ROWS + rank * BM;
+    // A is re-read for every tile of a unit and by the units of its m-group;
+    // a W tile is shared by the m-blocks in flight at the same moment.
+    const uint64_t pol_a = p.policy == 1 ? policy_evict_last() : policy_evict_normal();
+    const uint64_t pol_b = p.policy == 2 ? policy_evict_first() : policy_evict_normal();
+    uint32_t stage = 0, phase = 0;
+    for (int64_t u = cluster; u < units; u += n_clusters) {
+      int mb, s;
+      unit_coords(p, m_blocks, u, mb, s);
+      const int t0 = s * p.tiles_per_split;
+      const int t1 = min(t0 + p.tiles_per_split, p.n_tiles);
+      const int a_row = mb * C::ROWS + rank * BM;
+      if constexpr (kGather) {
+        // this CTA's 128 source rows, once per unit (rows past M read row 0;
+        // their statistics are never stored)
+#pragma unroll
+        for (int j = 0; j < BM / 32; ++j) {
+          const int r = a_row + j * 32 + lane;
+          int v = r < M ? __ldg(p.idx + r) : 0;
+          if (p.shift) v = max(v - 1, 0);
+          sidx[j * 32 + lane] = v;
+        }
+        __syncwarp();
+      }
+      if (lane == 0) {
         for (int t = t0; t < t1; ++t) {
           const int b_row = t * BN + rank * C::B_ROWS;
           for (int kb = 0; kb < k_blocks; ++kb) {
             mbar_wait(&empty[stage], phase ^ 1);
             if (rank == 0) mbar_arrive_expect_tx(&full[stage], C::STAGE_BYTES * CG);
-            if constexpr (CG == 1) {
-              tma_load_2d(sA + stage * C::A_BYTES, &tmap_a, &full[stage], kb * BK, a_row, pol_a);
+            if constexpr (CG == 1)
               tma_load_2d(sB + stage * C::B_BYTES, &tmap_b, &full[stage], kb * BK, b_row, pol_b);
+            else
+              tma_load_2d_cg2(sB + stage * C::B_BYTES, &tmap_b, &full[stage], kb * BK, b_row, pol_b);
+            if constexpr (kGather) {
+              const uint32_t rows_addr = smem_u32(sidx);
+#pragma unroll 4
+              for (int i = 0; i < BM / 4; ++i) {
+                int4 r4;
+                asm volatile("ld.shared.v4.s32 {%0, %1, %2, %3}, [%4];"
+                             : "=r"(r4.x), "=r"(r4.y), "=r"(r4.z), "=r"(r4.w)
+                             : "r"(rows_addr + i * 16));
+                tma_gather4<CG>(sA + stage * C::A_BYTES + i * 4 * (BK * 2), &tmap_a, &full[stage], kb * BK,
+                                r4, pol_a);
+              }
+            } else if constexpr (CG == 1) {
+              tma_load_2d(sA + stage * C::A_BYTES, &tmap_a, &full[stage], kb * BK, a_row, pol_a);
             } else {
               tma_load_2d_cg2(sA + stage * C::A_BYTES, &tmap_a, &full[stage], kb * BK, a_row, pol_a);
-              tma_load_2d_cg2(sB + stage * C::B_BYTES, &tmap_b, &full[stage], kb * BK, b_row, pol_b);
             }
             if (++stage == C::STAGES) {
               stage = 0;
@@ -186,6 +240,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
         }
       }
+      __syncwarp();
     }
   } else if (warp == 1) {
     // ------------------------------------------------------------ MMA issuer (pair leader)
@@ -399,11 +454,11 @@ void plan_splits(int64_t m_cap, int64_t V, int32_t* n_splits, int32_t* tps) {
   *n_splits = static_cast<int32_t>(ceil_div(n_tiles, best_tps));
 }
 
-template <int CG, bool kStore>
+template <int CG, bool kStore, bool kGather>
 int launch_cg(const CUtensorMap& ta, const CUtensorMap& tb, const Params& p, int64_t m_cap,
               cudaStream_t stream) {
   using C = Cfg<CG>;
-  auto kern = k3_lmhead<CG, kStore>;
+  auto kern = k3_lmhead<CG, kStore, kGather>;
   static bool attr_set = false;  // per instantiation
   if (!attr_set) {
     MOSAIC_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
@@ -428,20 +483,46 @@ int launch_cg(const CUtensorMap& ta, const CUtensorMap& tb, const Params& p, int
   return MOSAIC_OK;
 }
 
+// A operand source: a dense [m_cap, d] buffer (Hc, K2's output) or, in gather
+// mode, the hidden states H [n_rows, d] (row stride ld_h) read at idx[].
+struct ASource {
+  const uint16_t* base;
+  int64_t rows;
+  int64_t ld;
+  const int32_t* idx;  // non-null = gather mode
+  int32_t shift;
+};
+
+int encode_rows_bf16(CUtensorMap* map, const void* base, int64_t rows, int64_t K, int64_t ld, int box_rows) {
+  static EncodeTiledFn fn = reinterpret_cast<EncodeTiledFn>(driver_fn("cuTensorMapEncodeTiled"));
+  if (!fn) return fail(MOSAIC_E_CUDA, "cuTensorMapEncodeTiled unavailable from the driver");
+  const cuuint64_t dims[2] = {static_cast<cuuint64_t>(K), static_cast<cuuint64_t>(rows)};
+  const cuuint64_t strides[1] = {static_cast<cuuint64_t>(ld) * 2};
+  const cuuint32_t box[2] = {BK, static_cast<cuuint32_t>(box_rows)};
+  const cuuint32_t elem_strides[2] = {1, 1};
+  CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box,
+                  elem_strides, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(MOSAIC_E_CUDA, "cuTensorMapEncodeTiled failed (%d)", int(r));
+  return MOSAIC_OK;
+}
+
 template <bool kStore>
-int launch(const uint16_t* Hc, int64_t m_cap, const int32_t* m_dev, int64_t m_host,
-           const uint16_t* W, int64_t V, int64_t d, Params p, void* stream) {
+int launch(const ASource& a, int64_t m_cap, const int32_t* m_dev, int64_t m_host, const uint16_t* W, int64_t V,
+           int64_t d, Params p, void* stream) {
   MOSAIC_REQUIRE(d > 0 && d % BK == 0, "d=%lld must be a positive multiple of %d", (long long)d, BK);
   MOSAIC_REQUIRE(V >= 1 && V < (int64_t(1) << 31), "vocab shard %lld out of range", (long long)V);
   MOSAIC_REQUIRE(m_cap >= 0 && m_cap < (int64_t(1) << 31), "m_cap out of range");
   MOSAIC_REQUIRE(m_dev != nullptr || (m_host >= 0 && m_host <= m_cap), "m_host=%lld > m_cap=%lld",
                  (long long)m_host, (long long)m_cap);
-  MOSAIC_REQUIRE((reinterpret_cast<uintptr_t>(Hc) & 15) == 0 && (reinterpret_cast<uintptr_t>(W) & 15) == 0,
-                 "Hc and W must be 16-byte aligned");
+  MOSAIC_REQUIRE((reinterpret_cast<uintptr_t>(a.base) & 15) == 0 && (reinterpret_cast<uintptr_t>(W) & 15) == 0,
+                 "A rows and W must be 16-byte aligned");
+  MOSAIC_REQUIRE(a.ld >= d && a.ld % 8 == 0, "row stride %lld must be >= d and a multiple of 8", (long long)a.ld);
   if (m_cap == 0) return MOSAIC_OK;
+  const bool gather = a.idx != nullptr;
   const int cg = cta_group_for(m_cap);
   CUtensorMap ta, tb;
-  int st = encode_kmajor_bf16(&ta, Hc, m_cap, d, BM);
+  int st = gather ? encode_rows_bf16(&ta, a.base, a.rows, d, a.ld, 1) : encode_rows_bf16(&ta, a.base, m_cap, d, a.ld, BM);
   if (st) return st;
   st = encode_kmajor_bf16(&tb, W, V, d, BN / cg);
   if (st) return st;
@@ -451,13 +532,20 @@ int launch(const uint16_t* Hc, int64_t m_cap, const int32_t* m_dev, int64_t m_ho
   p.V = V;
   p.K = static_cast<int32_t>(d);
   p.n_tiles = static_cast<int32_t>(ceil_div(V, BN));
+  p.idx = a.idx;
+  p.shift = a.shift;
   if (p.group_m <= 0) p.group_m = group_m_default() > 0 ? group_m_default() : 16;
   static const int policy = env_int("MOSAIC_L2_POLICY", 1);  // measured best: A evict_last
   p.policy = policy;
   static const int epilogue = env_int("MOSAIC_K3_EPILOGUE", 1);
   p.epilogue = epilogue;
-  st = cg == 2 ? launch_cg<2, kStore>(ta, tb, p, m_cap, as_stream(stream))
-               : launch_cg<1, kStore>(ta, tb, p, m_cap, as_stream(stream));
+  cudaStream_t s = as_stream(stream);
+  if (gather) {
+    if constexpr (kStore) return fail(MOSAIC_E_UNSUPPORTED, "gather mode has no logits debug path");
+    else st = cg == 2 ? launch_cg<2, false, true>(ta, tb, p, m_cap, s) : launch_cg<1, false, true>(ta, tb, p, m_cap, s);
+  } else {
+    st = cg == 2 ? launch_cg<2, kStore, false>(ta, tb, p, m_cap, s) : launch_cg<1, kStore, false>(ta, tb, p, m_cap, s);
+  }
   if (st) return st;
   return check_launch(kStore ? "mosaic_lmhead_logits" : "mosaic_lmhead_stats");
 }
@@ -492,7 +580,30 @@ extern "C" int mosaic_lmhead_stats(const uint16_t* Hc, int64_t m_cap, const int3
   p.part_max = part_max;
   p.part_sum = part_sum;
   p.part_arg = part_arg;
-  return launch<false>(Hc, m_cap, m_dev, m_host, W, V_shard, d, p, stream);
+  return launch<false>(ASource{Hc, m_cap, d, nullptr, 0}, m_cap, m_dev, m_host, W, V_shard, d, p, stream);
+}
+
+extern "C" int mosaic_lmhead_stats_gather(const uint16_t* H, int64_t n_rows, int64_t ld_h, const int32_t* idx,
+                                          int32_t shift, int64_t m_cap, const int32_t* m_dev, int64_t m_host,
+                                          const uint16_t* W, int64_t V_shard, int64_t d, int64_t v_offset,
+                                          int32_t n_splits, float* part_max, float* part_sum, int32_t* part_arg,
+                                          void* stream) {
+  MOSAIC_REQUIRE(H && idx && part_max && part_sum && part_arg, "null operands");
+  MOSAIC_REQUIRE(n_rows >= 1 && n_rows < (int64_t(1) << 31), "n_rows out of range");
+  const int64_t n_tiles = ceil_div(V_shard, BN);
+  MOSAIC_REQUIRE(n_splits >= 1 && n_splits <= n_tiles, "n_splits=%d not in [1, %lld]", n_splits,
+                 (long long)n_tiles);
+  Params p{};
+  p.tiles_per_split = static_cast<int32_t>(ceil_div(n_tiles, n_splits));
+  p.n_splits = static_cast<int32_t>(ceil_div(n_tiles, p.tiles_per_split));
+  MOSAIC_REQUIRE(p.n_splits == n_splits, "n_splits=%d does not tile %lld vocab tiles evenly; use mosaic_lmhead_plan",
+                 n_splits, (long long)n_tiles);
+  p.v_offset = v_offset;
+  p.part_max = part_max;
+  p.part_sum = part_sum;
+  p.part_arg = part_arg;
+  return launch<false>(ASource{H, n_rows, ld_h, idx, shift ? 1 : 0}, m_cap, m_dev, m_host, W, V_shard, d, p,
+                       stream);
 }
 
 extern "C" int mosaic_lmhead_logits(const uint16_t* Hc, int64_t m_cap, const int32_t* m_dev,
@@ -505,5 +616,5 @@ extern "C" int mosaic_lmhead_logits(const uint16_t* Hc, int64_t m_cap, const int
   p.n_splits = 1;
   p.out = out;
   p.ldo = ldo;
-  return launch<true>(Hc, m_cap, m_dev, m_host, W, V_shard, d, p, stream);
+  return launch<true>(ASource{Hc, m_cap, d, nullptr, 0}, m_cap, m_dev, m_host, W, V_shard, d, p, stream);
 }

@@ -111,6 +111,30 @@ def lmhead_stats(hc: torch.Tensor, weight: torch.Tensor, n_splits: int, part_max
                  _p(part_arg), _s(stream))
 
 
+def lmhead_stats_gather(hidden: torch.Tensor, idx: torch.Tensor, weight: torch.Tensor, n_splits: int,
+                        part_max: torch.Tensor, part_sum: torch.Tensor, part_arg: torch.Tensor, m_cap: int,
+                        m_dev=None, m_host: int = 0, shift: bool = False, v_offset: int = 0, stream=None) -> None:
+    """K3 in gather mode: the A rows come straight from ``hidden`` [n, d] at
+    the masked positions ``idx`` (TMA gather4), no compacted buffer."""
+    if hidden.dtype != torch.bfloat16 or hidden.dim() != 2 or hidden.stride(1) != 1 or not hidden.is_cuda:
+        raise InputError("hidden must be a 2-D bf16 CUDA tensor with contiguous rows")
+    _req(idx, torch.int32, "idx", 1)
+    _req(weight, torch.bfloat16, "weight", 2)
+    d = hidden.shape[1]
+    if weight.shape[1] != d:
+        raise InputError(f"weight is {tuple(weight.shape)}, expected [V, {d}]")
+    if idx.numel() < m_cap:
+        raise InputError("idx must hold m_cap entries")
+    for t, dt, n in ((part_max, torch.float32, "part_max"), (part_sum, torch.float32, "part_sum"),
+                     (part_arg, torch.int32, "part_arg")):
+        _req(t, dt, n)
+        if t.numel() < n_splits * m_cap:
+            raise InputError(f"{n} must hold n_splits*m_cap entries")
+    _native.call("mosaic_lmhead_stats_gather", _p(hidden), hidden.shape[0], hidden.stride(0), _p(idx),
+                 int(bool(shift)), int(m_cap), _p(m_dev), int(m_host), _p(weight), weight.shape[0], d,
+                 int(v_offset), int(n_splits), _p(part_max), _p(part_sum), _p(part_arg), _s(stream))
+
+
 def lmhead_logits(hc: torch.Tensor, weight: torch.Tensor, out: torch.Tensor, m_dev=None,
                   m_host: int = 0, stream=None) -> None:
     _req(hc, torch.bfloat16, "hc", 2)
@@ -270,7 +294,7 @@ class MaskOnlyHead:
         lay.add("part_max", (S, m), torch.float32)
         lay.add("part_sum", (S, m), torch.float32)
         lay.add("part_arg", (S, m), torch.int32)
-        if P > 1:
+        if group is not None:  # the exchange path runs whenever a process group is given (even P = 1)
             lay.add("local", (3, m), torch.float32)     # merged (max, sum, arg-bits) of this shard
             lay.add("gathered", (P, 3, m), torch.float32)
         lay.add("token", (m,), torch.int32)
@@ -299,7 +323,7 @@ class MaskOnlyHead:
         lmhead_stats(b["hc"], self.weight, self.n_splits, b["part_max"], b["part_sum"],
                      b["part_arg"], m_dev=m_dev, v_offset=self.vocab_offset, stream=stream)
         m, S = self.m_cap, self.n_splits
-        if self.world == 1:
+        if self.group is None:
             stats_merge(b["part_max"], b["part_sum"], b["part_arg"], S, m, m, m_dev=m_dev,
                         token=b["token"], lse=b["lse"], conf=b["conf"], stream=stream)
         else:

@@ -311,3 +311,91 @@ def test_swiglu_vs_torch_fp32(dev, n):
     hotpath.swiglu_(gate, up)
     torch.testing.assert_close(up.float(), want.float(), rtol=1e-2, atol=1e-2)
     assert (up != want).float().mean() < 0.01  # differs only by fp32 exp rounding
+
+
+def test_nccl_exchange_path_world1(dev):
+    """The vocab-sharded path end to end on one GPU: a real NCCL process group
+    (world 1) drives K4 -> all_gather_into_tensor -> rank-order K4 merge; the
+    result must equal the ungrouped step bit for bit (merging one triple is
+    the identity)."""
+    import socket
+
+    import torch.distributed as dist
+
+    from paper_2601_06562_b200 import MaskOnlyHead
+
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    dist.init_process_group("nccl", init_method=f"tcp://127.0.0.1:{port}", rank=0, world_size=1, device_id=dev)
+    try:
+        rng = np.random.default_rng(21)
+        L, d, V, mask_id, k = 4096, 512, 16384, 16383, 100
+        x = rng.integers(0, V - 1, size=L).astype(np.int32)
+        x[rng.random(L) < 0.5] = mask_id
+        H = bf16_tensor(rng.standard_normal((L, d)), dev)
+        W = bf16_tensor(rng.standard_normal((V, d)) * 0.05, dev)
+        outs = []
+        for group in (None, dist.group.WORLD):
+            head = MaskOnlyHead(W, seq_len=L, mask_id=mask_id, group=group)
+            xd = torch.from_numpy(x).to(dev)
+            o = head.step(xd, H, k)
+            torch.cuda.synchronize()
+            M = int(o.m_dev.item())
+            outs.append((xd.cpu(), o.token[:M].cpu(), o.lse[:M].cpu(), o.conf[:M].cpu()))
+        for a, b in zip(*outs):
+            assert torch.equal(a, b)
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("L,d,V,m,layout,shift", [(4096, 256, 8192, 2000, "scattered", False),
+                                                  (4096, 256, 8192, 2000, "scattered", True),
+                                                  (300, 512, 1000, 100, "suffix", False),      # M <= 128 -> cg1
+                                                  (9000, 4096, 126464 // 8 + 5, 4500, "scattered", False),
+                                                  (20000, 3584, 19008, 10000, "suffix", True)])
+def test_lmhead_gather_mode_equals_gathered_buffer(dev, L, d, V, m, layout, shift):
+    """K3 with the A operand gathered by TMA gather4 from H must be bit-identical
+    to K2 (gather into Hc) followed by the dense-A K3: same operands, same
+    MMA order, same epilogue."""
+    from paper_2601_06562_b200 import hotpath
+
+    rng = np.random.default_rng(L + m)
+    H = bf16_tensor(rng.standard_normal((L, d)), dev)
+    W = bf16_tensor(rng.standard_normal((V, d)) * 0.03, dev)
+    pos = np.arange(L - m, L) if layout == "suffix" else np.sort(rng.choice(L, m, replace=False))
+    idx = torch.from_numpy(pos.astype(np.int32)).to(dev)
+    cap = m + 37  # capacity larger than M: rows past M never stored
+    idx_cap = torch.zeros(cap, dtype=torch.int32, device=dev)
+    idx_cap[:m] = idx
+    m_dev = torch.tensor([m], dtype=torch.int32, device=dev)
+    S, _ = hotpath.lmhead_plan(cap, V, d)
+    outs = []
+    for mode in ("buffer", "gather"):
+        pm = torch.full((S, cap), 7.0, device=dev)
+        ps = torch.full((S, cap), 7.0, device=dev)
+        pa = torch.full((S, cap), -5, dtype=torch.int32, device=dev)
+        if mode == "buffer":
+            hc = torch.zeros(cap, d, dtype=torch.bfloat16, device=dev)
+            hotpath.gather_rows(H, idx_cap, hc, m_dev=m_dev, shift=shift)
+            hotpath.lmhead_stats(hc, W, S, pm, ps, pa, m_dev=m_dev, v_offset=11)
+        else:
+            hotpath.lmhead_stats_gather(H, idx_cap, W, S, pm, ps, pa, cap, m_dev=m_dev, shift=shift, v_offset=11)
+        torch.cuda.synchronize()
+        outs.append((pm[:, :m].cpu(), ps[:, :m].cpu(), pa[:, :m].cpu(), pm[:, m:].cpu()))
+    for a, b in zip(outs[0][:3], outs[1][:3]):
+        assert torch.equal(a, b)
+    assert torch.all(outs[1][3] == 7.0)  # capacity rows untouched
+    # and against the oracle on the shifted/gathered rows
+    src = np.maximum(pos - 1, 0) if shift else pos
+    Hn = H.float().cpu().numpy().astype(np.float64)
+    z = orc.logits_f64(Hn[src], W.float().cpu().numpy().astype(np.float64))
+    ref = orc.softmax_stats(z)
+    token = torch.empty(m, dtype=torch.int32, device=dev)
+    lse = torch.empty(m, device=dev)
+    conf = torch.empty(m, device=dev)
+    pm, ps, pa = (t.to(dev).contiguous() for t in outs[1][:3])
+    hotpath.stats_merge(pm, ps, pa, S, m, m, m_host=m, token=token, lse=lse, conf=conf)
+    ok = ref["margin"] > 1e-3
+    assert np.array_equal(token.cpu().numpy()[ok], ref["arg"][ok] + 11)
+    assert orc.isclose_rel(as_f64(lse), ref["lse"], 1e-3)
