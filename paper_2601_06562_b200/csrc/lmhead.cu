@@ -33,6 +33,10 @@ constexpr int UK = 16;           // K per tcgen05.mma (kind::f16)
 constexpr int NUM_ACC = 2;       // TMEM accumulator double buffer
 constexpr int TMEM_COLS = 512;   // 2 x 256 fp32 columns
 constexpr int kThreads = 192;    // warp0 TMA, warp1 MMA+TMEM, warps 2..5 epilogue
+constexpr int kAWarps = 8;       // cp.async gather path: A loader warps (warp 0 + warps 6..)
+constexpr int kRowsPerAWarp = BM / kAWarps;  // 16
+static_assert(kRowsPerAWarp % 4 == 0 && kRowsPerAWarp <= 32, "loader warp covers 4-row groups");
+constexpr int kThreadsCpAsync = kThreads + (kAWarps - 1) * 32;
 constexpr int kEpiWarps = 4;
 constexpr int kMaxSplits = 64;
 constexpr float kLog2e = 1.4426950408889634f;
@@ -72,6 +76,8 @@ struct Params {
   float* out;   // logits (debug path)
   int64_t ldo;
   const int32_t* idx;  // gather mode: masked positions, A rows are H[src(idx[r])]
+  const uint16_t* h;   // gather mode: H base (cp.async path)
+  int64_t ld_h;        // gather mode: H row stride (elements)
   int32_t shift;       // gather mode: src(p) = max(p - 1, 0) (Dream token shift)
 };
 
@@ -136,8 +142,24 @@ __device__ __forceinline__ void tma_gather4(void* smem_dst, const void* tmap, ui
 // states H themselves, fetched row by row with TMA gather4 at the masked
 // positions idx[] -- the gather-GEMM of the paper with no intermediate
 // buffer (K2 is skipped entirely).
-template <int CG, bool kStoreLogits, bool kGather = false>
-__global__ void __launch_bounds__(kThreads, 1)
+// kGather selects the A path: 0 = dense TMA box of Hc, 1 = TMA gather4 from
+// H, 2 = cp.async 16-byte row segments from H issued by the whole producer
+// warp (swizzled in software to the 128-byte TMA layout).
+constexpr int kGatherNone = 0, kGatherTma4 = 1, kGatherCpAsync = 2;
+
+__device__ __forceinline__ void cp_async16(uint32_t dst, const void* src, uint64_t policy) {
+  asm volatile("cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %2;" ::"r"(dst), "l"(src), "l"(policy)
+               : "memory");
+}
+// Arrive on a local mbarrier once all of this thread's prior cp.async copies
+// have landed (no blocking; the barrier's count includes these arrivals).
+__device__ __forceinline__ void cp_async_arrive_noinc(uint64_t* bar) {
+  asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
+
+template <int CG, bool kStoreLogits, int kGather = kGatherNone>
+__global__ void __launch_bounds__(kGather == kGatherCpAsync ? kThreadsCpAsync : kThreads, 1)
     k3_lmhead(const __grid_constant__ CUtensorMap tmap_a, const __grid_constant__ CUtensorMap tmap_b,
               const Params p) {
   using C = Cfg<CG>;
@@ -150,7 +172,11 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* empty = full + C::STAGES;
   uint64_t* tfull = empty + C::STAGES;
   uint64_t* tempty = tfull + NUM_ACC;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + NUM_ACC);
+  // cp.async A path: the producer lanes' copies of a slot landed (32 async
+  // arrivals per CTA; the pair leader's barrier also takes one relayed
+  // arrival from the peer CTA)
+  uint64_t* afull = tempty + NUM_ACC;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(afull + C::STAGES);
   int32_t* sidx = reinterpret_cast<int32_t*>(smem + C::STAGES * C::STAGE_BYTES + 256);  // gather rows
 
   const int warp = threadIdx.x >> 5;
@@ -169,6 +195,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     for (int i = 0; i < C::STAGES; ++i) {
       mbar_init(&full[i], 1);
       mbar_init(&empty[i], 1);
+      mbar_init(&afull[i], kAWarps * 32 + (CG == 2 && rank == 0 ? 1 : 0));
     }
     for (int i = 0; i < NUM_ACC; ++i) {
       mbar_init(&tfull[i], 1);
@@ -182,7 +209,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
 
-  if (warp == 0) {
+  if (warp == 0 || (kGather == kGatherCpAsync && warp >= 6)) {
     // ------------------------------------------------------------ TMA producer (both CTAs)
     // A is re-read for every tile of a unit and by the units of its m-group;
     // a W tile is shared by the m-blocks in flight at the same moment.
@@ -195,7 +222,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int t0 = s * p.tiles_per_split;
       const int t1 = min(t0 + p.tiles_per_split, p.n_tiles);
       const int a_row = mb * C::ROWS + rank * BM;
-      if constexpr (kGather) {
+      if constexpr (kGather == kGatherTma4) {
         // this CTA's 128 source rows, once per unit (rows past M read row 0;
         // their statistics are never stored)
 #pragma unroll
@@ -207,7 +234,46 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         __syncwarp();
       }
-      if (lane == 0) {
+      if constexpr (kGather == kGatherCpAsync) {
+        // kAWarps loader warps, kRowsPerAWarp rows each (warp 0 also issues the B tile). Lane
+        // copies 16-byte chunk (lane & 7) of rows (lane >> 3) + 4 i; the row
+        // sources are resolved once per unit and kept in registers.
+        const int slot = warp == 0 ? 0 : warp - 5;
+        const int chunk = lane & 7;
+        const int my_row = a_row + slot * kRowsPerAWarp + (lane % kRowsPerAWarp);
+        int src = my_row < M ? __ldg(p.idx + my_row) : 0;  // rows past M read row 0, never stored
+        if (p.shift) src = max(src - 1, 0);
+        int64_t off[kRowsPerAWarp / 4];
+#pragma unroll
+        for (int i = 0; i < kRowsPerAWarp / 4; ++i)
+          off[i] = static_cast<int64_t>(__shfl_sync(0xffffffffu, src, 4 * i + (lane >> 3))) * p.ld_h + chunk * 8;
+        const uint32_t row_dst = (slot * kRowsPerAWarp + (lane >> 3)) * (BK * 2);
+        for (int t = t0; t < t1; ++t) {
+          const int b_row = t * BN + rank * C::B_ROWS;
+          for (int kb = 0; kb < k_blocks; ++kb) {
+            mbar_wait(&empty[stage], phase ^ 1);
+            if (warp == 0 && lane == 0) {
+              if (rank == 0) mbar_arrive_expect_tx(&full[stage], C::B_BYTES * CG);
+              if constexpr (CG == 1)
+                tma_load_2d(sB + stage * C::B_BYTES, &tmap_b, &full[stage], kb * BK, b_row, pol_b);
+              else
+                tma_load_2d_cg2(sB + stage * C::B_BYTES, &tmap_b, &full[stage], kb * BK, b_row, pol_b);
+            }
+            const uint32_t dst0 = smem_u32(sA + stage * C::A_BYTES) + row_dst;
+            const uint16_t* hk = p.h + static_cast<int64_t>(kb) * BK;
+#pragma unroll
+            for (int i = 0; i < kRowsPerAWarp / 4; ++i) {
+              const int r = 4 * i + (lane >> 3);  // row within this warp's slice (same residue mod 8 as in the tile)
+              cp_async16(dst0 + 4 * i * (BK * 2) + ((chunk ^ (r & 7)) << 4), hk + off[i], pol_a);
+            }
+            cp_async_arrive_noinc(&afull[stage]);
+            if (++stage == C::STAGES) {
+              stage = 0;
+              phase ^= 1;
+            }
+          }
+        }
+      } else if (lane == 0) {
         for (int t = t0; t < t1; ++t) {
           const int b_row = t * BN + rank * C::B_ROWS;
           for (int kb = 0; kb < k_blocks; ++kb) {
@@ -217,7 +283,7 @@ __global__ void __launch_bounds__(kThreads, 1)
               tma_load_2d(sB + stage * C::B_BYTES, &tmap_b, &full[stage], kb * BK, b_row, pol_b);
             else
               tma_load_2d_cg2(sB + stage * C::B_BYTES, &tmap_b, &full[stage], kb * BK, b_row, pol_b);
-            if constexpr (kGather) {
+            if constexpr (kGather == kGatherTma4) {
               const uint32_t rows_addr = smem_u32(sidx);
 #pragma unroll 4
               for (int i = 0; i < BM / 4; ++i) {
@@ -258,6 +324,12 @@ __global__ void __launch_bounds__(kThreads, 1)
           const uint32_t d_tmem = tmem_base + acc * BN;
           for (int kb = 0; kb < k_blocks; ++kb) {
             mbar_wait(&full[stage], phase);
+            if constexpr (kGather == kGatherCpAsync) {
+              mbar_wait_cluster(&afull[stage], phase);
+              // generic-proxy cp.async writes of this CTA -> tcgen05.mma reads (the
+              // peer's half was fenced by its relay before it arrived here)
+              asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            }
             tc_fence_after();
             const uint32_t a0 = smem_u32(sA + stage * C::A_BYTES);
             const uint32_t b0 = smem_u32(sB + stage * C::B_BYTES);
@@ -276,6 +348,28 @@ __global__ void __launch_bounds__(kThreads, 1)
             acc = 0;
             acc_phase ^= 1;
           }
+        }
+      }
+    }
+    if constexpr (kGather == kGatherCpAsync && CG == 2) {
+      // peer CTA of the pair: relay "A slot landed" to the leader's barrier
+      if (lane == 0 && rank == 1) {
+        uint32_t stage = 0, phase = 0;
+        for (int64_t u = cluster; u < units; u += n_clusters) {
+          int mb, s;
+          unit_coords(p, m_blocks, u, mb, s);
+          const int t0 = s * p.tiles_per_split;
+          const int t1 = min(t0 + p.tiles_per_split, p.n_tiles);
+          for (int t = t0; t < t1; ++t)
+            for (int kb = 0; kb < k_blocks; ++kb) {
+              mbar_wait(&afull[stage], phase);
+              asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // landed rows -> async proxy
+              mbar_arrive_cluster(mapa_shared(smem_u32(&afull[stage]), 0));
+              if (++stage == C::STAGES) {
+                stage = 0;
+                phase ^= 1;
+              }
+            }
         }
       }
     }
@@ -454,7 +548,7 @@ void plan_splits(int64_t m_cap, int64_t V, int32_t* n_splits, int32_t* tps) {
   *n_splits = static_cast<int32_t>(ceil_div(n_tiles, best_tps));
 }
 
-template <int CG, bool kStore, bool kGather>
+template <int CG, bool kStore, int kGather>
 int launch_cg(const CUtensorMap& ta, const CUtensorMap& tb, const Params& p, int64_t m_cap,
               cudaStream_t stream) {
   using C = Cfg<CG>;
@@ -469,7 +563,7 @@ int launch_cg(const CUtensorMap& ta, const CUtensorMap& tb, const Params& p, int
   const int64_t clusters = units_cap < workers ? units_cap : workers;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(static_cast<unsigned>(clusters * CG));
-  cfg.blockDim = dim3(kThreads);
+  cfg.blockDim = dim3(kGather == kGatherCpAsync ? kThreadsCpAsync : kThreads);
   cfg.dynamicSmemBytes = C::SMEM;
   cfg.stream = stream;
   cudaLaunchAttribute attr[1];
@@ -520,7 +614,11 @@ int launch(const ASource& a, int64_t m_cap, const int32_t* m_dev, int64_t m_host
   MOSAIC_REQUIRE(a.ld >= d && a.ld % 8 == 0, "row stride %lld must be >= d and a multiple of 8", (long long)a.ld);
   if (m_cap == 0) return MOSAIC_OK;
   const bool gather = a.idx != nullptr;
-  const int cg = cta_group_for(m_cap);
+  // Gather mode runs cta_group::1 unless forced: its cp.async A path reaches
+  // parity with K2 + dense K3 on single-SM tiles, while the pair variant pays
+  // a cross-CTA "rows landed" relay per stage (profiles/r01_k3_gather_modes.txt).
+  static const int forced_cg = env_int("MOSAIC_CTA_GROUP", 0);
+  const int cg = gather ? (forced_cg == 2 && m_cap > BM ? 2 : 1) : cta_group_for(m_cap);
   CUtensorMap ta, tb;
   int st = gather ? encode_rows_bf16(&ta, a.base, a.rows, d, a.ld, 1) : encode_rows_bf16(&ta, a.base, m_cap, d, a.ld, BM);
   if (st) return st;
@@ -541,10 +639,21 @@ int launch(const ASource& a, int64_t m_cap, const int32_t* m_dev, int64_t m_host
   p.epilogue = epilogue;
   cudaStream_t s = as_stream(stream);
   if (gather) {
-    if constexpr (kStore) return fail(MOSAIC_E_UNSUPPORTED, "gather mode has no logits debug path");
-    else st = cg == 2 ? launch_cg<2, false, true>(ta, tb, p, m_cap, s) : launch_cg<1, false, true>(ta, tb, p, m_cap, s);
+    p.h = a.base;
+    p.ld_h = a.ld;
+    static const int gmode = env_int("MOSAIC_K3_GATHER", kGatherCpAsync);  // 1 = TMA gather4 (measured slower)
+    if constexpr (kStore) {
+      return fail(MOSAIC_E_UNSUPPORTED, "gather mode has no logits debug path");
+    } else if (gmode == kGatherTma4) {
+      st = cg == 2 ? launch_cg<2, false, kGatherTma4>(ta, tb, p, m_cap, s)
+                   : launch_cg<1, false, kGatherTma4>(ta, tb, p, m_cap, s);
+    } else {
+      st = cg == 2 ? launch_cg<2, false, kGatherCpAsync>(ta, tb, p, m_cap, s)
+                   : launch_cg<1, false, kGatherCpAsync>(ta, tb, p, m_cap, s);
+    }
   } else {
-    st = cg == 2 ? launch_cg<2, kStore, false>(ta, tb, p, m_cap, s) : launch_cg<1, kStore, false>(ta, tb, p, m_cap, s);
+    st = cg == 2 ? launch_cg<2, kStore, kGatherNone>(ta, tb, p, m_cap, s)
+                 : launch_cg<1, kStore, kGatherNone>(ta, tb, p, m_cap, s);
   }
   if (st) return st;
   return check_launch(kStore ? "mosaic_lmhead_logits" : "mosaic_lmhead_stats");

@@ -53,7 +53,7 @@ class RandomDLLM:
 
     def __init__(self, cfg: ModelConfig, device, seed: int = 0, distinct_layers: Optional[int] = None,
                  vocab_shard: tuple[int, int] | None = None):
-        if cfg.moe is not None and cfg.logits_mode != "fused":
+        if cfg.moe is not None and cfg.logits_mode not in ("fused", "fused_gather"):
             raise InputError("MoE models execute through the fused template (logits_mode='fused'), "
                              "whose FFN block carries the expert routing")
         if cfg.element_size != 2:
@@ -181,7 +181,8 @@ class StepExecutor:
             raise InputError("x must be int32 [L]")
         side = self._side_buffers(L)
         kinds = {op.kind for op in g.ops}  # the graph, not the model config, fixes the logits mode
-        self._mode = "fused" if "lmhead_stats" in kinds else ("mask_only" if "gather_logits" in kinds else "eager")
+        fused = "lmhead_stats" in kinds or "lmhead_stats_gather" in kinds
+        self._mode = "fused" if fused else ("mask_only" if "gather_logits" in kinds else "eager")
         views = self._views(g, table, plan)
         kept: dict[str, torch.Tensor] = {}
         start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -294,6 +295,21 @@ class StepExecutor:
             if r1 > r0:
                 hotpath.lmhead_stats(hc, self.model.w_vocab, S, pm, ps, pa, m_host=r1 - r0,
                                      v_offset=self.model.vocab_offset)
+            self._last_splits = S
+        elif kind == "lmhead_stats_gather":  # K3 gather mode: A rows read from h at mask_idx
+            r0, r1 = _rows(M, b["K_logits"], op.iteration)
+            h, buf = v[op.inputs[0]], v[op.outputs[0]]
+            cap = buf.shape[0]
+            S, _ = hotpath.lmhead_plan(cap, self.model.w_vocab.shape[0], d)
+            if 3 * S > buf.shape[1]:
+                raise InputError(f"K3 wants {S} splits but the template reserved {buf.shape[1] // 3}")
+            flat = buf.view(-1)
+            pm, ps = flat[: S * cap].view(S, cap), flat[S * cap: 2 * S * cap].view(S, cap)
+            pa = flat[2 * S * cap: 3 * S * cap].view(torch.int32).view(S, cap)
+            if r1 > r0:
+                idx = side["mask_idx"][r0:r0 + cap]  # the chunk's positions (rows past r1 never stored)
+                hotpath.lmhead_stats_gather(h, idx, self.model.w_vocab, S, pm, ps, pa, cap, m_host=r1 - r0,
+                                            shift=self.shift, v_offset=self.model.vocab_offset)
             self._last_splits = S
         elif kind == "sample":
             self._sample(op, g, v)

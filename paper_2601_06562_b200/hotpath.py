@@ -123,8 +123,8 @@ def lmhead_stats_gather(hidden: torch.Tensor, idx: torch.Tensor, weight: torch.T
     d = hidden.shape[1]
     if weight.shape[1] != d:
         raise InputError(f"weight is {tuple(weight.shape)}, expected [V, {d}]")
-    if idx.numel() < m_cap:
-        raise InputError("idx must hold m_cap entries")
+    if idx.numel() < (m_cap if m_dev is not None else min(int(m_host), m_cap)):
+        raise InputError("idx must cover the masked rows (m_cap entries with a device count)")
     for t, dt, n in ((part_max, torch.float32, "part_max"), (part_sum, torch.float32, "part_sum"),
                      (part_arg, torch.int32, "part_arg")):
         _req(t, dt, n)
@@ -270,7 +270,7 @@ class MaskOnlyHead:
 
     def __init__(self, weight_shard: torch.Tensor, *, seq_len: int, mask_id: int,
                  vocab_offset: int = 0, m_cap: Optional[int] = None, shift: bool = False,
-                 group=None, block: Optional[torch.Tensor] = None):
+                 group=None, block: Optional[torch.Tensor] = None, fused_gather: bool = False):
         _req(weight_shard, torch.bfloat16, "weight_shard", 2)
         self.weight = weight_shard
         self.v_shard, self.d = weight_shard.shape
@@ -280,6 +280,7 @@ class MaskOnlyHead:
         self.mask_id = int(mask_id)
         self.shift = bool(shift)
         self.group = group
+        self.fused_gather = bool(fused_gather)  # K3 reads rows of `hidden` directly: no K2, no hc buffer
         self.world = 1
         if group is not None:
             import torch.distributed as dist
@@ -290,7 +291,8 @@ class MaskOnlyHead:
         lay.add("idx", (max(self.L, m),), torch.int32)
         lay.add("m_dev", (1,), torch.int32)
         lay.add("compact_scratch", (mask_compact_scratch_bytes(self.L),), torch.uint8)
-        lay.add("hc", (m, self.d), torch.bfloat16)
+        if not self.fused_gather:
+            lay.add("hc", (m, self.d), torch.bfloat16)
         lay.add("part_max", (S, m), torch.float32)
         lay.add("part_sum", (S, m), torch.float32)
         lay.add("part_arg", (S, m), torch.int32)
@@ -319,9 +321,14 @@ class MaskOnlyHead:
             raise InputError("x/hidden do not match the configured sequence length / width")
         m_dev = b["m_dev"]
         mask_compact(x, self.mask_id, b["idx"], m_dev, b["compact_scratch"], stream)
-        gather_rows(hidden, b["idx"], b["hc"], m_dev=m_dev, shift=self.shift, stream=stream)
-        lmhead_stats(b["hc"], self.weight, self.n_splits, b["part_max"], b["part_sum"],
-                     b["part_arg"], m_dev=m_dev, v_offset=self.vocab_offset, stream=stream)
+        if self.fused_gather:
+            lmhead_stats_gather(hidden, b["idx"], self.weight, self.n_splits, b["part_max"], b["part_sum"],
+                                b["part_arg"], self.m_cap, m_dev=m_dev, shift=self.shift,
+                                v_offset=self.vocab_offset, stream=stream)
+        else:
+            gather_rows(hidden, b["idx"], b["hc"], m_dev=m_dev, shift=self.shift, stream=stream)
+            lmhead_stats(b["hc"], self.weight, self.n_splits, b["part_max"], b["part_sum"],
+                         b["part_arg"], m_dev=m_dev, v_offset=self.vocab_offset, stream=stream)
         m, S = self.m_cap, self.n_splits
         if self.group is None:
             stats_merge(b["part_max"], b["part_sum"], b["part_arg"], S, m, m, m_dev=m_dev,

@@ -128,3 +128,20 @@ def test_denoising_run_unmasks_everything(env):
     assert int((x == MASK_ID).sum()) == 0
     assert all(r.measured["committed"] >= r.metrics.theoretical_peak for r in res)
     assert len(seen) == 8
+
+
+@pytest.mark.parametrize("K", [(1, 1), (3, 2)])
+def test_fused_gather_template_matches_fused(env, K):
+    """logits_mode='fused_gather' (K3 reads h at mask_idx; no hc tensor in the
+    plan) commits exactly what the buffered fused template commits."""
+    cfg, model, ex, dev = env
+    L, M, k = 2048, 1024, 64
+    x0 = _x(L, M, dev, seed=9)
+    res = {}
+    for mode in ("fused", "fused_gather"):
+        x = x0.clone()
+        r = _step(cfg, ex, x, M, k, K=K, mode=mode, keep=("token_out",))
+        res[mode] = (x.cpu(), r["kept"]["token_out"].cpu(), r["kept"]["confidence"].cpu(), r["workspace_bytes"])
+    for a, b in zip(res["fused"][:3], res["fused_gather"][:3]):
+        assert torch.equal(a, b)
+    assert res["fused_gather"][3] <= res["fused"][3]

@@ -399,3 +399,28 @@ def test_lmhead_gather_mode_equals_gathered_buffer(dev, L, d, V, m, layout, shif
     ok = ref["margin"] > 1e-3
     assert np.array_equal(token.cpu().numpy()[ok], ref["arg"][ok] + 11)
     assert orc.isclose_rel(as_f64(lse), ref["lse"], 1e-3)
+
+
+@pytest.mark.parametrize("shift", [False, True])
+def test_mask_only_head_fused_gather_equals_buffered(dev, shift):
+    """MaskOnlyHead in gather mode (no K2, no hc buffer) commits exactly what
+    the buffered head commits: same statistics bit for bit, same x."""
+    from paper_2601_06562_b200 import MaskOnlyHead
+
+    rng = np.random.default_rng(5 + shift)
+    L, d, V, mask_id, k = 6000, 1024, 32000, 31999, 200
+    x = rng.integers(0, V - 1, size=L).astype(np.int32)
+    x[rng.random(L) < 0.6] = mask_id
+    H = bf16_tensor(rng.standard_normal((L, d)), dev)
+    W = bf16_tensor(rng.standard_normal((V, d)) * 0.04, dev)
+    outs = []
+    for fg in (False, True):
+        head = MaskOnlyHead(W, seq_len=L, mask_id=mask_id, shift=shift, fused_gather=fg)
+        xd = torch.from_numpy(x).to(dev)
+        o = head.step(xd, H, k)
+        torch.cuda.synchronize()
+        M = int(o.m_dev.item())
+        outs.append((xd.cpu(), o.token[:M].cpu(), o.lse[:M].cpu(), o.conf[:M].cpu(), head.workspace_bytes))
+    for a, b in zip(outs[0][:4], outs[1][:4]):
+        assert torch.equal(a, b)
+    assert outs[1][4] < outs[0][4] - L * d  # the [m_cap, d] buffer is gone

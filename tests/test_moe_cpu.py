@@ -99,3 +99,19 @@ def test_reference_modes_keep_the_reference_moe_template():
     assert "moe_route" not in ops and "ffn_up" in ops
     with pytest.raises(InputError):
         RandomDLLM(cfg, torch.device("cpu"))
+
+
+def test_fused_gather_template_drops_the_compacted_buffer():
+    from paper_2601_06562_b200 import chunker, workload
+
+    base = workload.toy_configs()["tiny_llada"]
+    t_f = workload.build_layer_template(base)
+    t_g = workload.build_layer_template(replace(base, logits_mode="fused_gather"))
+    assert "hc" in t_f.tensors and "hc" not in t_g.tensors
+    kinds = {op.kind for op in t_g.ops}
+    assert "lmhead_stats_gather" in kinds and "gather" not in kinds
+    b = {"L": 4096, "M": 4000}
+    pf = chunker.evaluate_peak(t_f, b, chunker.ChunkConfig(1, 1))
+    pg = chunker.evaluate_peak(t_g, b, chunker.ChunkConfig(1, 1))
+    assert pg.component_peaks["logits"] < pf.component_peaks["logits"]
+    assert pg.total_peak <= pf.total_peak
