@@ -12,24 +12,46 @@
 namespace mosaic {
 namespace {
 
-__device__ __forceinline__ float silu(float g) { return g / (1.f + __expf(-g)); }
+__device__ __forceinline__ float silu(float g) { return __fdividef(g, 1.f + __expf(-g)); }
 
-__global__ void __launch_bounds__(256) k6_swiglu(const uint4* __restrict__ gate, uint4* __restrict__ up,
-                                                 int64_t n_vec) {
-  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
-  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n_vec; i += stride) {
-    const uint4 g = __ldg(gate + i);
-    uint4 u = up[i];
-    const __nv_bfloat162* g2 = reinterpret_cast<const __nv_bfloat162*>(&g);
-    __nv_bfloat162* u2 = reinterpret_cast<__nv_bfloat162*>(&u);
+__device__ __forceinline__ uint4 swiglu8(uint4 g, uint4 u) {
+  const __nv_bfloat162* g2 = reinterpret_cast<const __nv_bfloat162*>(&g);
+  __nv_bfloat162* u2 = reinterpret_cast<__nv_bfloat162*>(&u);
 #pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      const float2 gf = __bfloat1622float2(g2[j]);
-      const float2 uf = __bfloat1622float2(u2[j]);
-      u2[j] = __floats2bfloat162_rn(silu(gf.x) * uf.x, silu(gf.y) * uf.y);
-    }
-    up[i] = u;
+  for (int j = 0; j < 4; ++j) {
+    const float2 gf = __bfloat1622float2(g2[j]);
+    const float2 uf = __bfloat1622float2(u2[j]);
+    u2[j] = __floats2bfloat162_rn(silu(gf.x) * uf.x, silu(gf.y) * uf.y);
   }
+  return u;
+}
+
+// Each block streams contiguous 1024-vector (16 KB per operand) tiles: all of
+// a thread's 4 (gate, up) vector pairs are loaded before any math, so 8
+// independent 16-byte loads per thread are in flight; evict-first loads and
+// streaming stores keep the chunk from displacing the GEMM operands in L2.
+constexpr int kVecPerThread = 4;
+constexpr int kK6Threads = 256;
+
+__global__ void __launch_bounds__(kK6Threads) k6_swiglu(const uint4* __restrict__ gate, uint4* __restrict__ up,
+                                                        int64_t n_vec) {
+  constexpr int64_t kTile = static_cast<int64_t>(kK6Threads) * kVecPerThread;
+  const int64_t n_full = n_vec / kTile;
+  for (int64_t t = blockIdx.x; t < n_full; t += gridDim.x) {
+    const int64_t base = t * kTile + threadIdx.x;
+    uint4 g[kVecPerThread], u[kVecPerThread];
+#pragma unroll
+    for (int j = 0; j < kVecPerThread; ++j) {
+      g[j] = __ldcs(gate + base + j * kK6Threads);
+      u[j] = __ldcs(up + base + j * kK6Threads);
+    }
+#pragma unroll
+    for (int j = 0; j < kVecPerThread; ++j) __stcs(up + base + j * kK6Threads, swiglu8(g[j], u[j]));
+  }
+  // ragged vector tail (< one tile): plain grid-stride
+  for (int64_t i = n_full * kTile + blockIdx.x * static_cast<int64_t>(kK6Threads) + threadIdx.x; i < n_vec;
+       i += static_cast<int64_t>(gridDim.x) * kK6Threads)
+    up[i] = swiglu8(__ldg(gate + i), up[i]);
 }
 
 __global__ void k6_swiglu_tail(const __nv_bfloat16* __restrict__ gate, __nv_bfloat16* __restrict__ up,
@@ -52,9 +74,9 @@ extern "C" int mosaic_swiglu(const uint16_t* gate, uint16_t* up, int64_t n, void
   cudaStream_t s = as_stream(stream);
   const int64_t n_vec = n / 8;
   if (n_vec > 0) {
-    const int64_t want = ceil_div(n_vec, 256);
-    const int64_t cap = static_cast<int64_t>(num_sms()) * 8;
-    k6_swiglu<<<static_cast<int>(want < cap ? want : cap), 256, 0, s>>>(
+    const int64_t want = ceil_div(n_vec, kK6Threads * kVecPerThread);
+    const int64_t cap = static_cast<int64_t>(num_sms()) * 8;  // 8 resident 256-thread blocks per SM
+    k6_swiglu<<<static_cast<int>(want < cap ? (want > 0 ? want : 1) : cap), kK6Threads, 0, s>>>(
         reinterpret_cast<const uint4*>(gate), reinterpret_cast<uint4*>(up), n_vec);
   }
   const int64_t rest = n - n_vec * 8;
