@@ -1,0 +1,32 @@
+"""Small invocations of every kernel family for compute-sanitizer runs."""
+import sys, os
+sys.path.insert(0, os.getcwd()); sys.path.insert(0, os.path.join(os.getcwd(), "oracle"))
+import numpy as np, torch
+import __graft_entry__ as ge
+from paper_2601_06562_b200 import hotpath, MaskOnlyHead, _native
+_native.load()
+dev = torch.device("cuda", 0)
+ge.smoke()  # K1, K2, K3 (cg2), K4, K5 at the tiny config, checked against the oracle
+rng = np.random.default_rng(0)
+L, d, V, mid = 3000, 256, 5000, 4999
+x = rng.integers(0, V - 1, size=L).astype(np.int32); x[rng.random(L) < 0.5] = mid
+H = torch.from_numpy(rng.standard_normal((L, d)).astype(np.float32)).to(dev).bfloat16()
+W = torch.from_numpy((rng.standard_normal((V, d)) * 0.05).astype(np.float32)).to(dev).bfloat16()
+for fg in (False, True):
+    head = MaskOnlyHead(W, seq_len=L, mask_id=mid, shift=True, fused_gather=fg)
+    head.step(torch.from_numpy(x).to(dev), H, 50)
+head = MaskOnlyHead(W, seq_len=L, mask_id=mid, m_cap=100)  # M <= 128 -> cta_group::1
+xs = x.copy(); xs[:] = 1; xs[:90] = mid
+head.step(torch.from_numpy(xs).to(dev), H, 10)
+z = torch.randn(700, 64, device=dev)
+n = 700 * 8
+a = torch.empty(n, dtype=torch.int32, device=dev); b = torch.empty(n, dtype=torch.int32, device=dev)
+w = torch.empty(n, device=dev); off = torch.empty(65, dtype=torch.int32, device=dev)
+sc = torch.empty(hotpath.moe_route_scratch_bytes(700, 64), dtype=torch.uint8, device=dev)
+hotpath.moe_route(z, 8, a, b, w, off, sc)
+src = torch.randn(n, 256, device=dev).bfloat16(); out = torch.empty(700, 256, device=dev).bfloat16()
+hotpath.moe_combine(src, b, w, 8, out)
+g = torch.randn(4099 * 3, device=dev).bfloat16(); u = torch.randn(4099 * 3, device=dev).bfloat16()
+hotpath.swiglu_(g, u)
+torch.cuda.synchronize()
+print("sanitize run ok")
