@@ -141,6 +141,73 @@ __global__ void __launch_bounds__(256) k5_commit(const float* __restrict__ conf,
   }
 }
 
+// Single-CTA K5 for capacities up to kFusedRemaskCap rows: the same 8-pass
+// radix select (one 8-bit digit of the 64-bit key per pass, histogram in
+// shared memory) and the commit, in one launch instead of 18 -- at LLaDA 32k
+// (M = 16384) the 18 dependent launches cost more than the work.
+constexpr int64_t kFusedRemaskCap = 65536;
+constexpr int kFusedThreads = 1024;
+
+__global__ void __launch_bounds__(kFusedThreads) k5_fused(const float* __restrict__ conf,
+                                                          const int32_t* __restrict__ pos,
+                                                          const int32_t* __restrict__ token,
+                                                          const int32_t* __restrict__ m_dev, int64_t m_host,
+                                                          int64_t m_cap, int64_t k, int32_t* __restrict__ x,
+                                                          int32_t* __restrict__ selected) {
+  __shared__ uint32_t h[256];
+  __shared__ uint32_t cum[256];
+  __shared__ unsigned long long s_prefix;
+  __shared__ uint32_t s_krem;
+  const int t = threadIdx.x;
+  const int64_t M = min(static_cast<int64_t>(load_count(m_dev, m_host)), m_cap);
+  const int64_t kk = k < M ? k : M;
+  if (t == 0) {
+    s_prefix = 0ull;
+    s_krem = static_cast<uint32_t>(kk > 0 ? kk : 0);
+  }
+  for (int pass = 0; pass < 8; ++pass) {
+    if (t < 256) h[t] = 0u;
+    __syncthreads();
+    if (s_krem == 0u) break;  // only when k == 0 (uniform)
+    const unsigned long long prefix = s_prefix;
+    const int hi_shift = 64 - 8 * pass;
+    const int lo_shift = 56 - 8 * pass;
+    for (int64_t r = t; r < M; r += kFusedThreads) {
+      const unsigned long long key = remask_key(conf[r], pos[r]);
+      if (pass == 0 || (key >> hi_shift) == (prefix >> hi_shift)) atomicAdd(&h[(key >> lo_shift) & 255u], 1u);
+    }
+    __syncthreads();
+    uint32_t cnt = 0u;
+    if (t < 256) {
+      cnt = h[255 - t];  // descending digit order
+      cum[t] = cnt;
+    }
+    __syncthreads();
+    for (int o = 1; o < 256; o <<= 1) {
+      const uint32_t add = (t < 256 && t >= o) ? cum[t - o] : 0u;
+      __syncthreads();
+      if (t < 256) cum[t] += add;
+      __syncthreads();
+    }
+    if (t < 256) {
+      const uint32_t k_rem = s_krem, incl = cum[t], above = incl - cnt;
+      if (above < k_rem && incl >= k_rem) {  // exactly one digit qualifies
+        s_prefix = prefix | (static_cast<unsigned long long>(255 - t) << lo_shift);
+        s_krem = k_rem - above;
+      }
+    }
+    __syncthreads();
+  }
+  const bool active = kk > 0;
+  const unsigned long long thr = s_prefix;
+  for (int64_t r = t; r < M; r += kFusedThreads) {
+    const int32_t p = pos[r];
+    const bool sel = active && remask_key(conf[r], p) >= thr;
+    if (sel) x[p] = token[r];
+    if (selected) selected[r] = sel ? 1 : 0;
+  }
+}
+
 int grid_for(int64_t n, int per_block) {
   const int64_t want = ceil_div(n > 0 ? n : 1, per_block);
   const int64_t cap = static_cast<int64_t>(num_sms()) * 8;
@@ -179,6 +246,10 @@ extern "C" int mosaic_remask_commit(const float* conf, const int32_t* pos, const
   if (m_cap == 0) return MOSAIC_OK;
   MOSAIC_REQUIRE(conf && pos && token && x, "null inputs");
   cudaStream_t s = as_stream(stream);
+  if (m_cap <= kFusedRemaskCap) {
+    k5_fused<<<1, kFusedThreads, 0, s>>>(conf, pos, token, m_dev, m_host, m_cap, k, x, selected);
+    return check_launch("mosaic_remask_commit");
+  }
   SelectState* st = static_cast<SelectState*>(scratch);
   const int grid = grid_for(m_cap, 256);
   k5_init<<<1, 256, 0, s>>>(st, m_dev, m_host, m_cap, k);
