@@ -213,7 +213,8 @@ def gpu_main(args):
         _hp.l2_persisting_limit(persist)
     head = MaskOnlyHead(W, seq_len=SEQ, mask_id=MASK_ID, vocab_offset=v0, m_cap=M, group=group)
     stream = torch.cuda.current_stream()
-    launches_per_step = 6  # K1 x2, K2, K3, K4, K5 (single-CTA path, m_cap <= 65536)
+    # ours per step: K1 x2, K2, K3, K4 (+ the rank-order K4 after the all-gather), K5 (single-CTA, m_cap <= 65536)
+    launches_per_step = 6 + (1 if world > 1 else 0)
 
     # K3 timing events on the launching stream (the current stream)
     from paper_2601_06562_b200 import hotpath
