@@ -10,6 +10,9 @@ layer weights resident (random-init bf16). One denoising step at L = seq,
 r_p = 0.5 (M = L/2 masked), k = M/64 tokens committed. Two plans are run:
 
 * ``unchunked``: K = (1, 1) -- one FFN chunk of L*top_k dispatch rows;
+The expert FFN runs as K10 grouped tcgen05 GEMMs over the K8 expert
+segments (gate/up with the SwiGLU epilogue, then down), offsets on the device.
+
 * ``searched``: the reference's lazy bottleneck search (chunker.search_bottleneck)
   under an activation budget halfway between the non-chunkable floor and the
   unchunked peak, so the expert FFN must be chunked (K_FFN > 1).
@@ -64,7 +67,7 @@ def summarize(cfg, L, r):
     d, f, nl = cfg.d_model, cfg.d_ff, cfg.n_layers
     P = L * k
     byk = r["ms_by_kind"]
-    gemm_ms = sum(byk.get(kd, 0.0) for kd in ("ffn_up", "ffn_gate", "ffn_down"))
+    gemm_ms = sum(byk.get(kd, 0.0) for kd in ("ffn_gate_up", "ffn_down"))  # K10 (gate/up + SwiGLU, down)
     gemm_flops = 3 * 2.0 * P * d * f * nl
     # K9 reads k rows of d + writes 1 row per token; K8 reads E fp32 logits per token
     k9_bytes = nl * L * (k + 1) * d * 2.0 + nl * L * k * 8.0

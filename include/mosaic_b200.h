@@ -178,6 +178,20 @@ MOSAIC_API int mosaic_moe_combine(const uint16_t* src, int64_t ld_src, const int
                        const float* comb_w, int64_t rows, int32_t top_k, int64_t d,
                        uint16_t* out, int64_t ld_out, void* stream);
 
+/* ---------------------------------------------------------------- K10 -----
+ * Grouped tcgen05 GEMM of the FFN chunk (workload.py:231-273, MoE rows
+ * :238-253): for each group g < G, rows [off[g], off[g+1]) of A [rows_cap, K]
+ * (row stride lda) times W[g] = W rows [g*N, (g+1)*N) (K-major, i.e. torch's
+ * [K, N] weight transposed) into C (row stride ldc), bf16 in/out, fp32
+ * accumulation. group_off is a device int32 array of G+1 offsets (the K8
+ * expert_off output), or NULL for one group of m_host rows. swiglu = 1: W
+ * rows alternate 128-row gate / up blocks and C receives silu(gate) * up,
+ * N/2 columns -- the ffn_up + ffn_gate + glu ops of a chunk in one kernel.
+ * K % 64 == 0, N % 32 == 0 (N % 256 == 0 with swiglu), G <= 256.            */
+MOSAIC_API int mosaic_ffn_gemm(const uint16_t* A, int64_t rows_cap, int64_t lda, const int32_t* group_off,
+                    int32_t G, int64_t m_host, const uint16_t* W, int64_t N, int64_t K, int32_t swiglu,
+                    uint16_t* C, int64_t ldc, void* stream);
+
 /* ---------------------------------------------------------------- K7 ------
  * Contiguous device workspace with lazy physical commitment (cuMem VMM):
  * reserve a VA range once, map physical granules for the prefix

@@ -1,0 +1,318 @@
+// K10: grouped tcgen05 GEMM for the lazily chunked FFN, with an optional
+// SwiGLU epilogue -- the FFN chunk's up/gate projections and activation in one
+// kernel (act = silu(x Wg) * (x Wu) straight from the TMEM accumulators, so
+// neither `gate` nor `up` is ever written), and the down projection.
+//
+// Reference counterpart: the FFN chunk loop of the step template
+// (mosaic/workload.py:231-273: ffn_up / ffn_gate / glu / ffn_down per chunk of
+// ceil(L/K_FFN) rows, x top_k rows for MoE, :195,238-253). The MoE routing
+// (K8) orders the chunk's dispatch rows by expert, so the experts' GEMMs are
+// one grouped GEMM over contiguous row segments whose bounds stay on the
+// device (no host round trip): group g multiplies rows
+// [group_off[g], group_off[g+1]) of A by its own weight block W[g].
+//
+// Layout: A [rows, K] bf16 (row stride lda), W [G * N, K] bf16 K-major (the
+// transpose of torch's [K, N] weight), C [rows, N or N/2] bf16 (row stride
+// ldc). SwiGLU mode expects W rows interleaved in 128-row blocks (gate block
+// j, then up block j) so one 256-column tile holds matching gate and up
+// columns; it writes 128 act columns per tile.
+//
+// Structure as K3 (csrc/lmhead.cu), cta_group::1: warp 0 TMA producer, warp 1
+// TMEM allocator + single-thread tcgen05.mma issuer (M=128, N=256, K=16, BF16
+// -> FP32), warps 2-5 epilogue draining a double-buffered TMEM accumulator;
+// persistent CTAs walk (m-block, n-tile) units rasterised in groups of
+// `group_m` m-blocks so the weight tiles in flight are shared through L2.
+#include <cuda_bf16.h>
+
+#include "common.cuh"
+
+namespace mosaic {
+namespace {
+
+constexpr int BM = 128;
+constexpr int BN = 256;
+constexpr int BK = 64;
+constexpr int UK = 16;
+constexpr int STAGES = 4;
+constexpr int A_BYTES = BM * BK * 2;
+constexpr int B_BYTES = BN * BK * 2;
+constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+constexpr int NUM_ACC = 2;
+constexpr int TMEM_COLS = 512;
+constexpr int kThreads = 192;
+constexpr int kEpiWarps = 4;
+constexpr int kMaxGroups = 256;
+constexpr int kGroupM = 16;
+constexpr int SMEM = STAGES * STAGE_BYTES + 1024 + 256 + 2 * (kMaxGroups + 1) * 4;
+constexpr uint32_t IDESC = umma_idesc_bf16(BM, BN);
+
+struct GParams {
+  const int32_t* group_off;  // [G + 1] device row offsets, or null: one group of m_host rows
+  int32_t G;
+  int64_t m_host;
+  int64_t N;        // weight rows per group (output columns; 2 x act columns with SwiGLU)
+  int32_t K;
+  int32_t n_tiles;  // ceil(N / BN)
+  int32_t swiglu;
+  uint16_t* C;
+  int64_t ldc;
+};
+
+__device__ __forceinline__ float silu(float g) { return __fdividef(g, 1.f + __expf(-g)); }
+
+__device__ __forceinline__ uint32_t pack_bf16x2(float lo, float hi) {
+  __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);
+  return *reinterpret_cast<uint32_t*>(&v);
+}
+
+// unit -> (group, first row, end row of the group, n-tile)
+struct Unit {
+  int g;
+  int64_t row0;
+  int64_t row_end;
+  int nt;
+};
+
+__device__ __forceinline__ Unit unit_of(int64_t u, int n_tiles, int total_mb, const int32_t* s_off,
+                                        const int32_t* s_mbp, int G) {
+  const int64_t per_group = static_cast<int64_t>(kGroupM) * n_tiles;
+  const int64_t gi = u / per_group;
+  const int64_t rem = u - gi * per_group;
+  const int64_t gm = min(static_cast<int64_t>(kGroupM), total_mb - gi * kGroupM);
+  const int nt = static_cast<int>(rem / gm);
+  const int gmb = static_cast<int>(gi * kGroupM + rem % gm);
+  int lo = 0, hi = G - 1;  // largest g with s_mbp[g] <= gmb
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (s_mbp[mid] <= gmb) lo = mid;
+    else hi = mid - 1;
+  }
+  Unit r;
+  r.g = lo;
+  r.row0 = s_off[lo] + static_cast<int64_t>(gmb - s_mbp[lo]) * BM;
+  r.row_end = s_off[lo + 1];
+  r.nt = nt;
+  return r;
+}
+
+__global__ void __launch_bounds__(kThreads, 1)
+    k10_ffn_gemm(const __grid_constant__ CUtensorMap tmap_a, const __grid_constant__ CUtensorMap tmap_b,
+                 const GParams p) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~static_cast<uintptr_t>(1023));
+  uint8_t* sA = smem;
+  uint8_t* sB = smem + STAGES * A_BYTES;
+  uint64_t* full = reinterpret_cast<uint64_t*>(sB + STAGES * B_BYTES);
+  uint64_t* empty = full + STAGES;
+  uint64_t* tfull = empty + STAGES;
+  uint64_t* tempty = tfull + NUM_ACC;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + NUM_ACC);
+  int32_t* s_off = reinterpret_cast<int32_t*>(smem + STAGES * STAGE_BYTES + 256);
+  int32_t* s_mbp = s_off + kMaxGroups + 1;
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const int G = p.G;
+
+  if (threadIdx.x == 0) {
+    tma_prefetch_desc(&tmap_a);
+    tma_prefetch_desc(&tmap_b);
+    for (int i = 0; i < STAGES; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&empty[i], 1);
+    }
+    for (int i = 0; i < NUM_ACC; ++i) {
+      mbar_init(&tfull[i], 1);
+      mbar_init(&tempty[i], kEpiWarps);
+    }
+    fence_mbar_init();
+    // group row offsets and the exclusive prefix of their m-block counts
+    int32_t mb = 0;
+    for (int g = 0; g <= G; ++g) {
+      const int32_t o = p.group_off ? __ldg(p.group_off + g) : (g == 0 ? 0 : static_cast<int32_t>(p.m_host));
+      s_off[g] = o;
+      s_mbp[g] = mb;
+      if (g < G) {
+        const int32_t cnt = (p.group_off ? __ldg(p.group_off + g + 1) : static_cast<int32_t>(p.m_host)) - o;
+        mb += (cnt + BM - 1) / BM;
+      }
+    }
+  }
+  if (warp == 1) tmem_alloc<1>(tmem_slot, TMEM_COLS);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+  const int total_mb = s_mbp[G];
+  const int64_t units = static_cast<int64_t>(total_mb) * p.n_tiles;
+  const int k_blocks = p.K / BK;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      const uint64_t pol_a = policy_evict_last();
+      const uint64_t pol_b = policy_evict_normal();
+      uint32_t stage = 0, phase = 0;
+      for (int64_t u = blockIdx.x; u < units; u += gridDim.x) {
+        const Unit w = unit_of(u, p.n_tiles, total_mb, s_off, s_mbp, G);
+        const int32_t a_row = static_cast<int32_t>(w.row0);
+        const int32_t b_row = static_cast<int32_t>(w.g * p.N + static_cast<int64_t>(w.nt) * BN);
+        for (int kb = 0; kb < k_blocks; ++kb) {
+          mbar_wait(&empty[stage], phase ^ 1);
+          mbar_arrive_expect_tx(&full[stage], STAGE_BYTES);
+          tma_load_2d(sA + stage * A_BYTES, &tmap_a, &full[stage], kb * BK, a_row, pol_a);
+          tma_load_2d(sB + stage * B_BYTES, &tmap_b, &full[stage], kb * BK, b_row, pol_b);
+          if (++stage == STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      uint32_t stage = 0, phase = 0, acc = 0, acc_phase = 0;
+      for (int64_t u = blockIdx.x; u < units; u += gridDim.x) {
+        mbar_wait(&tempty[acc], acc_phase ^ 1);
+        tc_fence_after();
+        const uint32_t d_tmem = tmem_base + acc * BN;
+        for (int kb = 0; kb < k_blocks; ++kb) {
+          mbar_wait(&full[stage], phase);
+          tc_fence_after();
+          const uint32_t a0 = smem_u32(sA + stage * A_BYTES);
+          const uint32_t b0 = smem_u32(sB + stage * B_BYTES);
+#pragma unroll
+          for (int kk = 0; kk < BK / UK; ++kk)
+            umma_bf16<1>(d_tmem, umma_desc_sw128(a0 + kk * UK * 2), umma_desc_sw128(b0 + kk * UK * 2), IDESC,
+                         (kb | kk) != 0);
+          umma_commit<1>(&empty[stage]);
+          if (++stage == STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+        umma_commit<1>(&tfull[acc]);
+        if (++acc == NUM_ACC) {
+          acc = 0;
+          acc_phase ^= 1;
+        }
+      }
+    }
+  } else {
+    const int q = warp & 3;
+    const int row_local = q * 32 + lane;
+    uint32_t acc = 0, acc_phase = 0;
+    for (int64_t u = blockIdx.x; u < units; u += gridDim.x) {
+      const Unit w = unit_of(u, p.n_tiles, total_mb, s_off, s_mbp, G);
+      const int64_t row = w.row0 + row_local;
+      const bool live = row < w.row_end;
+      mbar_wait(&tfull[acc], acc_phase);
+      tc_fence_after();
+      const uint32_t taddr = tmem_base + (static_cast<uint32_t>(q * 32) << 16) + acc * BN;
+      if (p.swiglu) {
+        const int64_t n_out = p.N >> 1;
+#pragma unroll 1
+        for (int c = 0; c < BN / 64; ++c) {
+          const int64_t col0 = static_cast<int64_t>(w.nt) * (BN / 2) + c * 32;
+          float gv[32], uv[32];
+          tmem_ld32(taddr + c * 32, gv);             // gate block columns
+          tmem_ld32(taddr + BN / 2 + c * 32, uv);    // matching up block columns
+          if (live && col0 < n_out) {
+            uint4* dst = reinterpret_cast<uint4*>(p.C + row * p.ldc + col0);
+#pragma unroll
+            for (int v = 0; v < 4; ++v) {
+              uint4 o;
+              o.x = pack_bf16x2(silu(gv[8 * v + 0]) * uv[8 * v + 0], silu(gv[8 * v + 1]) * uv[8 * v + 1]);
+              o.y = pack_bf16x2(silu(gv[8 * v + 2]) * uv[8 * v + 2], silu(gv[8 * v + 3]) * uv[8 * v + 3]);
+              o.z = pack_bf16x2(silu(gv[8 * v + 4]) * uv[8 * v + 4], silu(gv[8 * v + 5]) * uv[8 * v + 5]);
+              o.w = pack_bf16x2(silu(gv[8 * v + 6]) * uv[8 * v + 6], silu(gv[8 * v + 7]) * uv[8 * v + 7]);
+              dst[v] = o;
+            }
+          }
+        }
+      } else {
+#pragma unroll 1
+        for (int c = 0; c < BN / 32; ++c) {
+          const int64_t col0 = static_cast<int64_t>(w.nt) * BN + c * 32;
+          if (col0 >= p.N) break;  // warp-uniform (N % 32 == 0)
+          float v32[32];
+          tmem_ld32(taddr + c * 32, v32);
+          if (live) {
+            uint4* dst = reinterpret_cast<uint4*>(p.C + row * p.ldc + col0);
+#pragma unroll
+            for (int v = 0; v < 4; ++v) {
+              uint4 o;
+              o.x = pack_bf16x2(v32[8 * v + 0], v32[8 * v + 1]);
+              o.y = pack_bf16x2(v32[8 * v + 2], v32[8 * v + 3]);
+              o.z = pack_bf16x2(v32[8 * v + 4], v32[8 * v + 5]);
+              o.w = pack_bf16x2(v32[8 * v + 6], v32[8 * v + 7]);
+              dst[v] = o;
+            }
+          }
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tempty[acc]);
+      if (++acc == NUM_ACC) {
+        acc = 0;
+        acc_phase ^= 1;
+      }
+    }
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc<1>(tmem_base, TMEM_COLS);
+  }
+}
+
+}  // namespace
+}  // namespace mosaic
+
+using namespace mosaic;
+
+extern "C" int mosaic_ffn_gemm(const uint16_t* A, int64_t rows_cap, int64_t lda, const int32_t* group_off, int32_t G,
+                               int64_t m_host, const uint16_t* W, int64_t N, int64_t K, int32_t swiglu, uint16_t* C,
+                               int64_t ldc, void* stream) {
+  MOSAIC_REQUIRE(A && W && C, "null operands");
+  MOSAIC_REQUIRE(G >= 1 && G <= kMaxGroups, "G=%d not in [1, %d]", G, kMaxGroups);
+  MOSAIC_REQUIRE(group_off != nullptr || G == 1, "several groups need device offsets");
+  MOSAIC_REQUIRE(K >= BK && K % BK == 0, "K=%lld must be a positive multiple of %d", (long long)K, BK);
+  MOSAIC_REQUIRE(N >= 32 && N % 32 == 0, "N=%lld must be a positive multiple of 32", (long long)N);
+  MOSAIC_REQUIRE(!swiglu || N % BN == 0, "SwiGLU mode needs N (2 x d_ff) to be a multiple of %d", BN);
+  MOSAIC_REQUIRE(lda >= K && lda % 8 == 0 && ldc % 8 == 0, "row strides must be multiples of 8 elements");
+  MOSAIC_REQUIRE(ldc >= (swiglu ? N / 2 : N), "ldc too small");
+  MOSAIC_REQUIRE(rows_cap >= 0 && rows_cap < (int64_t(1) << 31) && G * N < (int64_t(1) << 31), "sizes out of range");
+  MOSAIC_REQUIRE(group_off != nullptr || (m_host >= 0 && m_host <= rows_cap), "m_host out of range");
+  MOSAIC_REQUIRE((reinterpret_cast<uintptr_t>(A) & 15) == 0 && (reinterpret_cast<uintptr_t>(W) & 15) == 0 &&
+                     (reinterpret_cast<uintptr_t>(C) & 15) == 0,
+                 "A, W, C must be 16-byte aligned");
+  if (rows_cap == 0) return MOSAIC_OK;
+  CUtensorMap ta, tb;
+  int st = encode_tma_bf16(&ta, A, rows_cap, K, lda, BM, BK);
+  if (st) return st;
+  st = encode_tma_bf16(&tb, W, G * N, K, K, BN, BK);
+  if (st) return st;
+  GParams p{};
+  p.group_off = group_off;
+  p.G = G;
+  p.m_host = m_host;
+  p.N = N;
+  p.K = static_cast<int32_t>(K);
+  p.n_tiles = static_cast<int32_t>(ceil_div(N, BN));
+  p.swiglu = swiglu ? 1 : 0;
+  p.C = C;
+  p.ldc = ldc;
+  static bool attr_set = false;
+  if (!attr_set) {
+    MOSAIC_CUDA(cudaFuncSetAttribute(k10_ffn_gemm, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM));
+    attr_set = true;
+  }
+  const int64_t units_cap = (ceil_div(rows_cap, BM) + G) * p.n_tiles;
+  const int64_t grid = units_cap < num_sms() ? units_cap : num_sms();
+  k10_ffn_gemm<<<static_cast<unsigned>(grid), kThreads, SMEM, as_stream(stream)>>>(ta, tb, p);
+  return check_launch("mosaic_ffn_gemm");
+}

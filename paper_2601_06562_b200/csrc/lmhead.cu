@@ -97,24 +97,6 @@ __device__ __forceinline__ float fast_exp2(float x) {
   return y;
 }
 
-// 32 lanes x 32 consecutive fp32 columns of this warp's TMEM lane quarter.
-__device__ __forceinline__ void tmem_ld32(uint32_t taddr, float (&v)[32]) {
-  uint32_t r[32];
-  asm volatile(
-      "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
-      "{%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, %15, "
-      "%16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31}, [%32];\n\t"
-      "tcgen05.wait::ld.sync.aligned;"
-      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
-        "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),
-        "=r"(r[14]), "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]),
-        "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]),
-        "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
-      : "r"(taddr)
-      : "memory");
-#pragma unroll
-  for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
-}
 
 // 2-D TMA gather of four K-major rows (64 bf16 columns each) by row index,
 // 128-byte swizzled like a plain box load; with CG == 2 the transaction bytes
@@ -466,25 +448,6 @@ __global__ void __launch_bounds__(kGather == kGatherCpAsync ? kThreadsCpAsync : 
   }
 }
 
-using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
-                                   const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
-                                   const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
-                                   CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
-
-int encode_kmajor_bf16(CUtensorMap* map, const void* base, int64_t rows, int64_t K, int box_rows) {
-  static EncodeTiledFn fn = reinterpret_cast<EncodeTiledFn>(driver_fn("cuTensorMapEncodeTiled"));
-  if (!fn) return fail(MOSAIC_E_CUDA, "cuTensorMapEncodeTiled unavailable from the driver");
-  const cuuint64_t dims[2] = {static_cast<cuuint64_t>(K), static_cast<cuuint64_t>(rows)};
-  const cuuint64_t strides[1] = {static_cast<cuuint64_t>(K) * 2};
-  const cuuint32_t box[2] = {BK, static_cast<cuuint32_t>(box_rows)};
-  const cuuint32_t elem_strides[2] = {1, 1};
-  CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides,
-                  box, elem_strides, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
-                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-  if (r != CUDA_SUCCESS) return fail(MOSAIC_E_CUDA, "cuTensorMapEncodeTiled failed (%d)", int(r));
-  return MOSAIC_OK;
-}
-
 int cta_group_for(int64_t m_cap) {
   static int forced = [] {
     const char* e = getenv("MOSAIC_CTA_GROUP");
@@ -587,20 +550,6 @@ struct ASource {
   int32_t shift;
 };
 
-int encode_rows_bf16(CUtensorMap* map, const void* base, int64_t rows, int64_t K, int64_t ld, int box_rows) {
-  static EncodeTiledFn fn = reinterpret_cast<EncodeTiledFn>(driver_fn("cuTensorMapEncodeTiled"));
-  if (!fn) return fail(MOSAIC_E_CUDA, "cuTensorMapEncodeTiled unavailable from the driver");
-  const cuuint64_t dims[2] = {static_cast<cuuint64_t>(K), static_cast<cuuint64_t>(rows)};
-  const cuuint64_t strides[1] = {static_cast<cuuint64_t>(ld) * 2};
-  const cuuint32_t box[2] = {BK, static_cast<cuuint32_t>(box_rows)};
-  const cuuint32_t elem_strides[2] = {1, 1};
-  CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box,
-                  elem_strides, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
-                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-  if (r != CUDA_SUCCESS) return fail(MOSAIC_E_CUDA, "cuTensorMapEncodeTiled failed (%d)", int(r));
-  return MOSAIC_OK;
-}
-
 template <bool kStore>
 int launch(const ASource& a, int64_t m_cap, const int32_t* m_dev, int64_t m_host, const uint16_t* W, int64_t V,
            int64_t d, Params p, void* stream) {
@@ -620,9 +569,9 @@ int launch(const ASource& a, int64_t m_cap, const int32_t* m_dev, int64_t m_host
   static const int forced_cg = env_int("MOSAIC_CTA_GROUP", 0);
   const int cg = gather ? (forced_cg == 2 && m_cap > BM ? 2 : 1) : cta_group_for(m_cap);
   CUtensorMap ta, tb;
-  int st = gather ? encode_rows_bf16(&ta, a.base, a.rows, d, a.ld, 1) : encode_rows_bf16(&ta, a.base, m_cap, d, a.ld, BM);
+  int st = gather ? encode_tma_bf16(&ta, a.base, a.rows, d, a.ld, 1, BK) : encode_tma_bf16(&ta, a.base, m_cap, d, a.ld, BM, BK);
   if (st) return st;
-  st = encode_kmajor_bf16(&tb, W, V, d, BN / cg);
+  st = encode_tma_bf16(&tb, W, V, d, d, BN / cg, BK);
   if (st) return st;
   p.m_dev = m_dev;
   p.m_host = m_host;

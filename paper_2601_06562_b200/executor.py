@@ -70,17 +70,21 @@ class RandomDLLM:
         n_sets = cfg.n_layers if distinct_layers is None else max(1, min(distinct_layers, cfg.n_layers))
         self.layers = []
         E = cfg.moe.n_experts if cfg.moe else None
+        fused = cfg.logits_mode in ("fused", "fused_gather")
         for _ in range(n_sets):
             lw = {"w_qkv": w(d, 3 * d), "w_attn_out": w(d, d, scale=0.02 * out_scale)}
-            if E is None:
+            if E is not None:
+                # K10 operands: gate/up interleaved K-major [E*2f, d]; down K-major [E*d, f]
+                lw["w_router"] = w(d, E, scale=1.0 / math.sqrt(d))
+                lw["w_gate_up"] = hotpath.interleave_gate_up(w(E, d, f), w(E, d, f)).view(E * 2 * f, d)
+                lw["w_down"] = w(E, f, d, scale=0.02 * out_scale).transpose(1, 2).contiguous().view(E * d, f)
+            elif cfg.fused_ffn and fused:
+                lw["w_gate_up"] = hotpath.interleave_gate_up(w(d, f), w(d, f))  # [2f, d]
+                lw["w_down"] = w(f, d, scale=0.02 * out_scale)
+            else:
                 lw.update(w_up=w(d, f), w_down=w(f, d, scale=0.02 * out_scale))
                 if cfg.gated_ffn:
                     lw["w_gate"] = w(d, f)
-            else:  # experts stacked [E, d, f] / [E, f, d]; router [d, E]
-                lw.update(w_router=w(d, E, scale=1.0 / math.sqrt(d)), w_up=w(E, d, f),
-                          w_down=w(E, f, d, scale=0.02 * out_scale))
-                if cfg.gated_ffn:
-                    lw["w_gate"] = w(E, d, f)
             self.layers.append(lw)
         v0, v1 = vocab_shard or (0, V)
         self.vocab_offset = v0
@@ -250,8 +254,13 @@ class StepExecutor:
             out = v[op.outputs[0]]
             if op.outputs[0][0].endswith("ffn_acc"):
                 out.zero_()
-        elif kind.startswith("moe_") or (self.cfg.moe is not None and kind in ("ffn_up", "ffn_gate", "ffn_down")):
+        elif kind.startswith("moe_") or (self.cfg.moe is not None and kind in ("ffn_gate_up", "ffn_down")):
             self._moe(op, g, v, side)
+        elif kind == "ffn_gate_up":  # K10: gate/up GEMM + SwiGLU epilogue -> act
+            r0, r1 = _rows(L, b["K_FFN"], op.iteration)
+            f = cfg.d_ff
+            hotpath.ffn_gemm(v[op.inputs[0]][r0:r1], self._layer(op.op_id)["w_gate_up"], v[op.outputs[0]][: r1 - r0],
+                             2 * f, m_host=r1 - r0, swiglu=True)
         elif kind in ("ffn_up", "ffn_gate"):
             layer = self._layer(op.op_id)
             r0, r1 = _rows(L, b["K_FFN"], op.iteration)
@@ -340,7 +349,8 @@ class StepExecutor:
 
     def _moe(self, op, g: ConcreteGraph, v, side) -> None:
         """The MoE FFN chunk (workload._moe_ffn_block): K8 routing, K2 dispatch
-        gather, per-expert cuBLAS GEMMs on the expert segments, K9 combine."""
+        gather, K10 grouped gate/up (+SwiGLU) and down GEMMs over the expert
+        segments (offsets stay on the device), K9 combine."""
         cfg = self.cfg
         E, k = cfg.moe.n_experts, cfg.moe.top_k
         L = g.bindings["L"]
@@ -350,7 +360,6 @@ class StepExecutor:
         if n <= 0:
             if kind == "moe_route":
                 v[op.outputs[3]].zero_()
-                self._moe_off = [0] * (E + 1)
             return
         lw = self._layer(op.op_id)
         if kind == "moe_router":
@@ -359,17 +368,17 @@ class StepExecutor:
         elif kind == "moe_route":
             rrow, rpos, rw, off = (v[key] for key in op.outputs)
             hotpath.moe_route(v[op.inputs[0]][:n], k, rrow, rpos, rw, off, side["route"], row_base=r0)
-            self._moe_off = off.tolist()  # segment bounds for the per-expert GEMMs (host sync)
         elif kind == "moe_dispatch":
             h, rrow = (v[key] for key in op.inputs)
             hotpath.gather_rows(h, rrow, v[op.outputs[0]][: n * k], m_host=n * k)
-        elif kind in ("ffn_up", "ffn_gate", "ffn_down"):
-            src, out = v[op.inputs[0]], v[op.outputs[0]]
-            w = lw["w_up" if kind == "ffn_up" else "w_gate" if kind == "ffn_gate" else "w_down"]
-            off = self._moe_off
-            for e in range(E):
-                if off[e + 1] > off[e]:
-                    torch.matmul(src[off[e]:off[e + 1]], w[e], out=out[off[e]:off[e + 1]])
+        elif kind == "ffn_gate_up":  # K10 grouped over the expert segments, SwiGLU epilogue
+            xin, off = v[op.inputs[0]], v[op.inputs[2]]
+            hotpath.ffn_gemm(xin[: n * k], lw["w_gate_up"], v[op.outputs[0]][: n * k], 2 * cfg.d_ff,
+                             group_off=off, groups=E, swiglu=True)
+        elif kind == "ffn_down":  # K10 grouped, written over the dispatch rows (in place)
+            act, off = v[op.inputs[0]], v[op.inputs[2]]
+            hotpath.ffn_gemm(act[: n * k], lw["w_down"], v[op.outputs[0]][: n * k], cfg.d_model,
+                             group_off=off, groups=E)
         elif kind == "moe_combine":
             src, rpos, rw, acc = (v[key] for key in op.inputs)
             hotpath.moe_combine(src[: n * k], rpos, rw, k, acc[r0:r1])
@@ -442,6 +451,9 @@ def reference_forward(model: RandomDLLM, x: torch.Tensor) -> torch.Tensor:
         if cfg.moe is not None:
             h = h + _moe_reference(cfg, lw, h)
             continue
+        if "w_gate_up" in lw:  # fused_ffn layout -> torch layout
+            wg, wu = _split_gate_up(lw["w_gate_up"], cfg.d_ff)
+            lw = {**lw, "w_gate": wg, "w_up": wu}
         up = h @ lw["w_up"]
         act = F.silu((h @ lw["w_gate"]).float()).mul(up.float()).to(torch.bfloat16) if cfg.gated_ffn else F.silu(up)
         h = h + act @ lw["w_down"]
@@ -453,6 +465,9 @@ def _moe_reference(cfg: ModelConfig, lw: dict, h: torch.Tensor) -> torch.Tensor:
     expert asc) over fp32 router logits, softmax over the selected logits,
     per-expert SwiGLU FFN, weighted fp32 sum."""
     E, k = cfg.moe.n_experts, cfg.moe.top_k
+    d, f = cfg.d_model, cfg.d_ff
+    wg, wu = _split_gate_up(lw["w_gate_up"].view(E, 2 * f, d), f)              # [E, d, f] each
+    wd = lw["w_down"].view(E, d, f).transpose(1, 2)                           # [E, f, d]
     logits = torch.mm(h, lw["w_router"], out_dtype=torch.float32)
     vals, idx = torch.sort(logits, dim=1, descending=True, stable=True)
     sel, wts = idx[:, :k], torch.softmax(vals[:, :k], dim=1)
@@ -462,8 +477,16 @@ def _moe_reference(cfg: ModelConfig, lw: dict, h: torch.Tensor) -> torch.Tensor:
         if rows.numel() == 0:
             continue
         x = h.index_select(0, rows)
-        up = x @ lw["w_up"][e]
-        act = F.silu((x @ lw["w_gate"][e]).float()).mul(up.float()).to(torch.bfloat16) if cfg.gated_ffn \
-            else F.silu(up)
-        out.index_add_(0, rows, wts[rows, j].unsqueeze(1) * (act @ lw["w_down"][e]).float())
+        up = x @ wu[e]
+        act = F.silu((x @ wg[e]).float()).mul(up.float()).to(torch.bfloat16)
+        out.index_add_(0, rows, wts[rows, j].unsqueeze(1) * (act @ wd[e]).float())
     return out.to(torch.bfloat16)
+
+
+def _split_gate_up(w_gu: torch.Tensor, f: int) -> tuple[torch.Tensor, torch.Tensor]:
+    """Inverse of hotpath.interleave_gate_up: [.., 2f, d] -> gate, up [.., d, f]."""
+    *lead, _, d = w_gu.shape
+    blocks = w_gu.reshape(*lead, f // 128, 2, 128, d)
+    gate = blocks[..., 0, :, :].reshape(*lead, f, d).transpose(-1, -2)
+    up = blocks[..., 1, :, :].reshape(*lead, f, d).transpose(-1, -2)
+    return gate, up

@@ -217,6 +217,42 @@ def moe_combine(src: torch.Tensor, comb_pos: torch.Tensor, comb_w: torch.Tensor,
                  src.shape[1], _p(out), out.stride(0), _s(stream))
 
 
+# ----------------------------------------------------------------- K10 (FFN GEMM)
+def interleave_gate_up(w_gate: torch.Tensor, w_up: torch.Tensor) -> torch.Tensor:
+    """[.., K, F] gate/up weights (torch layout) -> K10's SwiGLU operand
+    [.., 2F, K]: K-major, 128-row gate and up blocks alternating."""
+    *lead, K, F = w_gate.shape
+    if F % 128:
+        raise InputError(f"d_ff={F} must be a multiple of 128 for the fused SwiGLU GEMM")
+    g = w_gate.transpose(-1, -2).reshape(*lead, F // 128, 128, K)
+    u = w_up.transpose(-1, -2).reshape(*lead, F // 128, 128, K)
+    return torch.stack((g, u), dim=-3).reshape(*lead, 2 * F, K).contiguous()
+
+
+def ffn_gemm(a: torch.Tensor, w: torch.Tensor, out: torch.Tensor, n: int, group_off: Optional[torch.Tensor] = None,
+             groups: int = 1, m_host: int = 0, swiglu: bool = False, stream=None) -> None:
+    """K10: out[rows of group g] = a[rows of g] @ w[g].T (bf16, fp32 accumulate),
+    w = [groups * n, K] K-major; with ``swiglu`` out = silu(gate) * up, n/2 columns."""
+    if a.dtype != torch.bfloat16 or a.dim() != 2 or a.stride(1) != 1 or not a.is_cuda:
+        raise InputError("a must be 2-D bf16 with contiguous rows")
+    if out.dtype != torch.bfloat16 or out.dim() != 2 or out.stride(1) != 1:
+        raise InputError("out must be 2-D bf16 with contiguous rows")
+    _req(w, torch.bfloat16, "w")
+    K = a.shape[1]
+    if w.numel() != groups * n * K:
+        raise InputError(f"w must hold groups*n*K = {groups * n * K} elements")
+    if out.shape[1] < (n // 2 if swiglu else n):
+        raise InputError("out has too few columns")
+    if group_off is not None:
+        _req(group_off, torch.int32, "group_off")
+        if group_off.numel() < groups + 1:
+            raise InputError("group_off needs groups + 1 entries")
+    elif groups != 1:
+        raise InputError("several groups need device offsets")
+    _native.call("mosaic_ffn_gemm", _p(a), min(a.shape[0], out.shape[0]), a.stride(0), _p(group_off), int(groups),
+                 int(m_host), _p(w), int(n), K, int(bool(swiglu)), _p(out), out.stride(0), _s(stream))
+
+
 # ----------------------------------------------------------------- buffers
 class BufferLayout:
     """Bump layout of named buffers inside one device block (256 B aligned)."""

@@ -145,3 +145,25 @@ def test_fused_gather_template_matches_fused(env, K):
     for a, b in zip(res["fused"][:3], res["fused_gather"][:3]):
         assert torch.equal(a, b)
     assert res["fused_gather"][3] <= res["fused"][3]
+
+
+def test_fused_ffn_forward_matches_plain_torch(native_lib):
+    """fused_ffn=True: K10 gate/up GEMM with the SwiGLU epilogue inside the
+    arena, against the plain-PyTorch forward of the same weights."""
+    from paper_2601_06562_b200 import vmm, workload
+    from paper_2601_06562_b200.executor import RandomDLLM, StepExecutor, reference_forward
+
+    cfg = replace(workload.toy_configs()["tiny_llada"], fused_ffn=True)
+    dev = torch.device("cuda", 0)
+    model = RandomDLLM(cfg, dev, seed=4)
+    ws = vmm.reserve(4 << 30, backend="cuda")
+    try:
+        ex = StepExecutor(model, ws, MASK_ID)
+        L, M = 2048, 1024
+        x = _x(L, M, dev, seed=3)
+        ref = reference_forward(model, x.clone())
+        for K in ((1, 1), (1, 3)):
+            out = _step(cfg, ex, x.clone(), M, 16, K=K, keep=("l1.h_out",))
+            torch.testing.assert_close(out["kept"]["l1.h_out"].float(), ref.float(), rtol=2e-2, atol=2e-2)
+    finally:
+        ws.close()
