@@ -10,12 +10,12 @@ layer weights resident (random-init bf16). One denoising step at L = seq,
 r_p = 0.5 (M = L/2 masked), k = M/64 tokens committed. Two plans are run:
 
 * ``unchunked``: K = (1, 1) -- one FFN chunk of L*top_k dispatch rows;
-The expert FFN runs as K10 grouped tcgen05 GEMMs over the K8 expert
-segments (gate/up with the SwiGLU epilogue, then down), offsets on the device.
-
 * ``searched``: the reference's lazy bottleneck search (chunker.search_bottleneck)
   under an activation budget halfway between the non-chunkable floor and the
   unchunked peak, so the expert FFN must be chunked (K_FFN > 1).
+
+The expert FFN runs as K10 grouped tcgen05 GEMMs over the K8 expert
+segments (gate/up with the SwiGLU epilogue, then down), offsets on the device.
 
 Each is timed on the device (CUDA events, max of ``--steps`` after
 ``--warmup``) with a per-op-kind breakdown; the JSON line reports the step
