@@ -378,7 +378,8 @@ def context_fields() -> dict:
     the measured on-device sweep (bench_context.py) is read from profiles/."""
     from paper_2601_06562_b200 import chunker, workload
 
-    cfg = workload.ModelConfig("llada_8b", 32, D, 12288, 32, VOCAB, 2, 16 * 2 ** 30, True, "fused", "none")
+    cfg = workload.ModelConfig("llada_8b", 32, D, 12288, 32, VOCAB, 2, 16 * 2 ** 30, True, "fused", "none",
+                               fused_ffn=True)
     t = workload.build_layer_template(cfg)
     peak = chunker.evaluate_peak(t, {"L": SEQ, "M": round(MASK_RATIO * SEQ)}, chunker.ChunkConfig(1, 1))
     dense = chunker.evaluate_peak(workload.build_layer_template(

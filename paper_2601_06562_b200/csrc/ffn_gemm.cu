@@ -17,34 +17,45 @@
 // j, then up block j) so one 256-column tile holds matching gate and up
 // columns; it writes 128 act columns per tile.
 //
-// Structure as K3 (csrc/lmhead.cu), cta_group::1: warp 0 TMA producer, warp 1
-// TMEM allocator + single-thread tcgen05.mma issuer (M=128, N=256, K=16, BF16
-// -> FP32), warps 2-5 epilogue draining a double-buffered TMEM accumulator;
+// Structure as K3 (csrc/lmhead.cu): warp 0 TMA producer, warp 1 TMEM
+// allocator + single-thread tcgen05.mma issuer (cta_group::2 256x256 tiles over
+// an SM pair by default, cta_group::1 128x256 for tiny row counts; BF16 ->
+// FP32), warps 2-5 epilogue draining a double-buffered TMEM accumulator;
 // persistent CTAs walk (m-block, n-tile) units rasterised in groups of
 // `group_m` m-blocks so the weight tiles in flight are shared through L2.
 #include <cuda_bf16.h>
+
+#include <cstdlib>
 
 #include "common.cuh"
 
 namespace mosaic {
 namespace {
 
-constexpr int BM = 128;
-constexpr int BN = 256;
+constexpr int BM = 128;   // rows per CTA (TMEM lanes)
+constexpr int BN = 256;   // output (or gate|up) columns per tile
 constexpr int BK = 64;
 constexpr int UK = 16;
-constexpr int STAGES = 4;
-constexpr int A_BYTES = BM * BK * 2;
-constexpr int B_BYTES = BN * BK * 2;
-constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
 constexpr int NUM_ACC = 2;
 constexpr int TMEM_COLS = 512;
 constexpr int kThreads = 192;
 constexpr int kEpiWarps = 4;
 constexpr int kMaxGroups = 256;
 constexpr int kGroupM = 16;
-constexpr int SMEM = STAGES * STAGE_BYTES + 1024 + 256 + 2 * (kMaxGroups + 1) * 4;
-constexpr uint32_t IDESC = umma_idesc_bf16(BM, BN);
+
+// CG = 2: a CTA pair computes a 256 x 256 tile (tcgen05.mma.cta_group::2),
+// each CTA staging half of the rows and half of the weight columns, as K3.
+template <int CG>
+struct GCfg {
+  static constexpr int ROWS = BM * CG;   // rows per unit (UMMA M)
+  static constexpr int B_ROWS = BN / CG;  // weight rows staged per CTA
+  static constexpr int A_BYTES = BM * BK * 2;
+  static constexpr int B_BYTES = B_ROWS * BK * 2;
+  static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+  static constexpr int STAGES = CG == 1 ? 4 : 6;
+  static constexpr int SMEM = STAGES * STAGE_BYTES + 1024 + 256 + 2 * (kMaxGroups + 1) * 4;
+  static constexpr uint32_t IDESC = umma_idesc_bf16(ROWS, BN);
+};
 
 struct GParams {
   const int32_t* group_off;  // [G + 1] device row offsets, or null: one group of m_host rows
@@ -73,6 +84,7 @@ struct Unit {
   int nt;
 };
 
+template <int ROWS>
 __device__ __forceinline__ Unit unit_of(int64_t u, int n_tiles, int total_mb, const int32_t* s_off,
                                         const int32_t* s_mbp, int G) {
   const int64_t per_group = static_cast<int64_t>(kGroupM) * n_tiles;
@@ -89,15 +101,18 @@ __device__ __forceinline__ Unit unit_of(int64_t u, int n_tiles, int total_mb, co
   }
   Unit r;
   r.g = lo;
-  r.row0 = s_off[lo] + static_cast<int64_t>(gmb - s_mbp[lo]) * BM;
+  r.row0 = s_off[lo] + static_cast<int64_t>(gmb - s_mbp[lo]) * ROWS;
   r.row_end = s_off[lo + 1];
   r.nt = nt;
   return r;
 }
 
+template <int CG>
 __global__ void __launch_bounds__(kThreads, 1)
     k10_ffn_gemm(const __grid_constant__ CUtensorMap tmap_a, const __grid_constant__ CUtensorMap tmap_b,
                  const GParams p) {
+  using C = GCfg<CG>;
+  constexpr int STAGES = C::STAGES, A_BYTES = C::A_BYTES, B_BYTES = C::B_BYTES, STAGE_BYTES = C::STAGE_BYTES;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~static_cast<uintptr_t>(1023));
@@ -114,6 +129,9 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
   const int G = p.G;
+  const uint32_t rank = CG == 2 ? cluster_ctarank() : 0u;
+  const int64_t cluster = blockIdx.x / CG;
+  const int64_t n_clusters = gridDim.x / CG;
 
   if (threadIdx.x == 0) {
     tma_prefetch_desc(&tmap_a);
@@ -124,7 +142,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     for (int i = 0; i < NUM_ACC; ++i) {
       mbar_init(&tfull[i], 1);
-      mbar_init(&tempty[i], kEpiWarps);
+      mbar_init(&tempty[i], kEpiWarps * CG);
     }
     fence_mbar_init();
     // group row offsets and the exclusive prefix of their m-block counts
@@ -135,13 +153,13 @@ __global__ void __launch_bounds__(kThreads, 1)
       s_mbp[g] = mb;
       if (g < G) {
         const int32_t cnt = (p.group_off ? __ldg(p.group_off + g + 1) : static_cast<int32_t>(p.m_host)) - o;
-        mb += (cnt + BM - 1) / BM;
+        mb += (cnt + C::ROWS - 1) / C::ROWS;
       }
     }
   }
-  if (warp == 1) tmem_alloc<1>(tmem_slot, TMEM_COLS);
+  if (warp == 1) tmem_alloc<CG>(tmem_slot, TMEM_COLS);
   tc_fence_before();
-  __syncthreads();
+  if constexpr (CG == 2) cluster_sync(); else __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
   const int total_mb = s_mbp[G];
@@ -153,15 +171,20 @@ __global__ void __launch_bounds__(kThreads, 1)
       const uint64_t pol_a = policy_evict_last();
       const uint64_t pol_b = policy_evict_normal();
       uint32_t stage = 0, phase = 0;
-      for (int64_t u = blockIdx.x; u < units; u += gridDim.x) {
-        const Unit w = unit_of(u, p.n_tiles, total_mb, s_off, s_mbp, G);
-        const int32_t a_row = static_cast<int32_t>(w.row0);
-        const int32_t b_row = static_cast<int32_t>(w.g * p.N + static_cast<int64_t>(w.nt) * BN);
+      for (int64_t u = cluster; u < units; u += n_clusters) {
+        const Unit w = unit_of<C::ROWS>(u, p.n_tiles, total_mb, s_off, s_mbp, G);
+        const int32_t a_row = static_cast<int32_t>(w.row0 + rank * BM);
+        const int32_t b_row = static_cast<int32_t>(w.g * p.N + static_cast<int64_t>(w.nt) * BN + rank * C::B_ROWS);
         for (int kb = 0; kb < k_blocks; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
-          mbar_arrive_expect_tx(&full[stage], STAGE_BYTES);
-          tma_load_2d(sA + stage * A_BYTES, &tmap_a, &full[stage], kb * BK, a_row, pol_a);
-          tma_load_2d(sB + stage * B_BYTES, &tmap_b, &full[stage], kb * BK, b_row, pol_b);
+          if (rank == 0) mbar_arrive_expect_tx(&full[stage], STAGE_BYTES * CG);
+          if constexpr (CG == 1) {
+            tma_load_2d(sA + stage * A_BYTES, &tmap_a, &full[stage], kb * BK, a_row, pol_a);
+            tma_load_2d(sB + stage * B_BYTES, &tmap_b, &full[stage], kb * BK, b_row, pol_b);
+          } else {
+            tma_load_2d_cg2(sA + stage * A_BYTES, &tmap_a, &full[stage], kb * BK, a_row, pol_a);
+            tma_load_2d_cg2(sB + stage * B_BYTES, &tmap_b, &full[stage], kb * BK, b_row, pol_b);
+          }
           if (++stage == STAGES) {
             stage = 0;
             phase ^= 1;
@@ -170,10 +193,11 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
     }
   } else if (warp == 1) {
-    if (lane == 0) {
+    if (lane == 0 && rank == 0) {
       uint32_t stage = 0, phase = 0, acc = 0, acc_phase = 0;
-      for (int64_t u = blockIdx.x; u < units; u += gridDim.x) {
-        mbar_wait(&tempty[acc], acc_phase ^ 1);
+      for (int64_t u = cluster; u < units; u += n_clusters) {
+        if constexpr (CG == 2) mbar_wait_cluster(&tempty[acc], acc_phase ^ 1);
+        else mbar_wait(&tempty[acc], acc_phase ^ 1);
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + acc * BN;
         for (int kb = 0; kb < k_blocks; ++kb) {
@@ -183,15 +207,15 @@ __global__ void __launch_bounds__(kThreads, 1)
           const uint32_t b0 = smem_u32(sB + stage * B_BYTES);
 #pragma unroll
           for (int kk = 0; kk < BK / UK; ++kk)
-            umma_bf16<1>(d_tmem, umma_desc_sw128(a0 + kk * UK * 2), umma_desc_sw128(b0 + kk * UK * 2), IDESC,
-                         (kb | kk) != 0);
-          umma_commit<1>(&empty[stage]);
+            umma_bf16<CG>(d_tmem, umma_desc_sw128(a0 + kk * UK * 2), umma_desc_sw128(b0 + kk * UK * 2), C::IDESC,
+                          (kb | kk) != 0);
+          umma_commit<CG>(&empty[stage]);
           if (++stage == STAGES) {
             stage = 0;
             phase ^= 1;
           }
         }
-        umma_commit<1>(&tfull[acc]);
+        umma_commit<CG>(&tfull[acc]);
         if (++acc == NUM_ACC) {
           acc = 0;
           acc_phase ^= 1;
@@ -201,10 +225,11 @@ __global__ void __launch_bounds__(kThreads, 1)
   } else {
     const int q = warp & 3;
     const int row_local = q * 32 + lane;
+    const uint32_t tempty_addr0 = CG == 2 ? mapa_shared(smem_u32(&tempty[0]), 0) : smem_u32(&tempty[0]);
     uint32_t acc = 0, acc_phase = 0;
-    for (int64_t u = blockIdx.x; u < units; u += gridDim.x) {
-      const Unit w = unit_of(u, p.n_tiles, total_mb, s_off, s_mbp, G);
-      const int64_t row = w.row0 + row_local;
+    for (int64_t u = cluster; u < units; u += n_clusters) {
+      const Unit w = unit_of<C::ROWS>(u, p.n_tiles, total_mb, s_off, s_mbp, G);
+      const int64_t row = w.row0 + rank * BM + row_local;
       const bool live = row < w.row_end;
       mbar_wait(&tfull[acc], acc_phase);
       tc_fence_after();
@@ -253,7 +278,10 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(&tempty[acc]);
+      if (lane == 0) {
+        if constexpr (CG == 2) mbar_arrive_cluster(tempty_addr0 + acc * 8);
+        else mbar_arrive(&tempty[acc]);
+      }
       if (++acc == NUM_ACC) {
         acc = 0;
         acc_phase ^= 1;
@@ -262,11 +290,39 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
 
   tc_fence_before();
-  __syncthreads();
+  if constexpr (CG == 2) cluster_sync(); else __syncthreads();
   if (warp == 1) {
     tc_fence_after();
-    tmem_dealloc<1>(tmem_base, TMEM_COLS);
+    tmem_dealloc<CG>(tmem_base, TMEM_COLS);
   }
+}
+
+template <int CG>
+int launch_k10(const CUtensorMap& ta, const CUtensorMap& tb, const GParams& p, int64_t rows_cap,
+               cudaStream_t stream) {
+  using C = GCfg<CG>;
+  static bool attr_set = false;
+  if (!attr_set) {
+    MOSAIC_CUDA(cudaFuncSetAttribute(k10_ffn_gemm<CG>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
+    attr_set = true;
+  }
+  const int64_t units_cap = (ceil_div(rows_cap, C::ROWS) + p.G) * p.n_tiles;
+  const int64_t workers = num_sms() / CG;
+  const int64_t clusters = units_cap < workers ? units_cap : workers;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(static_cast<unsigned>(clusters * CG));
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = C::SMEM;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = CG;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  MOSAIC_CUDA(cudaLaunchKernelEx(&cfg, k10_ffn_gemm<CG>, ta, tb, p));
+  return MOSAIC_OK;
 }
 
 }  // namespace
@@ -291,10 +347,15 @@ extern "C" int mosaic_ffn_gemm(const uint16_t* A, int64_t rows_cap, int64_t lda,
                      (reinterpret_cast<uintptr_t>(C) & 15) == 0,
                  "A, W, C must be 16-byte aligned");
   if (rows_cap == 0) return MOSAIC_OK;
+  static const int forced = [] {
+    const char* e = getenv("MOSAIC_K10_CTA_GROUP");
+    return e ? atoi(e) : 0;
+  }();
+  const int cg = forced == 1 || forced == 2 ? forced : (rows_cap > BM ? 2 : 1);
   CUtensorMap ta, tb;
   int st = encode_tma_bf16(&ta, A, rows_cap, K, lda, BM, BK);
   if (st) return st;
-  st = encode_tma_bf16(&tb, W, G * N, K, K, BN, BK);
+  st = encode_tma_bf16(&tb, W, G * N, K, K, BN / cg, BK);
   if (st) return st;
   GParams p{};
   p.group_off = group_off;
@@ -306,13 +367,8 @@ extern "C" int mosaic_ffn_gemm(const uint16_t* A, int64_t rows_cap, int64_t lda,
   p.swiglu = swiglu ? 1 : 0;
   p.C = C;
   p.ldc = ldc;
-  static bool attr_set = false;
-  if (!attr_set) {
-    MOSAIC_CUDA(cudaFuncSetAttribute(k10_ffn_gemm, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM));
-    attr_set = true;
-  }
-  const int64_t units_cap = (ceil_div(rows_cap, BM) + G) * p.n_tiles;
-  const int64_t grid = units_cap < num_sms() ? units_cap : num_sms();
-  k10_ffn_gemm<<<static_cast<unsigned>(grid), kThreads, SMEM, as_stream(stream)>>>(ta, tb, p);
+  st = cg == 2 ? launch_k10<2>(ta, tb, p, rows_cap, as_stream(stream))
+               : launch_k10<1>(ta, tb, p, rows_cap, as_stream(stream));
+  if (st) return st;
   return check_launch("mosaic_ffn_gemm");
 }
