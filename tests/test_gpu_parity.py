@@ -424,3 +424,51 @@ def test_mask_only_head_fused_gather_equals_buffered(dev, shift):
     for a, b in zip(outs[0][:4], outs[1][:4]):
         assert torch.equal(a, b)
     assert outs[1][4] < outs[0][4] - L * d  # the [m_cap, d] buffer is gone
+
+
+# ----------------------------------------------------------------------- full BASELINE sizes
+@pytest.mark.parametrize("name,L,d,V,shift,k", [("llada_32k", 32768, 4096, 126464, False, 256),
+                                                ("dream_128k", 131072, 3584, 152064, True, 1024)])
+def test_full_size_step_properties(dev, name, L, d, V, shift, k):
+    """The fused step at BASELINE configs[1] / configs[2] sizes. The fp64
+    oracle is too slow for every row, so: (a) 256 sampled masked rows against
+    the oracle on exactly those rows (token where the margin > 1e-3, lse/conf
+    1e-3 relative); (b) size-independent invariants over all M rows: exactly k
+    commits, the committed set is the top-k of the device confidences (ties ->
+    lower position), committed tokens are the device argmax, 0 < conf <= 1,
+    lse >= the sampled rows' max logit."""
+    from paper_2601_06562_b200 import MaskOnlyHead
+
+    g = torch.Generator(device=dev).manual_seed(L)
+    M = L // 2
+    mask_id = V - 1
+    H = torch.randn(L, d, generator=g, device=dev).to(torch.bfloat16)
+    W = (torch.randn(V, d, generator=g, device=dev) * 0.02).to(torch.bfloat16)
+    x = torch.randint(0, V - 1, (L,), generator=g, device=dev, dtype=torch.int32)
+    x[torch.randperm(L, generator=g, device=dev)[:M]] = mask_id  # scattered layout
+    x0 = x.clone()
+    head = MaskOnlyHead(W, seq_len=L, mask_id=mask_id, shift=shift)
+    out = head.step(x, H, k)
+    torch.cuda.synchronize()
+    Mdev = int(out.m_dev.item())
+    assert Mdev == M
+    idx = out.idx[:M].cpu().numpy()
+    assert np.array_equal(idx, np.flatnonzero(x0.cpu().numpy() == mask_id))
+    tok, lse, conf = out.token[:M].cpu().numpy(), out.lse[:M].cpu().numpy(), out.conf[:M].cpu().numpy()
+    assert np.all(conf > 0) and np.all(conf <= 1.0) and np.all(np.isfinite(lse))
+    assert np.all((tok >= 0) & (tok < V))
+    sel = out.selected[:M].cpu().numpy().astype(bool)
+    assert sel.sum() == k
+    assert np.array_equal(sel, orc.remask_select(conf, idx, k))
+    xo = x.cpu().numpy()
+    assert np.array_equal(xo[idx[sel]], tok[sel]) and np.all(xo[idx[~sel]] == mask_id)
+    # sampled rows vs the fp64 oracle
+    rows = np.sort(np.random.default_rng(1).choice(M, 256, replace=False))
+    src = np.maximum(idx[rows] - 1, 0) if shift else idx[rows]
+    Hs = H[torch.from_numpy(src).to(dev).long()].float().cpu().numpy().astype(np.float64)
+    ref = orc.softmax_stats(orc.logits_f64(Hs, W.float().cpu().numpy().astype(np.float64)))
+    ok = ref["margin"] > MARGIN
+    assert np.array_equal(tok[rows][ok], ref["arg"][ok])
+    assert orc.isclose_rel(lse[rows], ref["lse"], LSE_REL)
+    assert orc.isclose_rel(conf[rows], ref["conf"], CONF_REL)
+    assert np.all(lse[rows] >= ref["max"] - 1e-3)
