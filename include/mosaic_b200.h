@@ -204,6 +204,14 @@ MOSAIC_API int mosaic_arena_info(const mosaic_arena* arena, uint64_t* base, uint
                       uint64_t* committed, uint64_t* granularity);
 MOSAIC_API int mosaic_arena_release(mosaic_arena* arena);
 
+/* Plan-executor canaries (execute_plan, mosaic/vmm.py:188-291) on device
+ * memory: fill [ptr, ptr+nbytes) with the 8-byte tag repeated from ptr; check
+ * adds to *mismatch_count (device uint32) when any byte differs. ptr 8-byte
+ * aligned (plan offsets are).                                                 */
+MOSAIC_API int mosaic_tag_fill(void* ptr, int64_t nbytes, uint64_t tag, void* stream);
+MOSAIC_API int mosaic_tag_check(const void* ptr, int64_t nbytes, uint64_t tag, uint32_t* mismatch_count,
+                     void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -28,7 +28,7 @@ from .dims import Dim, ceildiv, const, parse_dim, sym
 from .graph import ConcreteGraph, GraphTemplate, load_template, new_template, template_from_json_dict
 from .liveness import LifetimeTable, StorageGroup, analyze, max_live
 from .planner import MemoryPlan, PlanStats, plan_exact, plan_first_fit, validate
-from .vmm import Workspace, commit_to, reserve
+from .vmm import ExecutionReport, Fault, Workspace, commit_to, execute_plan, reserve
 from .workload import (
     ModelConfig,
     MoEConfig,

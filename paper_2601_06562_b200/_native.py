@@ -77,6 +77,8 @@ SIGNATURES: dict[str, tuple[object, list[object]]] = {
     "mosaic_arena_commit": (c_int, [c_void_p, c_uint64]),
     "mosaic_arena_info": (c_int, [c_void_p, _u64p, _u64p, _u64p, _u64p]),
     "mosaic_arena_release": (c_int, [c_void_p]),
+    "mosaic_tag_fill": (c_int, [c_void_p, c_int64, c_uint64, c_void_p]),
+    "mosaic_tag_check": (c_int, [c_void_p, c_int64, c_uint64, c_void_p, c_void_p]),
 }
 
 _lock = threading.Lock()

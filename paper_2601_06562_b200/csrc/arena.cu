@@ -166,3 +166,63 @@ extern "C" int mosaic_arena_release(mosaic_arena* a) {
   delete a;
   return st;
 }
+
+// ---------------------------------------------------------------- canaries
+// Plan-executor canaries on the device (mosaic/vmm.py:188-291 `execute_plan`):
+// a defined group's range is filled with its 8-byte tag repeated from the
+// range start; a read verifies the whole range still carries it, so any
+// overlap between simultaneously live groups shows up even away from the
+// range start.
+namespace mosaic {
+namespace {
+
+__device__ __forceinline__ uint8_t tag_byte(uint64_t tag, int64_t i) {
+  return static_cast<uint8_t>(tag >> (8 * (i & 7)));
+}
+
+__global__ void k7_tag_fill(uint8_t* p, int64_t n, uint64_t tag) {
+  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  const int64_t n8 = n / 8;
+  uint64_t* p8 = reinterpret_cast<uint64_t*>(p);  // range starts are plan-aligned (>= 8 B)
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n8; i += stride) p8[i] = tag;
+  for (int64_t i = n8 * 8 + blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n; i += stride)
+    p[i] = tag_byte(tag, i);
+}
+
+__global__ void k7_tag_check(const uint8_t* p, int64_t n, uint64_t tag, unsigned int* bad) {
+  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  const int64_t n8 = n / 8;
+  const uint64_t* p8 = reinterpret_cast<const uint64_t*>(p);
+  bool ok = true;
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n8; i += stride) ok &= p8[i] == tag;
+  for (int64_t i = n8 * 8 + blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n; i += stride)
+    ok &= p[i] == tag_byte(tag, i);
+  if (!__all_sync(0xffffffffu, ok) && (threadIdx.x & 31) == 0) atomicAdd(bad, 1u);
+}
+
+int tag_grid(int64_t n) {
+  const int64_t want = ceil_div(n / 8 > 0 ? n / 8 : 1, 256);
+  const int64_t cap = static_cast<int64_t>(num_sms()) * 4;
+  return static_cast<int>(want < cap ? want : cap);
+}
+
+}  // namespace
+}  // namespace mosaic
+
+extern "C" int mosaic_tag_fill(void* ptr, int64_t nbytes, uint64_t tag, void* stream) {
+  MOSAIC_REQUIRE(nbytes >= 0, "negative size");
+  if (nbytes == 0) return MOSAIC_OK;
+  MOSAIC_REQUIRE(ptr && (reinterpret_cast<uintptr_t>(ptr) & 7) == 0, "range must be 8-byte aligned");
+  k7_tag_fill<<<tag_grid(nbytes), 256, 0, as_stream(stream)>>>(static_cast<uint8_t*>(ptr), nbytes, tag);
+  return check_launch("mosaic_tag_fill");
+}
+
+extern "C" int mosaic_tag_check(const void* ptr, int64_t nbytes, uint64_t tag, uint32_t* mismatch_count,
+                                void* stream) {
+  MOSAIC_REQUIRE(nbytes >= 0 && mismatch_count, "bad arguments");
+  if (nbytes == 0) return MOSAIC_OK;
+  MOSAIC_REQUIRE(ptr && (reinterpret_cast<uintptr_t>(ptr) & 7) == 0, "range must be 8-byte aligned");
+  k7_tag_check<<<tag_grid(nbytes), 256, 0, as_stream(stream)>>>(static_cast<const uint8_t*>(ptr), nbytes, tag,
+                                                                 mismatch_count);
+  return check_launch("mosaic_tag_check");
+}
