@@ -39,6 +39,8 @@ def parse():
     ap.add_argument("--impl", choices=["b200", "reference"], default="b200")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--exchange", choices=["nccl", "p2p"], default="nccl",
+                    help="N>1: NCCL all-gather of the triples, or K4x peer-memory push (symmetric memory)")
     return ap.parse_args()
 
 
@@ -211,7 +213,8 @@ def gpu_main(args):
     if persist:
         from paper_2601_06562_b200 import hotpath as _hp
         _hp.l2_persisting_limit(persist)
-    head = MaskOnlyHead(W, seq_len=SEQ, mask_id=MASK_ID, vocab_offset=v0, m_cap=M, group=group)
+    head = MaskOnlyHead(W, seq_len=SEQ, mask_id=MASK_ID, vocab_offset=v0, m_cap=M, group=group,
+                        exchange=args.exchange)
     stream = torch.cuda.current_stream()
     # ours per step: K1 x2, K2, K3, K4 (+ the rank-order K4 after the all-gather), K5 (single-CTA, m_cap <= 65536)
     launches_per_step = 6 + (1 if world > 1 else 0)
@@ -347,7 +350,7 @@ def gpu_main(args):
         "data": "synthetic (seeded N(0,1) hidden, N(0,0.02^2) LM head, random-init; no checkpoint)",
         "config": {"workload": "llada8b_32k_mask50", "d_model": D, "vocab": VOCAB, "seq_len": SEQ,
                    "masked": M, "unmask_k": k, "mask_layout": "suffix (step 0)",
-                   "parallelism": f"vocab-sharded x{world}" if world > 1 else "single GPU",
+                   "parallelism": f"vocab-sharded x{world} ({args.exchange} exchange)" if world > 1 else "single GPU",
                    "vocab_shard": v1 - v0, "n_splits": head.n_splits,
                    "l2": "inputs larger than L2 (W 1.04 GB, H 268 MB > 126 MB)"},
         "roofline": {"bound": "tensor", "kernel": "k3_lmhead (tcgen05 stats GEMM)",

@@ -9,7 +9,7 @@ from __future__ import annotations
 import ctypes
 import os
 import threading
-from ctypes import POINTER, c_char_p, c_int, c_int32, c_int64, c_size_t, c_uint64, c_void_p
+from ctypes import POINTER, c_char_p, c_int, c_int32, c_int64, c_size_t, c_uint32, c_uint64, c_void_p
 from pathlib import Path
 
 from .errors import raise_for_status
@@ -51,6 +51,12 @@ SIGNATURES: dict[str, tuple[object, list[object]]] = {
         [c_void_p, c_void_p, c_void_p, c_int32, c_int64, c_void_p, c_int64, c_int64,
          c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p],
     ),
+    "mosaic_stats_exchange_push": (
+        c_int,
+        [c_void_p, c_void_p, c_void_p, c_int32, c_int64, c_void_p, c_int64, c_int64, c_void_p, c_void_p,
+         c_int32, c_int32, c_uint32, c_void_p, c_void_p],
+    ),
+    "mosaic_stats_exchange_wait": (c_int, [c_void_p, c_int32, c_uint32, c_void_p]),
     "mosaic_remask_scratch_bytes": (c_size_t, []),
     "mosaic_remask_commit": (
         c_int,

@@ -306,7 +306,8 @@ class MaskOnlyHead:
 
     def __init__(self, weight_shard: torch.Tensor, *, seq_len: int, mask_id: int,
                  vocab_offset: int = 0, m_cap: Optional[int] = None, shift: bool = False,
-                 group=None, block: Optional[torch.Tensor] = None, fused_gather: bool = False):
+                 group=None, block: Optional[torch.Tensor] = None, fused_gather: bool = False,
+                 exchange="nccl"):
         _req(weight_shard, torch.bfloat16, "weight_shard", 2)
         self.weight = weight_shard
         self.v_shard, self.d = weight_shard.shape
@@ -317,6 +318,9 @@ class MaskOnlyHead:
         self.shift = bool(shift)
         self.group = group
         self.fused_gather = bool(fused_gather)  # K3 reads rows of `hidden` directly: no K2, no hc buffer
+        if not (exchange in ("nccl", "p2p") or hasattr(exchange, "push")):
+            raise InputError(f"exchange must be 'nccl', 'p2p' or a P2PExchange, got {exchange!r}")
+        self.exchange = exchange
         self.world = 1
         if group is not None:
             import torch.distributed as dist
@@ -341,6 +345,14 @@ class MaskOnlyHead:
         lay.add("selected", (m,), torch.int32)
         lay.add("remask_scratch", (remask_scratch_bytes(),), torch.uint8)
         self.layout = lay
+        self.p2p = None
+        if hasattr(exchange, "push"):  # a prepared P2PExchange (peer buffers set up by the caller)
+            self.p2p = exchange
+            self.world = exchange.world
+        elif group is not None and exchange == "p2p":
+            from .shard import P2PExchange
+
+            self.p2p = P2PExchange(self.m_cap, group, weight_shard.device)
         if block is None:
             block = torch.empty(lay.size, dtype=torch.uint8, device=weight_shard.device)
         self.block = block
@@ -366,9 +378,15 @@ class MaskOnlyHead:
             lmhead_stats(b["hc"], self.weight, self.n_splits, b["part_max"], b["part_sum"],
                          b["part_arg"], m_dev=m_dev, v_offset=self.vocab_offset, stream=stream)
         m, S = self.m_cap, self.n_splits
-        if self.group is None:
+        if self.group is None and self.p2p is None:
             stats_merge(b["part_max"], b["part_sum"], b["part_arg"], S, m, m, m_dev=m_dev,
                         token=b["token"], lse=b["lse"], conf=b["conf"], stream=stream)
+        elif self.p2p is not None:  # K4x: merge + peer stores + signal, then wait; no NCCL call
+            self.p2p.push(b["part_max"], b["part_sum"], b["part_arg"], S, m, m_dev=m_dev, stream=stream)
+            self.p2p.wait(stream)
+            g = self.p2p.gathered
+            stats_merge(g[0, 0], g[0, 1], g[0, 2].view(torch.int32), self.world, 3 * m, m,
+                        m_dev=m_dev, token=b["token"], lse=b["lse"], conf=b["conf"], stream=stream)
         else:
             from .shard import exchange_triples
 

@@ -41,6 +41,68 @@ def exchange_triples(local: torch.Tensor, group=None, out: torch.Tensor | None =
     return out
 
 
+class P2PExchange:
+    """The exchange fused into the split merge over NVLink peer memory (K4x,
+    csrc/exchange.cu): symmetric ``gathered`` [P, 3, m] fp32 and ``signal`` [P]
+    uint32 buffers (torch symmetric memory), their peers' device pointers, and
+    a per-step epoch. ``push`` merges this rank's S split triples per row and
+    stores them into every rank's gathered slot [rank], then signals; ``wait``
+    blocks the stream until every rank has signalled this epoch. No NCCL call
+    on the step path."""
+
+    def __init__(self, m_cap: int, group, device):
+        import torch.distributed._symmetric_memory as symm_mem
+
+        world, rank = dist.get_world_size(group), dist.get_rank(group)
+        gathered = symm_mem.empty((world, 3, int(m_cap)), dtype=torch.float32, device=device)
+        signal = symm_mem.empty((world,), dtype=torch.int32, device=device)
+        signal.zero_()
+        torch.cuda.synchronize(device)
+        hg = symm_mem.rendezvous(gathered, group)
+        hs = symm_mem.rendezvous(signal, group)
+        self._init(gathered, signal, list(hg.buffer_ptrs), list(hs.buffer_ptrs), rank, world)
+        dist.barrier(group)  # every rank's pads are zero before anyone signals
+
+    @classmethod
+    def from_buffers(cls, gathered: torch.Tensor, signal: torch.Tensor, peer_gathered: list, peer_signal: list,
+                     rank: int, world: int) -> "P2PExchange":
+        """Peers given as raw device pointers (e.g. CUDA-IPC mappings of the
+        other processes' buffers); ``signal`` must be zeroed on every rank
+        before the first push."""
+        self = cls.__new__(cls)
+        self._init(gathered, signal, peer_gathered, peer_signal, rank, world)
+        return self
+
+    def _init(self, gathered, signal, peer_gathered, peer_signal, rank, world):
+        device = gathered.device
+        self.world, self.rank, self.m_cap = int(world), int(rank), int(gathered.shape[-1])
+        self.gathered, self.signal = gathered, signal
+        self._peer_gathered = torch.tensor([int(p) for p in peer_gathered], dtype=torch.int64, device=device)
+        self._peer_signal = torch.tensor([int(p) for p in peer_signal], dtype=torch.int64, device=device)
+        self._done = torch.zeros(1, dtype=torch.int32, device=device)
+        self.epoch = 0
+
+    def push(self, part_max, part_sum, part_arg, S: int, stride: int, m_dev=None, m_host: int = 0, stream=None):
+        import ctypes
+
+        from . import _native
+        from .hotpath import _p, _s
+
+        self.epoch = (self.epoch + 1) & 0xFFFFFFFF or 1
+        _native.call("mosaic_stats_exchange_push", _p(part_max), _p(part_sum), _p(part_arg), int(S), int(stride),
+                     _p(m_dev), int(m_host), self.m_cap, _p(self._peer_gathered), _p(self._peer_signal),
+                     self.rank, self.world, ctypes.c_uint32(self.epoch), _p(self._done), _s(stream))
+
+    def wait(self, stream=None):
+        import ctypes
+
+        from . import _native
+        from .hotpath import _p, _s
+
+        _native.call("mosaic_stats_exchange_wait", _p(self.signal), self.world, ctypes.c_uint32(self.epoch),
+                     _s(stream))
+
+
 def pack_triples(mx: torch.Tensor, sm: torch.Tensor, arg: torch.Tensor) -> torch.Tensor:
     """[3, m] fp32 block with the int32 argmax stored bit-exactly in row 2."""
     out = torch.empty((3, mx.numel()), dtype=torch.float32, device=mx.device)
