@@ -67,6 +67,7 @@ struct Params {
   int32_t tiles_per_split;
   int32_t n_splits;
   int32_t group_m;
+  int32_t seg_splits;  // vocab segments of this many splits, processed segment-major (0 = one segment)
   int32_t epilogue;  // 0 = skip the statistics math (power/overlap experiments only)
   int32_t policy;   // L2 policy of (A, B) loads: 0 = (evict_normal, evict_normal), 1 = (evict_last, evict_normal), 2 = (evict_normal, evict_first)
   int64_t v_offset;
@@ -81,13 +82,24 @@ struct Params {
   int32_t shift;       // gather mode: src(p) = max(p - 1, 0) (Dream token shift)
 };
 
+// Unit order: vocab segments of `seg_splits` consecutive splits, outermost;
+// inside a segment, groups of `group_m` m-blocks, then the segment's splits,
+// then m-blocks fastest. With segments sized so one segment's LM-head rows fit
+// in L2 (like a 1/8 vocab shard), every m-group re-reads them from L2 instead
+// of DRAM, while each group's gathered rows stay resident across the
+// segment's splits.
 __device__ __forceinline__ void unit_coords(const Params& p, int m_blocks, int64_t u, int& mb,
                                             int& s) {
-  const int64_t per_group = static_cast<int64_t>(p.group_m) * p.n_splits;
-  const int64_t g = u / per_group;
-  const int64_t rem = u - g * per_group;
+  const int64_t seg_splits = p.seg_splits > 0 ? p.seg_splits : p.n_splits;
+  const int64_t per_seg = static_cast<int64_t>(m_blocks) * seg_splits;
+  const int64_t seg = u / per_seg;
+  const int64_t su = u - seg * per_seg;
+  const int64_t s_in = min(seg_splits, static_cast<int64_t>(p.n_splits) - seg * seg_splits);
+  const int64_t per_group = static_cast<int64_t>(p.group_m) * s_in;
+  const int64_t g = su / per_group;
+  const int64_t rem = su - g * per_group;
   const int64_t gm = min(static_cast<int64_t>(p.group_m), m_blocks - g * p.group_m);
-  s = static_cast<int>(rem / gm);
+  s = static_cast<int>(seg * seg_splits + rem / gm);
   mb = static_cast<int>(g * p.group_m + rem % gm);
 }
 
@@ -582,6 +594,8 @@ int launch(const ASource& a, int64_t m_cap, const int32_t* m_dev, int64_t m_host
   p.idx = a.idx;
   p.shift = a.shift;
   if (p.group_m <= 0) p.group_m = group_m_default() > 0 ? group_m_default() : 16;
+  static const int seg_splits = env_int("MOSAIC_K3_SEG_SPLITS", 0);
+  p.seg_splits = seg_splits;
   static const int policy = env_int("MOSAIC_L2_POLICY", 1);  // measured best: A evict_last
   p.policy = policy;
   static const int epilogue = env_int("MOSAIC_K3_EPILOGUE", 1);
