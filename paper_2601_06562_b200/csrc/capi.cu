@@ -1,5 +1,6 @@
 // C-ABI plumbing shared by every entry point: thread-local error messages,
 // launch checking, device properties and driver entry-point lookup.
+#include <cstdlib>
 #include <mutex>
 #include <unordered_map>
 
@@ -71,9 +72,18 @@ int encode_tma_bf16(CUtensorMap* map, const void* base, int64_t rows, int64_t K,
   const cuuint64_t strides[1] = {static_cast<cuuint64_t>(ld) * 2};
   const cuuint32_t box[2] = {static_cast<cuuint32_t>(box_cols), static_cast<cuuint32_t>(box_rows)};
   const cuuint32_t elem_strides[2] = {1, 1};
+  // L2 promotion of TMA reads (experiment knob MOSAIC_TMA_L2_PROMOTION: 0 none, 1 64B, 2 128B, 3 256B)
+  static const int promo = [] {
+    const char* e = getenv("MOSAIC_TMA_L2_PROMOTION");
+    return e ? atoi(e) : 3;
+  }();
+  const CUtensorMapL2promotion pr = promo == 0 ? CU_TENSOR_MAP_L2_PROMOTION_NONE
+                                    : promo == 1 ? CU_TENSOR_MAP_L2_PROMOTION_L2_64B
+                                    : promo == 2 ? CU_TENSOR_MAP_L2_PROMOTION_L2_128B
+                                                 : CU_TENSOR_MAP_L2_PROMOTION_L2_256B;
   CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box,
-                  elem_strides, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
-                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+                  elem_strides, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, pr,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) return fail(MOSAIC_E_CUDA, "cuTensorMapEncodeTiled failed (%d)", int(r));
   return MOSAIC_OK;
 }
