@@ -53,6 +53,11 @@ def _stale(objs: list[Path]) -> bool:
     return any(p.stat().st_mtime > t for p in deps)
 
 
+def _extra_defines() -> list[str]:
+    """Experiment-only compile-time knobs, e.g. MOSAIC_NVCC_DEFINES="MOSAIC_K3_STAGES2=7"."""
+    return [f"-D{d}" for d in os.environ.get("MOSAIC_NVCC_DEFINES", "").split() if d]
+
+
 def build(force: bool = False, verbose: bool = False) -> Path:
     srcs = sources()
     objs = [BUILD / (s.stem + ".o") for s in srcs]
@@ -63,7 +68,7 @@ def build(force: bool = False, verbose: bool = False) -> Path:
 
     def compile_one(pair):
         src, obj = pair
-        cmd = [nvcc, *ARCH, *NVCC_FLAGS, "-I", str(REPO / "include"), "-c", str(src), "-o", str(obj)]
+        cmd = [nvcc, *ARCH, *NVCC_FLAGS, *_extra_defines(), "-I", str(REPO / "include"), "-c", str(src), "-o", str(obj)]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             raise RuntimeError(f"nvcc failed for {src.name}:\n{r.stderr}")

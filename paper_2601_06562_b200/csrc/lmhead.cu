@@ -52,7 +52,10 @@ struct Cfg {
   static constexpr int A_BYTES = BM * BK * 2;
   static constexpr int B_BYTES = B_ROWS * BK * 2;
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
-  static constexpr int STAGES = CG == 1 ? 4 : 6;
+#ifndef MOSAIC_K3_STAGES2
+#define MOSAIC_K3_STAGES2 6
+#endif
+  static constexpr int STAGES = CG == 1 ? 4 : MOSAIC_K3_STAGES2;
   static constexpr int SMEM = STAGES * STAGE_BYTES + 1024 + 256 + BM * 4;  // + gather row indices
   static constexpr uint32_t IDESC = umma_idesc_bf16(ROWS, BN);
 };

@@ -138,14 +138,16 @@ def ex_graph(cfg, L, M, K):
     return t.instantiate({"L": L, "M": M, "K_logits": K[0], "K_FFN": K[1]})
 
 
-def test_moe_fused_step_vs_oracle(env, dev):
-    """The hot path (K1-K5) after the in-arena MoE forward, checked against the
-    CPU oracle on the executor's own final hidden states."""
+@pytest.mark.parametrize("mode", ["fused", "fused_gather"])
+def test_moe_fused_step_vs_oracle(env, dev, mode):
+    """The hot path (K1-K5, or K1 + gather-mode K3 + K4/K5) after the in-arena
+    MoE forward, checked against the CPU oracle on the executor's own final
+    hidden states."""
     cfg, model, ex = env
     L, M, k = 2048, 1024, 64
     x = _x(L, M, dev, seed=4)
     x0 = x.cpu().numpy()
-    out = ex.run(ex_graph(cfg, L, M, (2, 3)), x, k, keep=("l1.h_out", "token_out"))
+    out = ex.run(ex_graph(replace(cfg, logits_mode=mode), L, M, (2, 3)), x, k, keep=("l1.h_out", "token_out"))
     h = out["kept"]["l1.h_out"].float().cpu().numpy().astype(np.float64)
     ref = orc.step(x0, h, model.w_vocab.float().cpu().numpy().astype(np.float64), MASK_ID, k)
     tok = out["kept"]["token_out"].cpu().numpy()
