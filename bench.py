@@ -389,13 +389,13 @@ def context_fields() -> dict:
         workload.ModelConfig("llada_8b", 32, D, 12288, 32, VOCAB, 2, 16 * 2 ** 30, True, "eager", "none")),
         {"L": SEQ, "M": round(MASK_RATIO * SEQ)}, chunker.ChunkConfig(1, 1))
     out = {"peak_activation_gb": peak.total_peak / 1e9, "peak_activation_gb_dense_logits_plan": dense.total_peak / 1e9}
-    sweep = ROOT / "profiles" / "r01_context_sweep.json"
+    sweep = ROOT / "profiles" / "r01e_context_sweep.json"
     if sweep.exists():
         d = json.loads(sweep.read_text())
         out["max_seq_len"] = d.get("pipeline_lmax_measured")
         out["max_seq_len_planned"] = d.get("planned_lmax", {}).get("fused_chunking")
         out["max_seq_len_dense_baseline"] = d.get("baseline_lmax")
-        out["max_seq_len_source"] = "profiles/r01_context_sweep.json (bench_context.py on one B200)"
+        out["max_seq_len_source"] = "profiles/r01e_context_sweep.json (bench_context.py on one B200)"
     return out
 
 
