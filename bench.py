@@ -366,7 +366,7 @@ def gpu_main(args):
         **context_fields(),
     }
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        cpu = run_cpu_reference(steps=2, warmup=0)
+        cpu = run_cpu_reference(steps=8, warmup=1)  # ~10 s of host work (bounded sample)
         line["cpu_baseline"] = {"value": cpu["value"], "unit": "masked tokens/s", "cores": cpu["cores"],
                                 "kind": "port", "sample": cpu["sample"]}
     if rank == 0:
