@@ -107,6 +107,25 @@ MOSAIC_API int mosaic_lmhead_stats(const uint16_t* Hc, int64_t m_cap, const int3
                         int32_t n_splits, float* part_max, float* part_sum, int32_t* part_arg,
                         void* stream);
 
+/* K3 with the die-aware unit schedule: as mosaic_lmhead_stats, but each of
+ * the GPU's two L2 dies takes the units of its own share of the masked-row
+ * blocks, so a block's rows stay in one die's L2. die_of_sm: device uint8
+ * [num SMs] from mosaic_die_map (0/1); sched_scratch: 16 caller-owned device
+ * bytes (zeroed by the call; one launch at a time per scratch). Exact for any
+ * map (only locality depends on it).                                         */
+MOSAIC_API int mosaic_lmhead_stats_die(const uint16_t* Hc, int64_t m_cap, const int32_t* m_dev, int64_t m_host,
+                            const uint16_t* W, int64_t V_shard, int64_t d, int64_t v_offset,
+                            int32_t n_splits, float* part_max, float* part_sum, int32_t* part_arg,
+                            const uint8_t* die_of_sm, uint32_t* sched_scratch, void* stream);
+
+/* SM -> L2-die map, measured (two cold-read latency classes; see
+ * csrc/topology.cu). die_of_sm_host receives 0/1 per SM (255 = unknown);
+ * scratch holds mosaic_die_map_scratch_bytes(n_sm) device bytes. Synchronises
+ * `stream`. *ambiguous_out counts SMs without a clear class.                 */
+MOSAIC_API size_t mosaic_die_map_scratch_bytes(int32_t n_sm);
+MOSAIC_API int mosaic_die_map(uint8_t* die_of_sm_host, int32_t n_sm, void* scratch, int32_t* n_die0_out,
+                   int32_t* ambiguous_out, void* stream);
+
 /* Gather mode of K3 -- the paper's gather-GEMM with no intermediate buffer:
  * the A rows are read straight from the hidden states H [n_rows, d] (row
  * stride ld_h elements) at the masked positions idx[0..M) (src(p) = p, or

@@ -37,6 +37,13 @@ SIGNATURES: dict[str, tuple[object, list[object]]] = {
         [c_void_p, c_int64, c_void_p, c_int64, c_void_p, c_int64, c_int64, c_int64, c_int32,
          c_void_p, c_void_p, c_void_p, c_void_p],
     ),
+    "mosaic_lmhead_stats_die": (
+        c_int,
+        [c_void_p, c_int64, c_void_p, c_int64, c_void_p, c_int64, c_int64, c_int64, c_int32,
+         c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p],
+    ),
+    "mosaic_die_map_scratch_bytes": (c_size_t, [c_int32]),
+    "mosaic_die_map": (c_int, [c_void_p, c_int32, c_void_p, POINTER(c_int32), POINTER(c_int32), c_void_p]),
     "mosaic_lmhead_stats_gather": (
         c_int,
         [c_void_p, c_int64, c_int64, c_void_p, c_int32, c_int64, c_void_p, c_int64, c_void_p, c_int64, c_int64,

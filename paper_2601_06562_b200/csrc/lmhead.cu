@@ -56,7 +56,7 @@ struct Cfg {
 #define MOSAIC_K3_STAGES2 6
 #endif
   static constexpr int STAGES = CG == 1 ? 4 : MOSAIC_K3_STAGES2;
-  static constexpr int SMEM = STAGES * STAGE_BYTES + 1024 + 256 + BM * 4;  // + gather row indices
+  static constexpr int SMEM = STAGES * STAGE_BYTES + 1024 + 256 + BM * 4 + 16;  // + gather rows, die schedule
   static constexpr uint32_t IDESC = umma_idesc_bf16(ROWS, BN);
 };
 
@@ -71,6 +71,8 @@ struct Params {
   int32_t n_splits;
   int32_t group_m;
   int32_t seg_splits;  // vocab segments of this many splits, processed segment-major (0 = one segment)
+  const uint8_t* die_of_sm;  // die-aware schedule: SM -> L2 die (null = off)
+  uint32_t* sched;           // die-aware schedule: [die0 pairs, die1 pairs, arrived], zeroed per launch
   int32_t epilogue;  // 0 = skip the statistics math (power/overlap experiments only)
   int32_t policy;   // L2 policy of (A, B) loads: 0 = (evict_normal, evict_normal), 1 = (evict_last, evict_normal), 2 = (evict_normal, evict_first)
   int64_t v_offset;
@@ -183,7 +185,6 @@ __global__ void __launch_bounds__(kGather == kGatherCpAsync ? kThreadsCpAsync : 
   const int64_t n_clusters = gridDim.x / CG;
   const int64_t M = min(static_cast<int64_t>(load_count(p.m_dev, p.m_host)), p.m_cap);
   const int m_blocks = static_cast<int>((M + C::ROWS - 1) / C::ROWS);
-  const int64_t units = static_cast<int64_t>(m_blocks) * p.n_splits;
   const int k_blocks = p.K / BK;
 
   if (warp == 0 && lane == 0) {
@@ -206,6 +207,48 @@ __global__ void __launch_bounds__(kGather == kGatherCpAsync ? kThreadsCpAsync : 
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
 
+  // Die-aware schedule: each die's pairs take the units of their own share of
+  // the m-blocks, so an m-group's gathered rows (re-read once per vocab tile)
+  // live in one die's L2 instead of being replicated in both. The pair leader
+  // registers its die (slot = arrival order on that die), all pairs meet at a
+  // grid barrier (persistent grid: every CTA is resident; bounded spin), then
+  // split the m-blocks in proportion to the pairs each die actually got -- so
+  // the result is exact for any SM placement or die map; only locality varies.
+  int64_t u_first = cluster, u_stride = n_clusters;
+  int mb_lo = 0, mb_cnt = m_blocks;
+  if (p.die_of_sm != nullptr) {
+    int32_t* info = reinterpret_cast<int32_t*>(smem + C::STAGES * C::STAGE_BYTES + 256 + BM * 4);
+    if (threadIdx.x == 0 && rank == 0) {
+      uint32_t smid;
+      asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+      const int d = p.die_of_sm[smid] == 1 ? 1 : 0;
+      const uint32_t slot = atomicAdd(p.sched + d, 1u);
+      __threadfence();
+      atomicAdd(p.sched + 2, 1u);
+      uint32_t spins = 0;
+      while (*reinterpret_cast<volatile uint32_t*>(p.sched + 2) < static_cast<uint32_t>(n_clusters))
+        if (++spins == (1u << 26)) __trap();  // a pair never became resident: fail, do not hang
+      __threadfence();
+      const int64_t n0 = *reinterpret_cast<volatile uint32_t*>(p.sched + 0);
+      const int64_t n1 = *reinterpret_cast<volatile uint32_t*>(p.sched + 1);
+      const int mb0 = static_cast<int>((m_blocks * n0 + (n0 + n1) / 2) / (n0 + n1));
+      const int32_t v[4] = {static_cast<int32_t>(slot), static_cast<int32_t>(d ? n1 : n0), d ? mb0 : 0,
+                            d ? m_blocks - mb0 : mb0};
+      for (int i = 0; i < 4; ++i) {
+        info[i] = v[i];
+        if constexpr (CG == 2)
+          asm volatile("st.shared::cluster.s32 [%0], %1;" ::"r"(mapa_shared(smem_u32(info + i), 1)), "r"(v[i])
+                       : "memory");
+      }
+    }
+    if constexpr (CG == 2) cluster_sync(); else __syncthreads();
+    u_first = info[0];
+    u_stride = info[1];
+    mb_lo = info[2];
+    mb_cnt = info[3];
+  }
+  const int64_t units_here = static_cast<int64_t>(mb_cnt) * p.n_splits;
+
   if (warp == 0 || (kGather == kGatherCpAsync && warp >= 6)) {
     // ------------------------------------------------------------ TMA producer (both CTAs)
     // A is re-read for every tile of a unit and by the units of its m-group;
@@ -213,9 +256,10 @@ __global__ void __launch_bounds__(kGather == kGatherCpAsync ? kThreadsCpAsync : 
     const uint64_t pol_a = p.policy == 1 ? policy_evict_last() : policy_evict_normal();
     const uint64_t pol_b = p.policy == 2 ? policy_evict_first() : policy_evict_normal();
     uint32_t stage = 0, phase = 0;
-    for (int64_t u = cluster; u < units; u += n_clusters) {
+    for (int64_t u = u_first; u < units_here; u += u_stride) {
       int mb, s;
-      unit_coords(p, m_blocks, u, mb, s);
+      unit_coords(p, mb_cnt, u, mb, s);
+      mb += mb_lo;
       const int t0 = s * p.tiles_per_split;
       const int t1 = min(t0 + p.tiles_per_split, p.n_tiles);
       const int a_row = mb * C::ROWS + rank * BM;
@@ -309,9 +353,10 @@ __global__ void __launch_bounds__(kGather == kGatherCpAsync ? kThreadsCpAsync : 
     // ------------------------------------------------------------ MMA issuer (pair leader)
     if (lane == 0 && rank == 0) {
       uint32_t stage = 0, phase = 0, acc = 0, acc_phase = 0;
-      for (int64_t u = cluster; u < units; u += n_clusters) {
+      for (int64_t u = u_first; u < units_here; u += u_stride) {
         int mb, s;
-        unit_coords(p, m_blocks, u, mb, s);
+        unit_coords(p, mb_cnt, u, mb, s);
+      mb += mb_lo;
         const int t0 = s * p.tiles_per_split;
         const int t1 = min(t0 + p.tiles_per_split, p.n_tiles);
         for (int t = t0; t < t1; ++t) {
@@ -352,9 +397,10 @@ __global__ void __launch_bounds__(kGather == kGatherCpAsync ? kThreadsCpAsync : 
       // peer CTA of the pair: relay "A slot landed" to the leader's barrier
       if (lane == 0 && rank == 1) {
         uint32_t stage = 0, phase = 0;
-        for (int64_t u = cluster; u < units; u += n_clusters) {
+        for (int64_t u = u_first; u < units_here; u += u_stride) {
           int mb, s;
-          unit_coords(p, m_blocks, u, mb, s);
+          unit_coords(p, mb_cnt, u, mb, s);
+      mb += mb_lo;
           const int t0 = s * p.tiles_per_split;
           const int t1 = min(t0 + p.tiles_per_split, p.n_tiles);
           for (int t = t0; t < t1; ++t)
@@ -377,9 +423,10 @@ __global__ void __launch_bounds__(kGather == kGatherCpAsync ? kThreadsCpAsync : 
     // tempty lives in the pair leader: arrive locally or through the cluster window
     const uint32_t tempty_addr0 = CG == 2 ? mapa_shared(smem_u32(&tempty[0]), 0) : smem_u32(&tempty[0]);
     uint32_t acc = 0, acc_phase = 0;
-    for (int64_t u = cluster; u < units; u += n_clusters) {
+    for (int64_t u = u_first; u < units_here; u += u_stride) {
       int mb, s;
-      unit_coords(p, m_blocks, u, mb, s);
+      unit_coords(p, mb_cnt, u, mb, s);
+      mb += mb_lo;
       const int t0 = s * p.tiles_per_split;
       const int t1 = min(t0 + p.tiles_per_split, p.n_tiles);
       const int64_t row = static_cast<int64_t>(mb) * C::ROWS + rank * BM + row_local;
@@ -604,6 +651,10 @@ int launch(const ASource& a, int64_t m_cap, const int32_t* m_dev, int64_t m_host
   static const int epilogue = env_int("MOSAIC_K3_EPILOGUE", 1);
   p.epilogue = epilogue;
   cudaStream_t s = as_stream(stream);
+  if (p.die_of_sm != nullptr) {
+    MOSAIC_REQUIRE(p.sched != nullptr, "die-aware schedule needs its 16-byte scratch");
+    MOSAIC_CUDA(cudaMemsetAsync(p.sched, 0, 16, s));
+  }
   if (gather) {
     p.h = a.base;
     p.ld_h = a.ld;
@@ -655,6 +706,28 @@ extern "C" int mosaic_lmhead_stats(const uint16_t* Hc, int64_t m_cap, const int3
   p.part_max = part_max;
   p.part_sum = part_sum;
   p.part_arg = part_arg;
+  return launch<false>(ASource{Hc, m_cap, d, nullptr, 0}, m_cap, m_dev, m_host, W, V_shard, d, p, stream);
+}
+
+extern "C" int mosaic_lmhead_stats_die(const uint16_t* Hc, int64_t m_cap, const int32_t* m_dev, int64_t m_host,
+                                       const uint16_t* W, int64_t V_shard, int64_t d, int64_t v_offset,
+                                       int32_t n_splits, float* part_max, float* part_sum, int32_t* part_arg,
+                                       const uint8_t* die_of_sm, uint32_t* sched_scratch, void* stream) {
+  MOSAIC_REQUIRE(part_max && part_sum && part_arg, "null partial buffers");
+  const int64_t n_tiles = ceil_div(V_shard, BN);
+  MOSAIC_REQUIRE(n_splits >= 1 && n_splits <= n_tiles, "n_splits=%d not in [1, %lld]", n_splits,
+                 (long long)n_tiles);
+  Params p{};
+  p.tiles_per_split = static_cast<int32_t>(ceil_div(n_tiles, n_splits));
+  p.n_splits = static_cast<int32_t>(ceil_div(n_tiles, p.tiles_per_split));
+  MOSAIC_REQUIRE(p.n_splits == n_splits, "n_splits=%d does not tile %lld vocab tiles evenly; use mosaic_lmhead_plan",
+                 n_splits, (long long)n_tiles);
+  p.v_offset = v_offset;
+  p.part_max = part_max;
+  p.part_sum = part_sum;
+  p.part_arg = part_arg;
+  p.die_of_sm = die_of_sm;
+  p.sched = sched_scratch;
   return launch<false>(ASource{Hc, m_cap, d, nullptr, 0}, m_cap, m_dev, m_host, W, V_shard, d, p, stream);
 }
 

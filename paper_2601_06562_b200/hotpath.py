@@ -93,9 +93,29 @@ def lmhead_plan(m_cap: int, v_shard: int, d: int) -> tuple[int, int]:
     return s.value, t.value
 
 
+_DIE_MAPS: dict = {}
+
+
+def die_map(device=None) -> tuple[torch.Tensor, dict]:
+    """The measured SM -> L2-die map of ``device`` (cached per process): a
+    device uint8 tensor [num SMs] for K3's die-aware schedule, plus counts."""
+    dev = torch.device("cuda", torch.cuda.current_device() if device is None else torch.device(device).index or 0)
+    if dev.index not in _DIE_MAPS:
+        n_sm = torch.cuda.get_device_properties(dev).multi_processor_count
+        scratch = torch.empty(int(_native.value("mosaic_die_map_scratch_bytes", n_sm)), dtype=torch.uint8, device=dev)
+        host = (ctypes.c_uint8 * n_sm)()
+        n0, amb = ctypes.c_int32(), ctypes.c_int32()
+        with torch.cuda.device(dev):
+            _native.call("mosaic_die_map", host, n_sm, _p(scratch), ctypes.byref(n0), ctypes.byref(amb), _s(None))
+        table = torch.tensor(list(host), dtype=torch.uint8, device=dev)
+        _DIE_MAPS[dev.index] = (table, {"n_sm": n_sm, "die0_sms": n0.value, "ambiguous": amb.value})
+    return _DIE_MAPS[dev.index]
+
+
 def lmhead_stats(hc: torch.Tensor, weight: torch.Tensor, n_splits: int, part_max: torch.Tensor,
                  part_sum: torch.Tensor, part_arg: torch.Tensor, m_dev=None, m_host: int = 0,
-                 v_offset: int = 0, stream=None) -> None:
+                 v_offset: int = 0, stream=None, die_of_sm: Optional[torch.Tensor] = None,
+                 sched: Optional[torch.Tensor] = None) -> None:
     _req(hc, torch.bfloat16, "hc", 2)
     _req(weight, torch.bfloat16, "weight", 2)
     m_cap, d = hc.shape
@@ -106,6 +126,13 @@ def lmhead_stats(hc: torch.Tensor, weight: torch.Tensor, n_splits: int, part_max
         _req(t, dt, n)
         if t.numel() < n_splits * m_cap:
             raise InputError(f"{n} must hold n_splits*m_cap entries")
+    if die_of_sm is not None:  # die-aware unit schedule (see csrc/lmhead.cu)
+        if sched is None or sched.numel() * sched.element_size() < 16:
+            raise InputError("the die-aware schedule needs a 16-byte sched scratch")
+        _native.call("mosaic_lmhead_stats_die", _p(hc), m_cap, _p(m_dev), int(m_host), _p(weight),
+                     weight.shape[0], d, int(v_offset), int(n_splits), _p(part_max), _p(part_sum),
+                     _p(part_arg), _p(die_of_sm), _p(sched), _s(stream))
+        return
     _native.call("mosaic_lmhead_stats", _p(hc), m_cap, _p(m_dev), int(m_host), _p(weight),
                  weight.shape[0], d, int(v_offset), int(n_splits), _p(part_max), _p(part_sum),
                  _p(part_arg), _s(stream))
@@ -307,7 +334,7 @@ class MaskOnlyHead:
     def __init__(self, weight_shard: torch.Tensor, *, seq_len: int, mask_id: int,
                  vocab_offset: int = 0, m_cap: Optional[int] = None, shift: bool = False,
                  group=None, block: Optional[torch.Tensor] = None, fused_gather: bool = False,
-                 exchange="nccl"):
+                 exchange="nccl", die_aware: Optional[bool] = None):
         _req(weight_shard, torch.bfloat16, "weight_shard", 2)
         self.weight = weight_shard
         self.v_shard, self.d = weight_shard.shape
@@ -318,6 +345,11 @@ class MaskOnlyHead:
         self.shift = bool(shift)
         self.group = group
         self.fused_gather = bool(fused_gather)  # K3 reads rows of `hidden` directly: no K2, no hc buffer
+        if die_aware is None:
+            import os
+
+            die_aware = os.environ.get("MOSAIC_DIE_AWARE", "0") == "1"
+        self.die_table = die_map(weight_shard.device)[0] if die_aware and not self.fused_gather else None
         if not (exchange in ("nccl", "p2p") or hasattr(exchange, "push")):
             raise InputError(f"exchange must be 'nccl', 'p2p' or a P2PExchange, got {exchange!r}")
         self.exchange = exchange
@@ -344,6 +376,7 @@ class MaskOnlyHead:
         lay.add("conf", (m,), torch.float32)
         lay.add("selected", (m,), torch.int32)
         lay.add("remask_scratch", (remask_scratch_bytes(),), torch.uint8)
+        lay.add("sched", (4,), torch.int32)
         self.layout = lay
         self.p2p = None
         if hasattr(exchange, "push"):  # a prepared P2PExchange (peer buffers set up by the caller)
@@ -376,7 +409,8 @@ class MaskOnlyHead:
         else:
             gather_rows(hidden, b["idx"], b["hc"], m_dev=m_dev, shift=self.shift, stream=stream)
             lmhead_stats(b["hc"], self.weight, self.n_splits, b["part_max"], b["part_sum"],
-                         b["part_arg"], m_dev=m_dev, v_offset=self.vocab_offset, stream=stream)
+                         b["part_arg"], m_dev=m_dev, v_offset=self.vocab_offset, stream=stream,
+                         die_of_sm=self.die_table, sched=b["sched"])
         m, S = self.m_cap, self.n_splits
         if self.group is None and self.p2p is None:
             stats_merge(b["part_max"], b["part_sum"], b["part_arg"], S, m, m, m_dev=m_dev,

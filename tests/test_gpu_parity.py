@@ -472,3 +472,32 @@ def test_full_size_step_properties(dev, name, L, d, V, shift, k):
     assert orc.isclose_rel(lse[rows], ref["lse"], LSE_REL)
     assert orc.isclose_rel(conf[rows], ref["conf"], CONF_REL)
     assert np.all(lse[rows] >= ref["max"] - 1e-3)
+
+
+def test_die_map_and_die_aware_k3(dev):
+    """The measured SM -> die map splits the SMs into two halves (TPC pairs
+    together), and K3 under the die-aware schedule is bit-identical to the
+    default schedule -- also with a deliberately wrong map (exactness does not
+    depend on the map)."""
+    from paper_2601_06562_b200 import hotpath
+
+    table, info = hotpath.die_map(dev)
+    t = table.cpu().numpy()
+    assert set(np.unique(t)) <= {0, 1} and info["ambiguous"] <= 16
+    assert abs(int((t == 0).sum()) - int((t == 1).sum())) <= 24
+    rng = np.random.default_rng(3)
+    for m, d, V in ((5000, 1024, 40000), (16384, 4096, 126464 // 4), (100, 256, 3000)):
+        Hc = bf16_tensor(rng.standard_normal((m, d)), dev)
+        W = bf16_tensor(rng.standard_normal((V, d)) * 0.03, dev)
+        S, _ = hotpath.lmhead_plan(m, V, d)
+        outs = []
+        for tab in (None, table, torch.zeros_like(table), torch.from_numpy(rng.integers(0, 2, t.size).astype(np.uint8)).to(dev)):
+            pm, ps = torch.empty(S, m, device=dev), torch.empty(S, m, device=dev)
+            pa = torch.empty(S, m, dtype=torch.int32, device=dev)
+            sched = torch.empty(4, dtype=torch.int32, device=dev)
+            hotpath.lmhead_stats(Hc, W, S, pm, ps, pa, m_host=m, v_offset=3, die_of_sm=tab, sched=sched)
+            torch.cuda.synchronize()
+            outs.append((pm.cpu(), ps.cpu(), pa.cpu()))
+        for o in outs[1:]:
+            for a, b in zip(outs[0], o):
+                assert torch.equal(a, b)
