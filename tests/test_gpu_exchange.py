@@ -79,6 +79,8 @@ def _rank_main(rank, world, bufs, q):
         torch.cuda.synchronize()
         M = int(o.m_dev.item())
         q.put((rank, xd.cpu().numpy(), o.token[:M].cpu().numpy(), o.conf[:M].cpu().numpy()))
+        del ex, head, gathered, signal, bufs  # release the IPC mappings before the producer goes away
+        torch.cuda.synchronize()
     except Exception as exc:  # report instead of hanging the parent
         q.put((rank, "error", repr(exc), None))
 
