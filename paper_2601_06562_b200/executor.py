@@ -88,7 +88,9 @@ class RandomDLLM:
             self.layers.append(lw)
         v0, v1 = vocab_shard or (0, V)
         self.vocab_offset = v0
-        self.w_vocab = w(v1 - v0, d)  # [V_shard, d]
+        w_vocab = w(V, d)  # the full head from the same stream, so a shard is a slice of the unsharded model
+        self.w_vocab = w_vocab if (v0, v1) == (0, V) else w_vocab[v0:v1].contiguous()  # [V_shard, d]
+        del w_vocab
 
     def layer(self, i: int) -> dict:
         return self.layers[i % len(self.layers)]
@@ -111,7 +113,8 @@ def _rows(n_total: int, trips: int, it: Optional[int]) -> tuple[int, int]:
 class StepExecutor:
     """Executes step graphs of one model inside one :class:`Workspace` (cuda)."""
 
-    def __init__(self, model: RandomDLLM, workspace: Workspace, mask_id: int, exec_layers: Optional[int] = None):
+    def __init__(self, model: RandomDLLM, workspace: Workspace, mask_id: int, exec_layers: Optional[int] = None,
+                 group=None):
         if workspace.backend != "cuda":
             raise InputError("the executor needs a cuda workspace")
         self.model = model
@@ -120,6 +123,14 @@ class StepExecutor:
         self.mask_id = int(mask_id)
         self.shift = self.cfg.shift_mode != "none"
         self.exec_layers = exec_layers  # execute only the first n layers (context sweep)
+        # vocab-sharded LM head (model built with vocab_shard): the sample op merges
+        # this rank's splits, all-gathers the per-row triples and merges in rank order
+        self.group = group
+        self.world = 1
+        if group is not None:
+            import torch.distributed as dist
+
+            self.world = dist.get_world_size(group)
         dev = torch.device("cuda", workspace.device)
         self.device = dev
         self._side: dict[int, dict] = {}
@@ -417,7 +428,18 @@ class StepExecutor:
             pm, ps = flat[: S * cap], flat[S * cap: 2 * S * cap]
             pa = flat[2 * S * cap: 3 * S * cap].view(torch.int32)
             tok, conf = v[op.inputs[1]], v[op.inputs[2]]
-            hotpath.stats_merge(pm, ps, pa, S, cap, cap, m_host=r1 - r0, token=tok[r0:r1], conf=conf[r0:r1])
+            if self.group is None:
+                hotpath.stats_merge(pm, ps, pa, S, cap, cap, m_host=r1 - r0, token=tok[r0:r1], conf=conf[r0:r1])
+                return
+            from .shard import exchange_triples
+
+            n = r1 - r0
+            loc = torch.empty((3, n), dtype=torch.float32, device=self.device)
+            hotpath.stats_merge(pm, ps, pa, S, cap, n, m_host=n, out_max=loc[0], out_sum=loc[1],
+                                out_arg=loc[2].view(torch.int32))
+            gat = exchange_triples(loc, group=self.group)  # [P, 3, n], rank-major
+            hotpath.stats_merge(gat[0, 0], gat[0, 1], gat[0, 2].view(torch.int32), self.world, 3 * n, n, m_host=n,
+                                token=tok[r0:r1], conf=conf[r0:r1])
             return
         # reference modes: fp32 softmax statistics of materialised bf16 logits
         if len(op.outputs) == 2:  # concat: sample over logits_all after the loop

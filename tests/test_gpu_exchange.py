@@ -119,3 +119,73 @@ def test_p2p_exchange_two_ranks_one_gpu(native_lib):
         assert np.array_equal(xo, xd.cpu().numpy())       # identical commits on every rank
         assert np.array_equal(tok, o.token[:M].cpu().numpy())
         assert np.allclose(conf, o.conf[:M].cpu().numpy(), rtol=1e-5)  # rank-order merge vs split merge
+
+
+def _exec_rank(rank, world, port, q):
+    import sys
+
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    import torch.distributed as dist
+
+    from paper_2601_06562_b200 import shard, vmm, workload
+    from paper_2601_06562_b200.executor import RandomDLLM, StepExecutor
+
+    os.environ["MASTER_ADDR"], os.environ["MASTER_PORT"] = "127.0.0.1", str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        dev = torch.device("cuda", 0)
+        cfg = workload.toy_configs()["tiny_llada"]
+        model = RandomDLLM(cfg, dev, seed=3, vocab_shard=shard.vocab_shard_bounds(cfg.vocab_size, world, rank))
+        ws = vmm.reserve(2 << 30, backend="cuda")
+        ex = StepExecutor(model, ws, 8191, group=dist.group.WORLD)
+        x = _exec_x(dev)
+        g = workload.build_layer_template(cfg).instantiate({"L": 2048, "M": 1024, "K_logits": 2, "K_FFN": 2})
+        ex.run(g, x, 64)
+        torch.cuda.synchronize()
+        q.put((rank, x.cpu().numpy()))
+        ws.close()
+    except Exception as exc:
+        q.put((rank, repr(exc)))
+    finally:
+        dist.destroy_process_group()
+
+
+def _exec_x(dev):
+    rng = np.random.default_rng(12)
+    x = rng.integers(0, 8191, size=2048).astype(np.int32)
+    x[1024:] = 8191
+    return torch.from_numpy(x).to(dev)
+
+
+def test_vocab_sharded_executor_two_ranks(native_lib):
+    """The step executor with a vocab-sharded LM head on two ranks (gloo
+    all-gather of the triples, both processes on this GPU): every rank commits
+    what the unsharded executor commits."""
+    import torch.multiprocessing as mp
+
+    from paper_2601_06562_b200 import vmm, workload
+    from paper_2601_06562_b200.executor import RandomDLLM, StepExecutor
+
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _port()
+    procs = [ctx.Process(target=_exec_rank, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = dict(q.get(timeout=300) for _ in procs)
+    for p in procs:
+        p.join(timeout=120)
+    assert all(not isinstance(v, str) for v in res.values()), res
+    dev = torch.device("cuda", 0)
+    cfg = workload.toy_configs()["tiny_llada"]
+    model = RandomDLLM(cfg, dev, seed=3)
+    ws = vmm.reserve(2 << 30, backend="cuda")
+    try:
+        x = _exec_x(dev)
+        g = workload.build_layer_template(cfg).instantiate({"L": 2048, "M": 1024, "K_logits": 2, "K_FFN": 2})
+        StepExecutor(model, ws, 8191).run(g, x, 64)
+        want = x.cpu().numpy()
+    finally:
+        ws.close()
+    for r in (0, 1):
+        assert np.array_equal(res[r], want)
