@@ -73,7 +73,6 @@ struct Params {
   int32_t seg_splits;  // vocab segments of this many splits, processed segment-major (0 = one segment)
   const uint8_t* die_of_sm;  // die-aware schedule: SM -> L2 die (null = off)
   uint32_t* sched;           // die-aware schedule: [die0 pairs, die1 pairs, arrived], zeroed per launch
-  int32_t epilogue;  // 0 = skip the statistics math (power/overlap experiments only)
   int32_t policy;   // L2 policy of (A, B) loads: 0 = (evict_normal, evict_normal), 1 = (evict_last, evict_normal), 2 = (evict_normal, evict_first)
   int64_t v_offset;
   float* part_max;
@@ -440,7 +439,7 @@ __global__ void __launch_bounds__(kGather == kGatherCpAsync ? kThreadsCpAsync : 
 #pragma unroll 1
         for (int c = 0; c < BN / 32; ++c) {
           const int64_t col0 = col_base + c * 32;
-          if (col0 >= p.V || !p.epilogue) break;  // warp-uniform: vocab tail
+          if (col0 >= p.V) break;  // warp-uniform: vocab tail
           float v[32];
           tmem_ld32(taddr + c * 32, v);
           if constexpr (kStoreLogits) {
@@ -648,8 +647,6 @@ int launch(const ASource& a, int64_t m_cap, const int32_t* m_dev, int64_t m_host
   p.seg_splits = seg_splits;
   static const int policy = env_int("MOSAIC_L2_POLICY", 1);  // measured best: A evict_last
   p.policy = policy;
-  static const int epilogue = env_int("MOSAIC_K3_EPILOGUE", 1);
-  p.epilogue = epilogue;
   cudaStream_t s = as_stream(stream);
   if (p.die_of_sm != nullptr) {
     MOSAIC_REQUIRE(p.sched != nullptr, "die-aware schedule needs its 16-byte scratch");
