@@ -1,23 +1,26 @@
 // K3: mask-only LM head as a persistent, warp-specialised tcgen05 GEMM whose
-// epilogue folds each 128x256 FP32 accumulator tile into per-row online
-// softmax statistics (max, sum-exp, argmax) and never writes the logits.
+// epilogue folds every FP32 accumulator tile into per-row online softmax
+// statistics (max, sum-exp, argmax) and never writes the logits.
 //
 // Reference counterpart: gather_gemm (mosaic/kernel.py:62-86) computes
 // logits[i, :] = H[mask_idx[i], :] @ W and materialises [m, V] (:68); the
 // `sample` op that consumes them is memory-only (mosaic/workload.py:306-308).
-// Here the gathered rows Hc (K2) and the vocab shard W [V, d] (K-major) stream
-// through TMA into a 4-stage shared-memory ring, one elected thread issues
-// tcgen05.mma (M=128, N=256, K=16, BF16 -> FP32 in TMEM), and four epilogue
-// warps drain a double-buffered TMEM accumulator with tcgen05.ld while the next
-// tile's MMAs run.
+// Here the gathered rows Hc (K2) -- or, in gather mode, the rows of H itself --
+// and the vocab shard W [V, d] (K-major) stream through TMA into a shared-memory
+// ring; one elected thread issues tcgen05.mma (BF16 -> FP32 in TMEM) and four
+// epilogue warps drain a double-buffered TMEM accumulator with tcgen05.ld while
+// the next tile's MMAs run. Default cta_group::2: a CTA pair computes 256 x 256
+// tiles (UMMA M=256, N=256, K=16) out of a 6-stage ring; cta_group::1 (128 x 256,
+// 4 stages) serves M <= 128.
 //
 // Work decomposition: the vocab tiles (256 columns) are cut into n_splits
-// contiguous splits; a work unit is (m-block of 128 rows, split). Each CTA loops
-// over units u = blockIdx.x, blockIdx.x + gridDim.x, ... and keeps the per-row
-// statistics of the current unit in registers across the split's tiles, so the
-// only global output is one (max, sum, arg) triple per row and split. Units are
-// numbered m-fastest inside groups of `group_m` m-blocks, so the ~148 units in
-// flight at once share a handful of W tiles and m-blocks through L2.
+// contiguous splits; a work unit is (row block, split). Each pair loops over
+// units u = cluster, cluster + n_clusters, ... (or its die's share, see the
+// die-aware schedule) and keeps the per-row statistics of the current unit in
+// registers across the split's tiles, so the only global output is one
+// (max, sum, arg) triple per row and split. Units are numbered m-fastest inside
+// groups of `group_m` row blocks, so the ~74 units in flight share a handful of
+// W tiles and row blocks through L2.
 #include <algorithm>
 #include <cstdlib>
 
