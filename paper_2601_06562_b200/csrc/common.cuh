@@ -89,6 +89,19 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   }
 }
 
+// Same as mbar_wait, but sleeping `ns` nanoseconds between polls: for waits
+// with plenty of slack (an epilogue warp waiting for the next accumulator, a
+// producer waiting for a free ring slot) a tight poll loop only burns issue
+// slots -- and, on a power-capped part, clock.
+__device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity, uint32_t ns) {
+  const uint32_t addr = smem_u32(bar);
+  uint32_t spins = 0;
+  while (!mbar_try_wait(addr, parity)) {
+    if (ns) __nanosleep(ns);
+    if (++spins == (1u << 28)) __trap();
+  }
+}
+
 // --- TMA -------------------------------------------------------------------
 __device__ __forceinline__ void tma_prefetch_desc(const void* tmap) {
   asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(tmap)) : "memory");

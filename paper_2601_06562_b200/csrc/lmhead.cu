@@ -42,6 +42,12 @@ static_assert(kRowsPerAWarp % 4 == 0 && kRowsPerAWarp <= 32, "loader warp covers
 constexpr int kThreadsCpAsync = kThreads + (kAWarps - 1) * 32;
 constexpr int kEpiWarps = 4;
 constexpr int kMaxSplits = 64;
+#ifndef MOSAIC_K3_EPI_SLEEP_NS
+#define MOSAIC_K3_EPI_SLEEP_NS 0   // epilogue poll backoff while the next accumulator fills
+#endif
+#ifndef MOSAIC_K3_PROD_SLEEP_NS
+#define MOSAIC_K3_PROD_SLEEP_NS 0  // producer poll backoff while the ring is full
+#endif
 constexpr float kLog2e = 1.4426950408889634f;
 
 // Per cta_group configuration. CG = 2 pairs two SMs on one 256 x 256 tile
@@ -294,7 +300,7 @@ __global__ void __launch_bounds__(kGather == kGatherCpAsync ? kThreadsCpAsync : 
         for (int t = t0; t < t1; ++t) {
           const int b_row = t * BN + rank * C::B_ROWS;
           for (int kb = 0; kb < k_blocks; ++kb) {
-            mbar_wait(&empty[stage], phase ^ 1);
+            mbar_wait_sleep(&empty[stage], phase ^ 1, MOSAIC_K3_PROD_SLEEP_NS);
             if (warp == 0 && lane == 0) {
               if (rank == 0) mbar_arrive_expect_tx(&full[stage], C::B_BYTES * CG);
               if constexpr (CG == 1)
@@ -320,7 +326,7 @@ __global__ void __launch_bounds__(kGather == kGatherCpAsync ? kThreadsCpAsync : 
         for (int t = t0; t < t1; ++t) {
           const int b_row = t * BN + rank * C::B_ROWS;
           for (int kb = 0; kb < k_blocks; ++kb) {
-            mbar_wait(&empty[stage], phase ^ 1);
+            mbar_wait_sleep(&empty[stage], phase ^ 1, MOSAIC_K3_PROD_SLEEP_NS);
             if (rank == 0) mbar_arrive_expect_tx(&full[stage], C::STAGE_BYTES * CG);
             if constexpr (CG == 1)
               tma_load_2d(sB + stage * C::B_BYTES, &tmap_b, &full[stage], kb * BK, b_row, pol_b);
@@ -435,7 +441,7 @@ __global__ void __launch_bounds__(kGather == kGatherCpAsync ? kThreadsCpAsync : 
       float run_max = -INFINITY, run_sum = 0.f;
       int64_t run_arg = 0;
       for (int t = t0; t < t1; ++t) {
-        mbar_wait(&tfull[acc], acc_phase);
+        mbar_wait_sleep(&tfull[acc], acc_phase, MOSAIC_K3_EPI_SLEEP_NS);
         tc_fence_after();
         const uint32_t taddr = tmem_base + (static_cast<uint32_t>(q * 32) << 16) + acc * BN;
         const int64_t col_base = static_cast<int64_t>(t) * BN;
