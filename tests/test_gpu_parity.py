@@ -501,3 +501,42 @@ def test_die_map_and_die_aware_k3(dev):
         for o in outs[1:]:
             for a, b in zip(outs[0], o):
                 assert torch.equal(a, b)
+
+
+@pytest.mark.parametrize("n_masked,k", [(0, 5), (1, 1), (1, 7), (17, 100), (4096, 0), (4096, 4096)])
+def test_step_edge_counts(dev, n_masked, k):
+    """Empty and degenerate masks through the whole fused step: nothing masked,
+    a single masked row, k larger than M (clamped to M), k = 0,
+    everything masked and fully committed."""
+    from paper_2601_06562_b200 import MaskOnlyHead
+
+    rng = np.random.default_rng(n_masked * 31 + k)
+    L, d, V = 4096, 256, 8192
+    mask_id = V - 1
+    x = rng.integers(0, V - 1, size=L).astype(np.int32)
+    pos = np.sort(rng.choice(L, n_masked, replace=False))
+    x[pos] = mask_id
+    H = orc.bf16_round(rng.standard_normal((L, d)))
+    W = orc.bf16_round(rng.standard_normal((V, d)) * 0.05)
+    head = MaskOnlyHead(bf16_tensor(W, dev), seq_len=L, mask_id=mask_id)
+    xd = torch.from_numpy(x).to(dev)
+    out = head.step(xd, bf16_tensor(H, dev), k)
+    torch.cuda.synchronize()
+    M = int(out.m_dev.item())
+    assert M == n_masked
+    xo = xd.cpu().numpy()
+    committed = min(k, M)
+    # committed positions carry their argmax token, which may itself be the mask
+    # id under random weights (the sampler takes the plain argmax, as LLaDA's)
+    tok = out.token[:M].cpu().numpy()
+    sel = out.selected[:M].cpu().numpy().astype(bool) if M else np.zeros(0, bool)
+    assert sel.sum() == committed
+    assert np.array_equal(xo[pos[sel]], tok[sel]) and np.all(xo[pos[~sel]] == mask_id)
+    assert np.array_equal(xo[np.setdiff1d(np.arange(L), pos)], x[np.setdiff1d(np.arange(L), pos)])
+    if M:
+        ref = orc.step(x, H, W, mask_id, committed)
+        sel = out.selected[:M].cpu().numpy().astype(bool)
+        assert sel.sum() == committed
+        assert np.array_equal(sel, orc.remask_select(out.conf[:M].cpu().numpy(), ref["idx"], committed))
+        ok = ref["margin"] > MARGIN
+        assert np.array_equal(out.token[:M].cpu().numpy()[ok], ref["arg"][ok])
