@@ -327,7 +327,11 @@ def gpu_main(args):
                        "previous step's compute); updated x read back every step"}
 
     peaks = json.loads((ROOT / "MEASURED_PEAKS.json").read_text()) if (ROOT / "MEASURED_PEAKS.json").exists() else {}
-    peak = peaks.get("bf16_tflops", 1590.0)
+    # K3 runs back to back for the whole timed region (steps x ~12 ms) under the
+    # 1000 W cap, i.e. "a kernel timed inside a long step": the denominator is the
+    # measured sustained cuBLAS figure; the burst fraction is reported beside it.
+    burst = peaks.get("bf16_tflops", 1590.0)
+    peak = peaks.get("bf16_tflops_sustained", burst)
     flops = 2.0 * D * (v1 - v0) * M
     achieved = flops / (k3_ms / 1e3) / 1e12
     traffic = None
@@ -355,8 +359,9 @@ def gpu_main(args):
                    "l2": "inputs larger than L2 (W 1.04 GB, H 268 MB > 126 MB)"},
         "roofline": {"bound": "tensor", "kernel": "k3_lmhead (tcgen05 stats GEMM)",
                      "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
-                     "peak_source": "MEASURED_PEAKS.json bf16_tflops (burst)" if peaks else "fallback 1590",
-                     "frac_of_sustained": achieved / peaks.get("bf16_tflops_sustained", 1416.3),
+                     "peak_source": ("MEASURED_PEAKS.json bf16_tflops_sustained (K3 timed inside a long, power-capped "
+                                     "step loop)") if "bf16_tflops_sustained" in peaks else "fallback 1590 (burst)",
+                     "peak_burst": burst, "frac_of_burst": achieved / burst,
                      "k3_ms": k3_ms, "k3_share_of_step": k3_ms / ms_per_step,
                      "flops_per_launch": flops, "traffic": traffic},
         "gpu_launches": launches_per_step * args.steps,
