@@ -168,7 +168,11 @@ __global__ void __launch_bounds__(kFusedThreads) k5_fused(const float* __restric
   for (int pass = 0; pass < 8; ++pass) {
     if (t < 256) h[t] = 0u;
     __syncthreads();
-    if (s_krem == 0u) break;  // only when k == 0 (uniform)
+    // every thread snapshots the pass state here; the single qualifying thread
+    // below is the only writer, and nobody re-reads s_krem / s_prefix before
+    // the closing barrier (racecheck/synccheck clean)
+    const uint32_t k_rem = s_krem;
+    if (k_rem == 0u) break;  // only when k == 0 (uniform)
     const unsigned long long prefix = s_prefix;
     const int hi_shift = 64 - 8 * pass;
     const int lo_shift = 56 - 8 * pass;
@@ -190,7 +194,7 @@ __global__ void __launch_bounds__(kFusedThreads) k5_fused(const float* __restric
       __syncthreads();
     }
     if (t < 256) {
-      const uint32_t k_rem = s_krem, incl = cum[t], above = incl - cnt;
+      const uint32_t incl = cum[t], above = incl - cnt;
       if (above < k_rem && incl >= k_rem) {  // exactly one digit qualifies
         s_prefix = prefix | (static_cast<unsigned long long>(255 - t) << lo_shift);
         s_krem = k_rem - above;
