@@ -68,3 +68,19 @@ def test_kernels_are_sm100a_tcgen05(native_lib):
     elf = subprocess.run(["cuobjdump", "-lelf", str(_native.LIB_PATH)], capture_output=True,
                          text=True).stdout
     assert "sm_100a" in elf
+
+
+def test_integration_stub_matches_the_abi():
+    """The ctypes stub INTEGRATION.md tells a reference maintainer to add binds
+    the same argument counts as this package's own binding (guards doc rot)."""
+    import re
+
+    from paper_2601_06562_b200 import _native
+
+    text = (ROOT / "INTEGRATION.md").read_text()
+    stub = text[text.index("for name, args in {"):text.index("}.items():")]
+    entries = re.findall(r'"(mosaic_[a-z0-9_]+)":\s*\[(.*?)\],', stub, flags=re.S)
+    assert len(entries) >= 6
+    for name, args in entries:
+        n_args = len([a for a in args.replace("\n", " ").split(",") if a.strip()])
+        assert n_args == len(_native.SIGNATURES[name][1]), name
