@@ -113,6 +113,23 @@ def main():
                                     "hc_bytes_saved": M * d * 2}
         del H, W, hc
 
+    # whole step: eager launches vs one captured CUDA graph (launch-bound at small sizes)
+    from paper_2601_06562_b200 import MaskOnlyHead
+
+    for name, L, d, V in (("tiny", 2048, 256, 8192), ("llada", 32768, 4096, 126464)):
+        H = torch.randn(L, d, generator=g, device=dev).to(torch.bfloat16)
+        W = (torch.randn(V, d, generator=g, device=dev) * 0.02).to(torch.bfloat16)
+        x0 = torch.randint(0, V - 1, (L,), generator=g, device=dev, dtype=torch.int32)
+        x0[L // 2:] = V - 1
+        head = MaskOnlyHead(W, seq_len=L, mask_id=V - 1)
+        x = x0.clone()
+        eager_ms = timeit(lambda: (x.copy_(x0), head.step(x, H, 64)), iters=20)
+        xg = x0.clone()
+        graph = head.capture(xg, H, 64)
+        graph_ms = timeit(lambda: (xg.copy_(x0), graph.replay()), iters=20)
+        out[f"step_{name}"] = {"L": L, "d": d, "V": V, "eager_ms": eager_ms, "graph_ms": graph_ms}
+        del H, W
+
     # K5 ---------------------------------------------------------------------
     for M, k in ((16384, 256), (65536, 683), (524288, 8192)):
         conf = torch.rand(M, generator=g, device=dev)

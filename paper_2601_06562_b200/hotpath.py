@@ -395,6 +395,23 @@ class MaskOnlyHead:
     def workspace_bytes(self) -> int:
         return self.layout.size
 
+    def capture(self, x: torch.Tensor, hidden: torch.Tensor, k: int) -> "torch.cuda.CUDAGraph":
+        """Capture one whole step (K1..K5) into a CUDA graph bound to these
+        ``x`` / ``hidden`` buffers and this ``k``. Every launch reads the masked
+        count from the device (K1's output), so one graph serves every step of
+        a run whatever M is: refill ``x`` / ``hidden`` in place and ``replay()``.
+        Nothing runs during capture (``x`` is untouched until the first replay).
+        Single-process heads only (the exchange paths are not captured)."""
+        if self.group is not None or self.p2p is not None:
+            raise InputError("graph capture is for single-process heads")
+        g = torch.cuda.CUDAGraph()
+        side = torch.cuda.Stream(device=x.device)
+        side.wait_stream(torch.cuda.current_stream(x.device))
+        with torch.cuda.graph(g, stream=side):
+            self.step(x, hidden, k)
+        torch.cuda.current_stream(x.device).wait_stream(side)
+        return g
+
     def step(self, x: torch.Tensor, hidden: torch.Tensor, k: int, stream=None) -> StepOutput:
         b = self.buf
         _req(x, torch.int32, "x", 1)

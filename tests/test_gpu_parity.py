@@ -540,3 +540,30 @@ def test_step_edge_counts(dev, n_masked, k):
         assert np.array_equal(sel, orc.remask_select(out.conf[:M].cpu().numpy(), ref["idx"], committed))
         ok = ref["margin"] > MARGIN
         assert np.array_equal(out.token[:M].cpu().numpy()[ok], ref["arg"][ok])
+
+
+def test_graph_captured_step_matches_eager(dev):
+    """One captured CUDA graph replays the whole step for successive steps
+    (different masked counts, same buffers) bit-identically to eager steps."""
+    from paper_2601_06562_b200 import MaskOnlyHead
+
+    rng = np.random.default_rng(77)
+    L, d, V, mid, k = 4096, 512, 16384, 16383, 64
+    H = bf16_tensor(rng.standard_normal((L, d)), dev)
+    W = bf16_tensor(rng.standard_normal((V, d)) * 0.05, dev)
+    x0 = rng.integers(0, V - 1, size=L).astype(np.int32)
+    x0[L // 3:] = mid
+    eager = MaskOnlyHead(W, seq_len=L, mask_id=mid)
+    graphed = MaskOnlyHead(W, seq_len=L, mask_id=mid)
+    xe = torch.from_numpy(x0).to(dev)
+    xg = torch.from_numpy(x0).to(dev)
+    g = graphed.capture(xg, H, k)
+    assert torch.equal(xg.cpu(), torch.from_numpy(x0))  # capture ran nothing
+    for _ in range(4):  # four denoising steps: M shrinks by k each time
+        oe = eager.step(xe, H, k)
+        g.replay()
+        torch.cuda.synchronize()
+        M = int(oe.m_dev.item())
+        assert int(graphed.buf["m_dev"].item()) == M
+        assert torch.equal(xe.cpu(), xg.cpu())
+        assert torch.equal(oe.conf[:M].cpu(), graphed.buf["conf"][:M].cpu())
