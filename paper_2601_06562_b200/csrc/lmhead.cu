@@ -375,10 +375,11 @@ __global__ void __launch_bounds__(kGather == kGatherCpAsync ? kThreadsCpAsync : 
           for (int kb = 0; kb < k_blocks; ++kb) {
             mbar_wait(&full[stage], phase);
             if constexpr (kGather == kGatherCpAsync) {
+              // best measured variant (profiles/r01_k3_gather_modes.txt): cluster-scope
+              // acquire poll, one consumer-side proxy fence covering both CTAs' rows
               mbar_wait_cluster(&afull[stage], phase);
-              // generic-proxy cp.async writes of this CTA -> tcgen05.mma reads (the
-              // peer's half was fenced by its relay before it arrived here)
-              asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+              if constexpr (CG == 2) asm volatile("fence.proxy.async.shared::cluster;" ::: "memory");
+              else asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
             }
             tc_fence_after();
             const uint32_t a0 = smem_u32(sA + stage * C::A_BYTES);
@@ -414,7 +415,6 @@ __global__ void __launch_bounds__(kGather == kGatherCpAsync ? kThreadsCpAsync : 
           for (int t = t0; t < t1; ++t)
             for (int kb = 0; kb < k_blocks; ++kb) {
               mbar_wait(&afull[stage], phase);
-              asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // landed rows -> async proxy
               mbar_arrive_cluster(mapa_shared(smem_u32(&afull[stage]), 0));
               if (++stage == C::STAGES) {
                 stage = 0;
