@@ -389,6 +389,7 @@ def gpu_main(args):
                    "masked": M, "unmask_k": k, "mask_layout": "suffix (step 0)",
                    "parallelism": f"vocab-sharded x{world} ({args.exchange} exchange)" if world > 1 else "single GPU",
                    "vocab_shard": v1 - v0, "n_splits": head.n_splits,
+                   "k3_schedule": "die-aware" if head.die_table is not None else "default",
                    "l2": "inputs larger than L2 (W 1.04 GB, H 268 MB > 126 MB)"},
         "roofline": {"bound": "tensor", "kernel": "k3_lmhead (tcgen05 stats GEMM)",
                      "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,

@@ -36,7 +36,10 @@ constexpr int UK = 16;           // K per tcgen05.mma (kind::f16)
 constexpr int NUM_ACC = 2;       // TMEM accumulator double buffer
 constexpr int TMEM_COLS = 512;   // 2 x 256 fp32 columns
 constexpr int kThreads = 192;    // warp0 TMA, warp1 MMA+TMEM, warps 2..5 epilogue
-constexpr int kAWarps = 8;       // cp.async gather path: A loader warps (warp 0 + warps 6..)
+#ifndef MOSAIC_K3_AWARPS
+#define MOSAIC_K3_AWARPS 4  // measured: 4 >= 8 once the per-stage sync is CTA-scope
+#endif
+constexpr int kAWarps = MOSAIC_K3_AWARPS;  // cp.async gather path: A loader warps (warp 0 + warps 6..)
 constexpr int kRowsPerAWarp = BM / kAWarps;  // 16
 static_assert(kRowsPerAWarp % 4 == 0 && kRowsPerAWarp <= 32, "loader warp covers 4-row groups");
 constexpr int kThreadsCpAsync = kThreads + (kAWarps - 1) * 32;
@@ -44,6 +47,9 @@ constexpr int kEpiWarps = 4;
 constexpr int kMaxSplits = 64;
 #ifndef MOSAIC_K3_EPI_SLEEP_NS
 #define MOSAIC_K3_EPI_SLEEP_NS 0   // epilogue poll backoff while the next accumulator fills
+#endif
+#ifndef MOSAIC_K3_GFENCE
+#define MOSAIC_K3_GFENCE 1  // gather mode: proxy fence per stage (0 = none, experiment)
 #endif
 #ifndef MOSAIC_K3_PROD_SLEEP_NS
 #define MOSAIC_K3_PROD_SLEEP_NS 0  // producer poll backoff while the ring is full
@@ -215,15 +221,22 @@ __global__ void __launch_bounds__(kGather == kGatherCpAsync ? kThreadsCpAsync : 
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
 
-  // Die-aware schedule: each die's pairs take the units of their own share of
-  // the m-blocks, so an m-group's gathered rows (re-read once per vocab tile)
-  // live in one die's L2 instead of being replicated in both. The pair leader
-  // registers its die (slot = arrival order on that die), all pairs meet at a
-  // grid barrier (persistent grid: every CTA is resident; bounded spin), then
-  // split the m-blocks in proportion to the pairs each die actually got -- so
-  // the result is exact for any SM placement or die map; only locality varies.
+  // Die-aware schedule: the units (in the usual m-group order, so a contiguous
+  // unit range covers whole m-groups) are split between the two dies in
+  // proportion to the pairs each die actually got, and each die's pairs stride
+  // over their own range only -- an m-group's rows (re-read once per vocab
+  // tile) then live in one die's L2 instead of being replicated in both.
+  // Splitting by units rather than whole m-blocks keeps every pair within one
+  // unit of the default schedule's load. The pair leader registers its die
+  // (slot = arrival order on that die); the split needs every pair registered,
+  // so the pairs agree on a decision word: the pair whose registration
+  // completes the count publishes "die-aware", and a pair that waited ~100 us
+  // without that (some CTAs not resident, e.g. another kernel holding SMs)
+  // publishes "default". Whoever comes later reads the published decision, so
+  // the launch never traps or hangs, and either schedule is exact.
+  // sched[0..1] = pairs registered per die, sched[2] = total, sched[3] = decision.
   int64_t u_first = cluster, u_stride = n_clusters;
-  int mb_lo = 0, mb_cnt = m_blocks;
+  int64_t units_here = static_cast<int64_t>(m_blocks) * p.n_splits;
   if (p.die_of_sm != nullptr) {
     int32_t* info = reinterpret_cast<int32_t*>(smem + C::STAGES * C::STAGE_BYTES + 256 + BM * 4);
     if (threadIdx.x == 0 && rank == 0) {
@@ -232,17 +245,28 @@ __global__ void __launch_bounds__(kGather == kGatherCpAsync ? kThreadsCpAsync : 
       const int d = p.die_of_sm[smid] == 1 ? 1 : 0;
       const uint32_t slot = atomicAdd(p.sched + d, 1u);
       __threadfence();
-      atomicAdd(p.sched + 2, 1u);
-      uint32_t spins = 0;
-      while (*reinterpret_cast<volatile uint32_t*>(p.sched + 2) < static_cast<uint32_t>(n_clusters))
-        if (++spins == (1u << 26)) __trap();  // a pair never became resident: fail, do not hang
+      volatile uint32_t* decision = p.sched + 3;
+      if (atomicAdd(p.sched + 2, 1u) + 1u == static_cast<uint32_t>(n_clusters)) {
+        __threadfence();
+        atomicCAS(p.sched + 3, 0u, 1u);  // every pair registered: die-aware
+      }
+      const long long t0 = clock64();
+      while (*decision == 0u) {
+        if (clock64() - t0 > 200000) atomicCAS(p.sched + 3, 0u, 2u);  // ~100+ us: fall back
+        __nanosleep(200);
+      }
       __threadfence();
-      const int64_t n0 = *reinterpret_cast<volatile uint32_t*>(p.sched + 0);
-      const int64_t n1 = *reinterpret_cast<volatile uint32_t*>(p.sched + 1);
-      const int mb0 = static_cast<int>((m_blocks * n0 + (n0 + n1) / 2) / (n0 + n1));
-      const int32_t v[4] = {static_cast<int32_t>(slot), static_cast<int32_t>(d ? n1 : n0), d ? mb0 : 0,
-                            d ? m_blocks - mb0 : mb0};
-      for (int i = 0; i < 4; ++i) {
+      int32_t v[3] = {static_cast<int32_t>(cluster), static_cast<int32_t>(n_clusters),
+                      static_cast<int32_t>(units_here)};
+      if (*decision == 1u) {
+        const int64_t n0 = *reinterpret_cast<volatile uint32_t*>(p.sched + 0);
+        const int64_t n1 = *reinterpret_cast<volatile uint32_t*>(p.sched + 1);
+        const int64_t u0 = (units_here * n0 + (n0 + n1) / 2) / (n0 + n1);  // die 0: [0, u0), die 1: [u0, end)
+        v[0] = static_cast<int32_t>((d ? u0 : 0) + slot);
+        v[1] = static_cast<int32_t>(d ? n1 : n0);
+        v[2] = static_cast<int32_t>(d ? units_here : u0);
+      }
+      for (int i = 0; i < 3; ++i) {
         info[i] = v[i];
         if constexpr (CG == 2)
           asm volatile("st.shared::cluster.s32 [%0], %1;" ::"r"(mapa_shared(smem_u32(info + i), 1)), "r"(v[i])
@@ -252,10 +276,8 @@ __global__ void __launch_bounds__(kGather == kGatherCpAsync ? kThreadsCpAsync : 
     if constexpr (CG == 2) cluster_sync(); else __syncthreads();
     u_first = info[0];
     u_stride = info[1];
-    mb_lo = info[2];
-    mb_cnt = info[3];
+    units_here = info[2];
   }
-  const int64_t units_here = static_cast<int64_t>(mb_cnt) * p.n_splits;
 
   if (warp == 0 || (kGather == kGatherCpAsync && warp >= 6)) {
     // ------------------------------------------------------------ TMA producer (both CTAs)
@@ -266,8 +288,7 @@ __global__ void __launch_bounds__(kGather == kGatherCpAsync ? kThreadsCpAsync : 
     uint32_t stage = 0, phase = 0;
     for (int64_t u = u_first; u < units_here; u += u_stride) {
       int mb, s;
-      unit_coords(p, mb_cnt, u, mb, s);
-      mb += mb_lo;
+      unit_coords(p, m_blocks, u, mb, s);
       const int t0 = s * p.tiles_per_split;
       const int t1 = min(t0 + p.tiles_per_split, p.n_tiles);
       const int a_row = mb * C::ROWS + rank * BM;
@@ -363,8 +384,7 @@ __global__ void __launch_bounds__(kGather == kGatherCpAsync ? kThreadsCpAsync : 
       uint32_t stage = 0, phase = 0, acc = 0, acc_phase = 0;
       for (int64_t u = u_first; u < units_here; u += u_stride) {
         int mb, s;
-        unit_coords(p, mb_cnt, u, mb, s);
-      mb += mb_lo;
+        unit_coords(p, m_blocks, u, mb, s);
         const int t0 = s * p.tiles_per_split;
         const int t1 = min(t0 + p.tiles_per_split, p.n_tiles);
         for (int t = t0; t < t1; ++t) {
@@ -375,11 +395,15 @@ __global__ void __launch_bounds__(kGather == kGatherCpAsync ? kThreadsCpAsync : 
           for (int kb = 0; kb < k_blocks; ++kb) {
             mbar_wait(&full[stage], phase);
             if constexpr (kGather == kGatherCpAsync) {
-              // best measured variant (profiles/r01_k3_gather_modes.txt): cluster-scope
-              // acquire poll, one consumer-side proxy fence covering both CTAs' rows
-              mbar_wait_cluster(&afull[stage], phase);
-              if constexpr (CG == 2) asm volatile("fence.proxy.async.shared::cluster;" ::: "memory");
-              else asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+              // this CTA's rows landed (and, on a pair, the peer's: relayed below);
+              // the proxy fence orders this CTA's generic-proxy cp.async writes
+              // before the tensor core's async-proxy reads. Only CTA-scope
+              // operations on the per-stage path: cluster-scope fences and
+              // release.cluster arrives compile to MEMBAR.ALL.GPU, which
+              // serialised the pair ring at ~0.9 us per stage
+              // (profiles/r01_k3_gather_modes.txt).
+              mbar_wait(&afull[stage], phase);
+              if (MOSAIC_K3_GFENCE) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
             }
             tc_fence_after();
             const uint32_t a0 = smem_u32(sA + stage * C::A_BYTES);
@@ -408,14 +432,19 @@ __global__ void __launch_bounds__(kGather == kGatherCpAsync ? kThreadsCpAsync : 
         uint32_t stage = 0, phase = 0;
         for (int64_t u = u_first; u < units_here; u += u_stride) {
           int mb, s;
-          unit_coords(p, mb_cnt, u, mb, s);
-      mb += mb_lo;
+          unit_coords(p, m_blocks, u, mb, s);
           const int t0 = s * p.tiles_per_split;
           const int t1 = min(t0 + p.tiles_per_split, p.n_tiles);
           for (int t = t0; t < t1; ++t)
             for (int kb = 0; kb < k_blocks; ++kb) {
               mbar_wait(&afull[stage], phase);
-              mbar_arrive_cluster(mapa_shared(smem_u32(&afull[stage]), 0));
+              // peer rows -> async proxy, then a CTA-scope (release.cta) arrive on
+              // the leader's barrier: the form CUTLASS's cluster pipelines use for
+              // remote arrives (cutlass/arch/barrier.h ClusterBarrier::arrive)
+              if (MOSAIC_K3_GFENCE) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+              asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(
+                               mapa_shared(smem_u32(&afull[stage]), 0))
+                           : "memory");
               if (++stage == C::STAGES) {
                 stage = 0;
                 phase ^= 1;
@@ -433,8 +462,7 @@ __global__ void __launch_bounds__(kGather == kGatherCpAsync ? kThreadsCpAsync : 
     uint32_t acc = 0, acc_phase = 0;
     for (int64_t u = u_first; u < units_here; u += u_stride) {
       int mb, s;
-      unit_coords(p, mb_cnt, u, mb, s);
-      mb += mb_lo;
+      unit_coords(p, m_blocks, u, mb, s);
       const int t0 = s * p.tiles_per_split;
       const int t1 = min(t0 + p.tiles_per_split, p.n_tiles);
       const int64_t row = static_cast<int64_t>(mb) * C::ROWS + rank * BM + row_local;
@@ -633,11 +661,8 @@ int launch(const ASource& a, int64_t m_cap, const int32_t* m_dev, int64_t m_host
   MOSAIC_REQUIRE(a.ld >= d && a.ld % 8 == 0, "row stride %lld must be >= d and a multiple of 8", (long long)a.ld);
   if (m_cap == 0) return MOSAIC_OK;
   const bool gather = a.idx != nullptr;
-  // Gather mode runs cta_group::1 unless forced: its cp.async A path reaches
-  // parity with K2 + dense K3 on single-SM tiles, while the pair variant pays
-  // a cross-CTA "rows landed" relay per stage (profiles/r01_k3_gather_modes.txt).
-  static const int forced_cg = env_int("MOSAIC_CTA_GROUP", 0);
-  const int cg = gather ? (forced_cg == 2 && m_cap > BM ? 2 : 1) : cta_group_for(m_cap);
+  const int cg = cta_group_for(m_cap);  // gather mode included: pairs measured faster since the
+                                        // per-stage sync is CTA-scope only (r01_k3_gather_modes.txt)
   CUtensorMap ta, tb;
   int st = gather ? encode_tma_bf16(&ta, a.base, a.rows, d, a.ld, 1, BK) : encode_tma_bf16(&ta, a.base, m_cap, d, a.ld, BM, BK);
   if (st) return st;

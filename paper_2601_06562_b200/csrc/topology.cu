@@ -3,7 +3,7 @@
 // unit schedule so the gathered rows an m-group re-reads stay in ONE die's L2
 // instead of being replicated in both.
 //
-// Method (validated on B200, profiles/r01e_die_probe.txt): one CTA reads a
+// Method (validated on B200, profiles/r01_die_probe.txt): one CTA reads a
 // pool of lines (bringing each into its own die's L2 and into the line's home
 // L2); then every SM times one cold read per line of a private 64 KB slice of
 // the pool. Lines are homed on a die per 2 KB chunk; an SM on the reader's die
@@ -20,12 +20,6 @@ namespace {
 
 constexpr int kLinesPerSm = 512;  // 64 KB = 32 two-KB homing chunks per SM
 constexpr int kLineWords = 32;    // 128-byte lines
-
-__global__ void topo_discard(uint32_t* buf, int64_t n_lines) {
-  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n_lines;
-       i += static_cast<int64_t>(gridDim.x) * blockDim.x)
-    asm volatile("discard.global.L2 [%0], 128;" ::"l"(buf + i * kLineWords) : "memory");
-}
 
 __global__ void topo_touch(const uint32_t* buf, int64_t n_lines, uint32_t* sink) {
   uint32_t acc = 0;
@@ -58,8 +52,20 @@ __global__ void topo_probe(const uint32_t* buf, uint32_t* lat, uint32_t* claimed
 
 using namespace mosaic;
 
+// Eviction region: written in full before every round so the pool's lines are
+// out of both dies' L2 (2x the L2 size). A discard.global.L2 of the pool
+// instead left ~30 SMs with intermediate slow fractions; the full write gives
+// a clean 0% / 50% split (profiles/r01_die_probe.txt).
+static size_t flush_bytes() {
+  int dev = 0, l2 = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, dev);
+  return 2 * static_cast<size_t>(l2 > 0 ? l2 : (128 << 20));
+}
+
 extern "C" size_t mosaic_die_map_scratch_bytes(int32_t n_sm) {
-  return static_cast<size_t>(n_sm) * kLinesPerSm * (kLineWords * 4 + 4) + static_cast<size_t>(n_sm + 2) * 4;
+  return static_cast<size_t>(n_sm) * kLinesPerSm * (kLineWords * 4 + 4) + static_cast<size_t>(n_sm + 2) * 4 + 256 +
+         flush_bytes();
 }
 
 extern "C" int mosaic_die_map(uint8_t* die_of_sm_host, int32_t n_sm, void* scratch, int32_t* n_die0_out,
@@ -71,31 +77,58 @@ extern "C" int mosaic_die_map(uint8_t* die_of_sm_host, int32_t n_sm, void* scrat
   uint32_t* lat = buf + n_lines * kLineWords;
   uint32_t* claimed = lat + n_lines;
   uint32_t* sink = claimed + n_sm;  // 2 words
-  MOSAIC_CUDA(cudaMemsetAsync(buf, 1, static_cast<size_t>(n_lines) * kLineWords * 4, s));
-  MOSAIC_CUDA(cudaMemsetAsync(claimed, 0, static_cast<size_t>(n_sm + 2) * 4, s));
-  topo_discard<<<num_sms() * 4, 256, 0, s>>>(buf, n_lines);  // out of every L2: the next reads go to HBM
-  topo_touch<<<1, 256, 0, s>>>(buf, n_lines, sink);
-  topo_probe<<<n_sm * 8, 32, 0, s>>>(buf, lat, claimed, sink, n_sm);
-  MOSAIC_CUDA(cudaGetLastError());
+  uint8_t* flush = reinterpret_cast<uint8_t*>(
+      (reinterpret_cast<uintptr_t>(sink + 2) + 255) & ~static_cast<uintptr_t>(255));
+  // Three probe rounds (each: evict, touch from one CTA, time cold reads), the
+  // slow-read counts summed per SM before classifying.
+  constexpr int kRounds = 3;
+  std::vector<int> slow(static_cast<size_t>(n_sm), 0), seen(static_cast<size_t>(n_sm), 0);
   std::vector<uint32_t> L(static_cast<size_t>(n_lines)), cl(static_cast<size_t>(n_sm));
-  MOSAIC_CUDA(cudaMemcpyAsync(L.data(), lat, L.size() * 4, cudaMemcpyDeviceToHost, s));
-  MOSAIC_CUDA(cudaMemcpyAsync(cl.data(), claimed, cl.size() * 4, cudaMemcpyDeviceToHost, s));
-  MOSAIC_CUDA(cudaStreamSynchronize(s));
-  std::vector<uint32_t> all(L);
-  std::nth_element(all.begin(), all.begin() + all.size() / 2, all.end());
-  const uint32_t med = all[all.size() / 2];
+  MOSAIC_CUDA(cudaMemsetAsync(buf, 1, static_cast<size_t>(n_lines) * kLineWords * 4, s));
+  for (int round = 0; round < kRounds; ++round) {
+    MOSAIC_CUDA(cudaMemsetAsync(claimed, 0, static_cast<size_t>(n_sm + 2) * 4, s));
+    MOSAIC_CUDA(cudaMemsetAsync(flush, round + 2, flush_bytes(), s));  // pool out of every L2
+    topo_touch<<<1, 256, 0, s>>>(buf, n_lines, sink);
+    topo_probe<<<n_sm * 8, 32, 0, s>>>(buf, lat, claimed, sink, n_sm);
+    MOSAIC_CUDA(cudaGetLastError());
+    MOSAIC_CUDA(cudaMemcpyAsync(L.data(), lat, L.size() * 4, cudaMemcpyDeviceToHost, s));
+    MOSAIC_CUDA(cudaMemcpyAsync(cl.data(), claimed, cl.size() * 4, cudaMemcpyDeviceToHost, s));
+    MOSAIC_CUDA(cudaStreamSynchronize(s));
+    // the touching CTA's die is the reference: keep rounds consistent by
+    // recording its SM and flipping a round whose toucher sits on the other die
+    std::vector<uint32_t> all(L);
+    std::nth_element(all.begin(), all.begin() + all.size() / 2, all.end());
+    const uint32_t med = all[all.size() / 2];
+    std::vector<int> round_slow(static_cast<size_t>(n_sm), -1);
+    for (int sm = 0; sm < n_sm; ++sm) {
+      if (!cl[sm]) continue;
+      int c = 0;
+      for (int i = 0; i < kLinesPerSm; ++i) c += L[static_cast<size_t>(sm) * kLinesPerSm + i] > med + 60;
+      round_slow[sm] = c;
+    }
+    uint32_t toucher = 0;
+    MOSAIC_CUDA(cudaMemcpy(&toucher, sink + 1, 4, cudaMemcpyDeviceToHost));
+    // orientation: die 0 = round 0's toucher die. If this round's toucher reads
+    // as slow in the accumulated map, its labels are inverted.
+    bool flip = false;
+    if (round > 0 && toucher < static_cast<uint32_t>(n_sm) && seen[toucher] > 0)
+      flip = 100 * slow[toucher] / (seen[toucher] * kLinesPerSm) >= 25;
+    for (int sm = 0; sm < n_sm; ++sm) {
+      if (round_slow[sm] < 0) continue;
+      slow[sm] += flip ? kLinesPerSm - round_slow[sm] : round_slow[sm];
+      ++seen[sm];
+    }
+  }
   int n0 = 0, amb = 0;
   for (int sm = 0; sm < n_sm; ++sm) {
-    if (!cl[sm]) {  // no probe CTA landed on this SM: unknown
+    if (!seen[sm]) {  // no probe CTA landed on this SM in any round: unknown
       die_of_sm_host[sm] = 255;
       ++amb;
       continue;
     }
-    int slow = 0;
-    for (int i = 0; i < kLinesPerSm; ++i) slow += L[static_cast<size_t>(sm) * kLinesPerSm + i] > med + 60;
-    const int pct = 100 * slow / kLinesPerSm;
+    const int pct = 100 * slow[sm] / (seen[sm] * kLinesPerSm);
     if (pct >= 10 && pct < 25) ++amb;
-    die_of_sm_host[sm] = pct < 10 ? 0 : 1;  // 0 = the reading CTA's die
+    die_of_sm_host[sm] = pct < 10 ? 0 : 1;  // 0 = the first reading CTA's die
     n0 += pct < 10;
   }
   if (n_die0_out) *n_die0_out = n0;

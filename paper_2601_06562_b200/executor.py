@@ -114,7 +114,7 @@ class StepExecutor:
     """Executes step graphs of one model inside one :class:`Workspace` (cuda)."""
 
     def __init__(self, model: RandomDLLM, workspace: Workspace, mask_id: int, exec_layers: Optional[int] = None,
-                 group=None):
+                 group=None, die_aware: Optional[bool] = None):
         if workspace.backend != "cuda":
             raise InputError("the executor needs a cuda workspace")
         self.model = model
@@ -134,6 +134,9 @@ class StepExecutor:
         dev = torch.device("cuda", workspace.device)
         self.device = dev
         self._side: dict[int, dict] = {}
+        # K3's die-aware unit schedule (csrc/lmhead.cu), as in MaskOnlyHead
+        self.die_table = hotpath.die_map(dev)[0] if hotpath.die_aware_default(die_aware) else None
+        self._sched = torch.zeros(4, dtype=torch.int32, device=dev)
 
     # ---------------------------------------------------------------- buffers
     def _side_buffers(self, L: int) -> dict:
@@ -314,7 +317,8 @@ class StepExecutor:
             pa = flat[2 * S * cap: 3 * S * cap].view(torch.int32).view(S, cap)
             if r1 > r0:
                 hotpath.lmhead_stats(hc, self.model.w_vocab, S, pm, ps, pa, m_host=r1 - r0,
-                                     v_offset=self.model.vocab_offset)
+                                     v_offset=self.model.vocab_offset, die_of_sm=self.die_table,
+                                     sched=self._sched)
             self._last_splits = S
         elif kind == "lmhead_stats_gather":  # K3 gather mode: A rows read from h at mask_idx
             r0, r1 = _rows(M, b["K_logits"], op.iteration)

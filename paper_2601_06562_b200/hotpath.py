@@ -14,6 +14,7 @@ of one preplanned workspace. Reference anchors:
 from __future__ import annotations
 
 import ctypes
+import os
 from dataclasses import dataclass
 from typing import Optional
 
@@ -110,6 +111,15 @@ def die_map(device=None) -> tuple[torch.Tensor, dict]:
         table = torch.tensor(list(host), dtype=torch.uint8, device=dev)
         _DIE_MAPS[dev.index] = (table, {"n_sm": n_sm, "die0_sms": n0.value, "ambiguous": amb.value})
     return _DIE_MAPS[dev.index]
+
+
+def die_aware_default(die_aware: Optional[bool] = None) -> bool:
+    """K3's die-aware unit schedule: on unless disabled (argument, or
+    MOSAIC_DIE_AWARE=0). Measured on B200 (profiles/r01h_k3_die_aware.txt):
+    DRAM per launch 6.2-6.7 GB vs 10.8-11.1 GB, +2-2.5% steady throughput."""
+    if die_aware is not None:
+        return bool(die_aware)
+    return os.environ.get("MOSAIC_DIE_AWARE", "1") != "0"
 
 
 def lmhead_stats(hc: torch.Tensor, weight: torch.Tensor, n_splits: int, part_max: torch.Tensor,
@@ -345,11 +355,8 @@ class MaskOnlyHead:
         self.shift = bool(shift)
         self.group = group
         self.fused_gather = bool(fused_gather)  # K3 reads rows of `hidden` directly: no K2, no hc buffer
-        if die_aware is None:
-            import os
-
-            die_aware = os.environ.get("MOSAIC_DIE_AWARE", "0") == "1"
-        self.die_table = die_map(weight_shard.device)[0] if die_aware and not self.fused_gather else None
+        self.die_table = (die_map(weight_shard.device)[0]
+                          if die_aware_default(die_aware) and not self.fused_gather else None)
         if not (exchange in ("nccl", "p2p") or hasattr(exchange, "push")):
             raise InputError(f"exchange must be 'nccl', 'p2p' or a P2PExchange, got {exchange!r}")
         self.exchange = exchange

@@ -483,7 +483,9 @@ def test_die_map_and_die_aware_k3(dev):
 
     table, info = hotpath.die_map(dev)
     t = table.cpu().numpy()
-    assert set(np.unique(t)) <= {0, 1} and info["ambiguous"] <= 16
+    # the map is a timing heuristic (three probe rounds); the kernel's exactness
+    # below does not depend on it, so only gross failures are asserted here
+    assert set(np.unique(t)) <= {0, 1} and info["ambiguous"] <= 8
     assert abs(int((t == 0).sum()) - int((t == 1).sum())) <= 24
     rng = np.random.default_rng(3)
     for m, d, V in ((5000, 1024, 40000), (16384, 4096, 126464 // 4), (100, 256, 3000)):
@@ -497,10 +499,44 @@ def test_die_map_and_die_aware_k3(dev):
             sched = torch.empty(4, dtype=torch.int32, device=dev)
             hotpath.lmhead_stats(Hc, W, S, pm, ps, pa, m_host=m, v_offset=3, die_of_sm=tab, sched=sched)
             torch.cuda.synchronize()
+            if tab is not None:  # alone on the GPU every pair registers: the die-aware split is taken
+                assert int(sched[3]) == 1
             outs.append((pm.cpu(), ps.cpu(), pa.cpu()))
         for o in outs[1:]:
             for a, b in zip(outs[0], o):
                 assert torch.equal(a, b)
+
+
+def test_die_aware_k3_with_sms_held_by_another_stream(dev):
+    """K3's die-aware prologue must neither trap nor hang when not every pair
+    can become resident (another stream's GEMM holds the SMs): the pairs agree
+    on the default schedule instead, and the result is unchanged."""
+    from paper_2601_06562_b200 import hotpath
+
+    table, _ = hotpath.die_map(dev)
+    rng = np.random.default_rng(5)
+    m, d, V = 16384, 4096, 126464 // 4
+    Hc = bf16_tensor(rng.standard_normal((m, d)), dev)
+    W = bf16_tensor(rng.standard_normal((V, d)) * 0.03, dev)
+    S, _ = hotpath.lmhead_plan(m, V, d)
+    outs, decisions = [], []
+    a = torch.randn(8192, 8192, device=dev, dtype=torch.bfloat16)
+    hog = torch.cuda.Stream(dev)
+    for tab in (None, table):
+        pm, ps = torch.empty(S, m, device=dev), torch.empty(S, m, device=dev)
+        pa = torch.empty(S, m, dtype=torch.int32, device=dev)
+        sched = torch.zeros(4, dtype=torch.int32, device=dev)
+        torch.cuda.synchronize()
+        with torch.cuda.stream(hog):
+            for _ in range(8):
+                a = (a @ a).clamp_(-1, 1)
+        hotpath.lmhead_stats(Hc, W, S, pm, ps, pa, m_host=m, die_of_sm=tab, sched=sched)
+        torch.cuda.synchronize()
+        decisions.append(int(sched[3]))
+        outs.append((pm.cpu(), ps.cpu(), pa.cpu()))
+    assert decisions[1] in (1, 2)
+    for x, y in zip(*outs):
+        assert torch.equal(x, y)
 
 
 @pytest.mark.parametrize("n_masked,k", [(0, 5), (1, 1), (1, 7), (17, 100), (4096, 0), (4096, 4096)])
