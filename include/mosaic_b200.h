@@ -107,12 +107,14 @@ MOSAIC_API int mosaic_lmhead_stats(const uint16_t* Hc, int64_t m_cap, const int3
                         int32_t n_splits, float* part_max, float* part_sum, int32_t* part_arg,
                         void* stream);
 
-/* K3 with the die-aware unit schedule: as mosaic_lmhead_stats, but each of
- * the GPU's two L2 dies takes the units of its own share of the masked-row
- * blocks, so a block's rows stay in one die's L2. die_of_sm: device uint8
- * [num SMs] from mosaic_die_map (0/1); sched_scratch: 16 caller-owned device
- * bytes (zeroed by the call; one launch at a time per scratch). Exact for any
- * map (only locality depends on it).                                         */
+/* K3 with the die-aware unit schedule: as mosaic_lmhead_stats, but the work
+ * units are split between the GPU's two L2 dies in proportion to the SM pairs
+ * each die holds, each die's pairs taking a contiguous range of whole m-groups,
+ * so a row block stays in one die's L2. die_of_sm: device uint8 [num SMs] from
+ * mosaic_die_map (0/1); sched_scratch: 16 caller-owned device bytes (zeroed by
+ * the call; one launch at a time per scratch; word 3 ends as 1 = die-aware
+ * split taken, 2 = not every pair became resident within ~100 us, default
+ * split taken). Exact for any map and either outcome.                        */
 MOSAIC_API int mosaic_lmhead_stats_die(const uint16_t* Hc, int64_t m_cap, const int32_t* m_dev, int64_t m_host,
                             const uint16_t* W, int64_t V_shard, int64_t d, int64_t v_offset,
                             int32_t n_splits, float* part_max, float* part_sum, int32_t* part_arg,
@@ -129,13 +131,20 @@ MOSAIC_API int mosaic_die_map(uint8_t* die_of_sm_host, int32_t n_sm, void* scrat
 /* Gather mode of K3 -- the paper's gather-GEMM with no intermediate buffer:
  * the A rows are read straight from the hidden states H [n_rows, d] (row
  * stride ld_h elements) at the masked positions idx[0..M) (src(p) = p, or
- * max(p-1, 0) with shift = 1) by TMA tile::gather4, so K2 and the [m_cap, d]
- * compacted buffer disappear. Outputs as mosaic_lmhead_stats.                */
+ * max(p-1, 0) with shift = 1) by cp.async loader warps (16-byte segments,
+ * swizzled in software to the UMMA layout), so K2 and the [m_cap, d]
+ * compacted buffer disappear. Outputs as mosaic_lmhead_stats. The _die form
+ * adds the die-aware schedule (arguments as mosaic_lmhead_stats_die).        */
 MOSAIC_API int mosaic_lmhead_stats_gather(const uint16_t* H, int64_t n_rows, int64_t ld_h, const int32_t* idx,
                                int32_t shift, int64_t m_cap, const int32_t* m_dev, int64_t m_host,
                                const uint16_t* W, int64_t V_shard, int64_t d, int64_t v_offset,
                                int32_t n_splits, float* part_max, float* part_sum, int32_t* part_arg,
                                void* stream);
+MOSAIC_API int mosaic_lmhead_stats_gather_die(const uint16_t* H, int64_t n_rows, int64_t ld_h, const int32_t* idx,
+                                   int32_t shift, int64_t m_cap, const int32_t* m_dev, int64_t m_host,
+                                   const uint16_t* W, int64_t V_shard, int64_t d, int64_t v_offset,
+                                   int32_t n_splits, float* part_max, float* part_sum, int32_t* part_arg,
+                                   const uint8_t* die_of_sm, uint32_t* sched_scratch, void* stream);
 
 /* Debug / parity path for the reference operator itself: out[r, v] =
  * <Hc[r, :], W[v, :]> in fp32, row stride ldo. Materialises the logits like

@@ -762,11 +762,12 @@ extern "C" int mosaic_lmhead_stats_die(const uint16_t* Hc, int64_t m_cap, const 
   return launch<false>(ASource{Hc, m_cap, d, nullptr, 0}, m_cap, m_dev, m_host, W, V_shard, d, p, stream);
 }
 
-extern "C" int mosaic_lmhead_stats_gather(const uint16_t* H, int64_t n_rows, int64_t ld_h, const int32_t* idx,
-                                          int32_t shift, int64_t m_cap, const int32_t* m_dev, int64_t m_host,
-                                          const uint16_t* W, int64_t V_shard, int64_t d, int64_t v_offset,
-                                          int32_t n_splits, float* part_max, float* part_sum, int32_t* part_arg,
-                                          void* stream) {
+namespace {
+int lmhead_stats_gather_impl(const uint16_t* H, int64_t n_rows, int64_t ld_h, const int32_t* idx, int32_t shift,
+                             int64_t m_cap, const int32_t* m_dev, int64_t m_host, const uint16_t* W,
+                             int64_t V_shard, int64_t d, int64_t v_offset, int32_t n_splits, float* part_max,
+                             float* part_sum, int32_t* part_arg, const uint8_t* die_of_sm, uint32_t* sched,
+                             void* stream) {
   MOSAIC_REQUIRE(H && idx && part_max && part_sum && part_arg, "null operands");
   MOSAIC_REQUIRE(n_rows >= 1 && n_rows < (int64_t(1) << 31), "n_rows out of range");
   const int64_t n_tiles = ceil_div(V_shard, BN);
@@ -781,8 +782,31 @@ extern "C" int mosaic_lmhead_stats_gather(const uint16_t* H, int64_t n_rows, int
   p.part_max = part_max;
   p.part_sum = part_sum;
   p.part_arg = part_arg;
+  p.die_of_sm = die_of_sm;
+  p.sched = sched;
   return launch<false>(ASource{H, n_rows, ld_h, idx, shift ? 1 : 0}, m_cap, m_dev, m_host, W, V_shard, d, p,
                        stream);
+}
+}  // namespace
+
+extern "C" int mosaic_lmhead_stats_gather(const uint16_t* H, int64_t n_rows, int64_t ld_h, const int32_t* idx,
+                                          int32_t shift, int64_t m_cap, const int32_t* m_dev, int64_t m_host,
+                                          const uint16_t* W, int64_t V_shard, int64_t d, int64_t v_offset,
+                                          int32_t n_splits, float* part_max, float* part_sum, int32_t* part_arg,
+                                          void* stream) {
+  return lmhead_stats_gather_impl(H, n_rows, ld_h, idx, shift, m_cap, m_dev, m_host, W, V_shard, d, v_offset,
+                                  n_splits, part_max, part_sum, part_arg, nullptr, nullptr, stream);
+}
+
+extern "C" int mosaic_lmhead_stats_gather_die(const uint16_t* H, int64_t n_rows, int64_t ld_h, const int32_t* idx,
+                                              int32_t shift, int64_t m_cap, const int32_t* m_dev, int64_t m_host,
+                                              const uint16_t* W, int64_t V_shard, int64_t d, int64_t v_offset,
+                                              int32_t n_splits, float* part_max, float* part_sum,
+                                              int32_t* part_arg, const uint8_t* die_of_sm, uint32_t* sched_scratch,
+                                              void* stream) {
+  MOSAIC_REQUIRE(die_of_sm && sched_scratch, "die-aware gather needs the die map and its 16-byte scratch");
+  return lmhead_stats_gather_impl(H, n_rows, ld_h, idx, shift, m_cap, m_dev, m_host, W, V_shard, d, v_offset,
+                                  n_splits, part_max, part_sum, part_arg, die_of_sm, sched_scratch, stream);
 }
 
 extern "C" int mosaic_lmhead_logits(const uint16_t* Hc, int64_t m_cap, const int32_t* m_dev,

@@ -333,7 +333,8 @@ class StepExecutor:
             if r1 > r0:
                 idx = side["mask_idx"][r0:r0 + cap]  # the chunk's positions (rows past r1 never stored)
                 hotpath.lmhead_stats_gather(h, idx, self.model.w_vocab, S, pm, ps, pa, cap, m_host=r1 - r0,
-                                            shift=self.shift, v_offset=self.model.vocab_offset)
+                                            shift=self.shift, v_offset=self.model.vocab_offset,
+                                            die_of_sm=self.die_table, sched=self._sched)
             self._last_splits = S
         elif kind == "sample":
             self._sample(op, g, v)

@@ -150,9 +150,12 @@ def lmhead_stats(hc: torch.Tensor, weight: torch.Tensor, n_splits: int, part_max
 
 def lmhead_stats_gather(hidden: torch.Tensor, idx: torch.Tensor, weight: torch.Tensor, n_splits: int,
                         part_max: torch.Tensor, part_sum: torch.Tensor, part_arg: torch.Tensor, m_cap: int,
-                        m_dev=None, m_host: int = 0, shift: bool = False, v_offset: int = 0, stream=None) -> None:
+                        m_dev=None, m_host: int = 0, shift: bool = False, v_offset: int = 0, stream=None,
+                        die_of_sm: Optional[torch.Tensor] = None, sched: Optional[torch.Tensor] = None) -> None:
     """K3 in gather mode: the A rows come straight from ``hidden`` [n, d] at
-    the masked positions ``idx`` (TMA gather4), no compacted buffer."""
+    the masked positions ``idx`` (cp.async loader warps), no compacted
+    buffer; ``die_of_sm``/``sched`` select the die-aware schedule as in
+    :func:`lmhead_stats`."""
     if hidden.dtype != torch.bfloat16 or hidden.dim() != 2 or hidden.stride(1) != 1 or not hidden.is_cuda:
         raise InputError("hidden must be a 2-D bf16 CUDA tensor with contiguous rows")
     _req(idx, torch.int32, "idx", 1)
@@ -167,6 +170,14 @@ def lmhead_stats_gather(hidden: torch.Tensor, idx: torch.Tensor, weight: torch.T
         _req(t, dt, n)
         if t.numel() < n_splits * m_cap:
             raise InputError(f"{n} must hold n_splits*m_cap entries")
+    if die_of_sm is not None:
+        if sched is None or sched.numel() * sched.element_size() < 16:
+            raise InputError("the die-aware schedule needs a 16-byte sched scratch")
+        _native.call("mosaic_lmhead_stats_gather_die", _p(hidden), hidden.shape[0], hidden.stride(0), _p(idx),
+                     int(bool(shift)), int(m_cap), _p(m_dev), int(m_host), _p(weight), weight.shape[0], d,
+                     int(v_offset), int(n_splits), _p(part_max), _p(part_sum), _p(part_arg), _p(die_of_sm),
+                     _p(sched), _s(stream))
+        return
     _native.call("mosaic_lmhead_stats_gather", _p(hidden), hidden.shape[0], hidden.stride(0), _p(idx),
                  int(bool(shift)), int(m_cap), _p(m_dev), int(m_host), _p(weight), weight.shape[0], d,
                  int(v_offset), int(n_splits), _p(part_max), _p(part_sum), _p(part_arg), _s(stream))
@@ -355,8 +366,7 @@ class MaskOnlyHead:
         self.shift = bool(shift)
         self.group = group
         self.fused_gather = bool(fused_gather)  # K3 reads rows of `hidden` directly: no K2, no hc buffer
-        self.die_table = (die_map(weight_shard.device)[0]
-                          if die_aware_default(die_aware) and not self.fused_gather else None)
+        self.die_table = die_map(weight_shard.device)[0] if die_aware_default(die_aware) else None
         if not (exchange in ("nccl", "p2p") or hasattr(exchange, "push")):
             raise InputError(f"exchange must be 'nccl', 'p2p' or a P2PExchange, got {exchange!r}")
         self.exchange = exchange
@@ -429,7 +439,8 @@ class MaskOnlyHead:
         if self.fused_gather:
             lmhead_stats_gather(hidden, b["idx"], self.weight, self.n_splits, b["part_max"], b["part_sum"],
                                 b["part_arg"], self.m_cap, m_dev=m_dev, shift=self.shift,
-                                v_offset=self.vocab_offset, stream=stream)
+                                v_offset=self.vocab_offset, stream=stream, die_of_sm=self.die_table,
+                                sched=b["sched"])
         else:
             gather_rows(hidden, b["idx"], b["hc"], m_dev=m_dev, shift=self.shift, stream=stream)
             lmhead_stats(b["hc"], self.weight, self.n_splits, b["part_max"], b["part_sum"],

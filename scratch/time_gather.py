@@ -21,6 +21,10 @@ def t(fn, n=5):
     torch.cuda.synchronize(); a.record()
     for _ in range(n): fn()
     b.record(); torch.cuda.synchronize(); return a.elapsed_time(b) / n
+die = hotpath.die_map(dev)[0]
+sched = torch.zeros(4, dtype=torch.int32, device=dev)
+print("die-aware: gather %.2f ms" % t(lambda: hotpath.lmhead_stats_gather(H, idx, W, S, pm, ps, pa, M, m_host=M, die_of_sm=die, sched=sched)),
+      "k2+k3 %.2f ms" % t(lambda: (hotpath.gather_rows(H, idx, hc, m_host=M), hotpath.lmhead_stats(hc, W, S, pm, ps, pa, m_host=M, die_of_sm=die, sched=sched))))
 print(os.environ.get("MOSAIC_CTA_GROUP"), os.environ.get("MOSAIC_K3_GATHER"),
       "gather %.2f ms" % t(lambda: hotpath.lmhead_stats_gather(H, idx, W, S, pm, ps, pa, M, m_host=M)),
       "k2+k3 %.2f ms" % t(lambda: (hotpath.gather_rows(H, idx, hc, m_host=M), hotpath.lmhead_stats(hc, W, S, pm, ps, pa, m_host=M))))

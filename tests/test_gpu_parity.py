@@ -355,9 +355,10 @@ def test_nccl_exchange_path_world1(dev):
                                                   (9000, 4096, 126464 // 8 + 5, 4500, "scattered", False),
                                                   (20000, 3584, 19008, 10000, "suffix", True)])
 def test_lmhead_gather_mode_equals_gathered_buffer(dev, L, d, V, m, layout, shift):
-    """K3 with the A operand gathered by TMA gather4 from H must be bit-identical
-    to K2 (gather into Hc) followed by the dense-A K3: same operands, same
-    MMA order, same epilogue."""
+    """K3 with the A operand gathered from H (cp.async loader warps) must be
+    bit-identical to K2 (gather into Hc) followed by the dense-A K3: same
+    operands, same MMA order, same epilogue -- also under the die-aware
+    schedule."""
     from paper_2601_06562_b200 import hotpath
 
     rng = np.random.default_rng(L + m)
@@ -371,7 +372,8 @@ def test_lmhead_gather_mode_equals_gathered_buffer(dev, L, d, V, m, layout, shif
     m_dev = torch.tensor([m], dtype=torch.int32, device=dev)
     S, _ = hotpath.lmhead_plan(cap, V, d)
     outs = []
-    for mode in ("buffer", "gather"):
+    table, _ = hotpath.die_map(dev)
+    for mode in ("buffer", "gather", "gather_die"):
         pm = torch.full((S, cap), 7.0, device=dev)
         ps = torch.full((S, cap), 7.0, device=dev)
         pa = torch.full((S, cap), -5, dtype=torch.int32, device=dev)
@@ -379,13 +381,18 @@ def test_lmhead_gather_mode_equals_gathered_buffer(dev, L, d, V, m, layout, shif
             hc = torch.zeros(cap, d, dtype=torch.bfloat16, device=dev)
             hotpath.gather_rows(H, idx_cap, hc, m_dev=m_dev, shift=shift)
             hotpath.lmhead_stats(hc, W, S, pm, ps, pa, m_dev=m_dev, v_offset=11)
-        else:
+        elif mode == "gather":
             hotpath.lmhead_stats_gather(H, idx_cap, W, S, pm, ps, pa, cap, m_dev=m_dev, shift=shift, v_offset=11)
+        else:
+            sched = torch.zeros(4, dtype=torch.int32, device=dev)
+            hotpath.lmhead_stats_gather(H, idx_cap, W, S, pm, ps, pa, cap, m_dev=m_dev, shift=shift, v_offset=11,
+                                        die_of_sm=table, sched=sched)
         torch.cuda.synchronize()
         outs.append((pm[:, :m].cpu(), ps[:, :m].cpu(), pa[:, :m].cpu(), pm[:, m:].cpu()))
-    for a, b in zip(outs[0][:3], outs[1][:3]):
-        assert torch.equal(a, b)
-    assert torch.all(outs[1][3] == 7.0)  # capacity rows untouched
+    for o in outs[1:]:
+        for a, b in zip(outs[0][:3], o[:3]):
+            assert torch.equal(a, b)
+        assert torch.all(o[3] == 7.0)  # capacity rows untouched
     # and against the oracle on the shifted/gathered rows
     src = np.maximum(pos - 1, 0) if shift else pos
     Hn = H.float().cpu().numpy().astype(np.float64)
