@@ -39,8 +39,17 @@ constexpr int kThreads = 192;    // warp0 TMA, warp1 MMA+TMEM, warps 2..5 epilog
 #ifndef MOSAIC_K3_AWARPS
 #define MOSAIC_K3_AWARPS 4  // measured: 4 >= 8 once the per-stage sync is CTA-scope
 #endif
+#ifndef MOSAIC_K3_GTMA_ROWS
+#define MOSAIC_K3_GTMA_ROWS 0  // gather mode: rows per CTA-stage fetched by TMA gather4 (rest by cp.async)
+#endif
 constexpr int kAWarps = MOSAIC_K3_AWARPS;  // cp.async gather path: A loader warps (warp 0 + warps 6..)
-constexpr int kRowsPerAWarp = BM / kAWarps;  // 16
+// Optionally the first kTmaRows rows of each CTA's 128 go through TMA gather4
+// ops issued beside the B box, the rest through the loader warps' cp.async.
+// Measured slower for every split (0/16/32/48 rows: 13.8/15.1/17.7/21.3 ms,
+// profiles/r01_k3_gather_modes.txt), so 0 by default.
+constexpr int kTmaRows = MOSAIC_K3_GTMA_ROWS;
+constexpr int kRowsPerAWarp = (BM - kTmaRows) / kAWarps;  // 32
+static_assert(kTmaRows % 4 == 0 && kTmaRows + kRowsPerAWarp * kAWarps == BM, "gather rows must tile the block");
 static_assert(kRowsPerAWarp % 4 == 0 && kRowsPerAWarp <= 32, "loader warp covers 4-row groups");
 constexpr int kThreadsCpAsync = kThreads + (kAWarps - 1) * 32;
 constexpr int kEpiWarps = 4;
@@ -305,36 +314,55 @@ __global__ void __launch_bounds__(kGather == kGatherCpAsync ? kThreadsCpAsync : 
         __syncwarp();
       }
       if constexpr (kGather == kGatherCpAsync) {
-        // kAWarps loader warps, kRowsPerAWarp rows each (warp 0 also issues the B tile). Lane
-        // copies 16-byte chunk (lane & 7) of rows (lane >> 3) + 4 i; the row
-        // sources are resolved once per unit and kept in registers.
+        // kAWarps loader warps, kRowsPerAWarp rows each after the first kTmaRows
+        // (warp 0 lane 0 also issues the B box and the gather4 ops of those
+        // rows). Lane copies 16-byte chunk (lane & 7) of rows (lane >> 3) + 4 i;
+        // the row sources are resolved once per unit and kept in registers.
         const int slot = warp == 0 ? 0 : warp - 5;
         const int chunk = lane & 7;
-        const int my_row = a_row + slot * kRowsPerAWarp + (lane % kRowsPerAWarp);
+        const int row0 = kTmaRows + slot * kRowsPerAWarp;  // this warp's first row in the CTA's block
+        const int my_row = a_row + row0 + (lane % kRowsPerAWarp);
         int src = my_row < M ? __ldg(p.idx + my_row) : 0;  // rows past M read row 0, never stored
         if (p.shift) src = max(src - 1, 0);
         int64_t off[kRowsPerAWarp / 4];
 #pragma unroll
         for (int i = 0; i < kRowsPerAWarp / 4; ++i)
           off[i] = static_cast<int64_t>(__shfl_sync(0xffffffffu, src, 4 * i + (lane >> 3))) * p.ld_h + chunk * 8;
-        const uint32_t row_dst = (slot * kRowsPerAWarp + (lane >> 3)) * (BK * 2);
+        int4 trow[kTmaRows / 4 > 0 ? kTmaRows / 4 : 1];
+        if (warp == 0 && lane == 0) {
+#pragma unroll
+          for (int i = 0; i < kTmaRows / 4; ++i) {
+            int v[4];
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+              const int r = a_row + 4 * i + j;
+              v[j] = r < M ? __ldg(p.idx + r) : 0;
+              if (p.shift) v[j] = max(v[j] - 1, 0);
+            }
+            trow[i] = make_int4(v[0], v[1], v[2], v[3]);
+          }
+        }
         for (int t = t0; t < t1; ++t) {
           const int b_row = t * BN + rank * C::B_ROWS;
           for (int kb = 0; kb < k_blocks; ++kb) {
             mbar_wait_sleep(&empty[stage], phase ^ 1, MOSAIC_K3_PROD_SLEEP_NS);
             if (warp == 0 && lane == 0) {
-              if (rank == 0) mbar_arrive_expect_tx(&full[stage], C::B_BYTES * CG);
+              if (rank == 0) mbar_arrive_expect_tx(&full[stage], (C::B_BYTES + kTmaRows * BK * 2) * CG);
               if constexpr (CG == 1)
                 tma_load_2d(sB + stage * C::B_BYTES, &tmap_b, &full[stage], kb * BK, b_row, pol_b);
               else
                 tma_load_2d_cg2(sB + stage * C::B_BYTES, &tmap_b, &full[stage], kb * BK, b_row, pol_b);
+#pragma unroll
+              for (int i = 0; i < kTmaRows / 4; ++i)
+                tma_gather4<CG>(sA + stage * C::A_BYTES + i * 4 * (BK * 2), &tmap_a, &full[stage], kb * BK,
+                                trow[i], pol_a);
             }
-            const uint32_t dst0 = smem_u32(sA + stage * C::A_BYTES) + row_dst;
+            const uint32_t dst0 = smem_u32(sA + stage * C::A_BYTES);
             const uint16_t* hk = p.h + static_cast<int64_t>(kb) * BK;
 #pragma unroll
             for (int i = 0; i < kRowsPerAWarp / 4; ++i) {
-              const int r = 4 * i + (lane >> 3);  // row within this warp's slice (same residue mod 8 as in the tile)
-              cp_async16(dst0 + 4 * i * (BK * 2) + ((chunk ^ (r & 7)) << 4), hk + off[i], pol_a);
+              const int r = row0 + 4 * i + (lane >> 3);  // row within the CTA's 128-row block
+              cp_async16(dst0 + r * (BK * 2) + ((chunk ^ (r & 7)) << 4), hk + off[i], pol_a);
             }
             cp_async_arrive_noinc(&afull[stage]);
             if (++stage == C::STAGES) {
