@@ -134,9 +134,18 @@ class StepExecutor:
         dev = torch.device("cuda", workspace.device)
         self.device = dev
         self._side: dict[int, dict] = {}
-        # K3's die-aware unit schedule (csrc/lmhead.cu), as in MaskOnlyHead
-        self.die_table = hotpath.die_map(dev)[0] if hotpath.die_aware_default(die_aware) else None
+        # K3's die-aware unit schedule (csrc/lmhead.cu), chosen per call by
+        # problem size as in MaskOnlyHead (hotpath.die_aware_default)
+        self._die_aware = die_aware
+        self._die_table = None
         self._sched = torch.zeros(4, dtype=torch.int32, device=dev)
+
+    def _die(self, m_cap: int):
+        if not hotpath.die_aware_default(self._die_aware, m_cap, self.model.w_vocab.shape[0]):
+            return None
+        if self._die_table is None:
+            self._die_table = hotpath.die_map(self.device)[0]
+        return self._die_table
 
     # ---------------------------------------------------------------- buffers
     def _side_buffers(self, L: int) -> dict:
@@ -317,7 +326,7 @@ class StepExecutor:
             pa = flat[2 * S * cap: 3 * S * cap].view(torch.int32).view(S, cap)
             if r1 > r0:
                 hotpath.lmhead_stats(hc, self.model.w_vocab, S, pm, ps, pa, m_host=r1 - r0,
-                                     v_offset=self.model.vocab_offset, die_of_sm=self.die_table,
+                                     v_offset=self.model.vocab_offset, die_of_sm=self._die(cap),
                                      sched=self._sched)
             self._last_splits = S
         elif kind == "lmhead_stats_gather":  # K3 gather mode: A rows read from h at mask_idx
@@ -334,7 +343,7 @@ class StepExecutor:
                 idx = side["mask_idx"][r0:r0 + cap]  # the chunk's positions (rows past r1 never stored)
                 hotpath.lmhead_stats_gather(h, idx, self.model.w_vocab, S, pm, ps, pa, cap, m_host=r1 - r0,
                                             shift=self.shift, v_offset=self.model.vocab_offset,
-                                            die_of_sm=self.die_table, sched=self._sched)
+                                            die_of_sm=self._die(cap), sched=self._sched)
             self._last_splits = S
         elif kind == "sample":
             self._sample(op, g, v)

@@ -113,13 +113,20 @@ def die_map(device=None) -> tuple[torch.Tensor, dict]:
     return _DIE_MAPS[dev.index]
 
 
-def die_aware_default(die_aware: Optional[bool] = None) -> bool:
-    """K3's die-aware unit schedule: on unless disabled (argument, or
-    MOSAIC_DIE_AWARE=0). Measured on B200 (profiles/r01h_k3_die_aware.txt):
-    DRAM per launch 6.2-6.7 GB vs 10.8-11.1 GB, +2-2.5% steady throughput."""
+def die_aware_default(die_aware: Optional[bool] = None, m_cap: int = 0, v_shard: int = 0) -> bool:
+    """Whether K3 takes the die-aware unit schedule. An explicit argument or
+    MOSAIC_DIE_AWARE=0/1 decides; otherwise it is on for large problems
+    (m_cap >= 4096 rows and a vocab shard >= 32768), where it was measured
+    faster (profiles/r01h_k3_die_aware.txt, r01h_kernels_die.json: Dream K3
+    -11%, MoE -3%, LLaDA steady step +2%), and off for small ones, where its
+    launch-time registration and the split's locality do not pay (tiny
+    +6 us, LLaDA 1/8 vocab shard +6%)."""
     if die_aware is not None:
         return bool(die_aware)
-    return os.environ.get("MOSAIC_DIE_AWARE", "1") != "0"
+    env = os.environ.get("MOSAIC_DIE_AWARE")
+    if env in ("0", "1"):
+        return env == "1"
+    return m_cap >= 4096 and v_shard >= 32768
 
 
 def lmhead_stats(hc: torch.Tensor, weight: torch.Tensor, n_splits: int, part_max: torch.Tensor,
@@ -366,7 +373,8 @@ class MaskOnlyHead:
         self.shift = bool(shift)
         self.group = group
         self.fused_gather = bool(fused_gather)  # K3 reads rows of `hidden` directly: no K2, no hc buffer
-        self.die_table = die_map(weight_shard.device)[0] if die_aware_default(die_aware) else None
+        self.die_table = (die_map(weight_shard.device)[0]
+                          if die_aware_default(die_aware, self.m_cap, self.v_shard) else None)
         if not (exchange in ("nccl", "p2p") or hasattr(exchange, "push")):
             raise InputError(f"exchange must be 'nccl', 'p2p' or a P2PExchange, got {exchange!r}")
         self.exchange = exchange
