@@ -81,9 +81,12 @@ def shard_times(M, d, V, dev):
         tok = torch.empty(M, dtype=torch.int32, device=dev)
         lse = torch.empty(M, device=dev)
         conf = torch.empty(M, device=dev)
+        # the schedule MaskOnlyHead would pick for this rank's shard
+        die = hotpath.die_map(dev)[0] if hotpath.die_aware_default(None, M, v) else None
+        sched = torch.zeros(4, dtype=torch.int32, device=dev)
 
         def step():
-            hotpath.lmhead_stats(hc, Ws, S, pm, ps, pa, m_host=M)
+            hotpath.lmhead_stats(hc, Ws, S, pm, ps, pa, m_host=M, die_of_sm=die, sched=sched)
             hotpath.stats_merge(pm, ps, pa, S, M, M, m_host=M, token=tok, lse=lse, conf=conf)
 
         for _ in range(2):
@@ -95,7 +98,8 @@ def shard_times(M, d, V, dev):
         b.record()
         torch.cuda.synchronize()
         ms = a.elapsed_time(b) / 3
-        out[f"P{P}"] = {"vocab_shard": v, "k3_k4_ms": ms, "tflops": 2.0 * M * d * v / ms / 1e9}
+        out[f"P{P}"] = {"vocab_shard": v, "k3_k4_ms": ms, "tflops": 2.0 * M * d * v / ms / 1e9,
+                        "k3_schedule": "die-aware" if die is not None else "default"}
     return out
 
 
