@@ -13,8 +13,9 @@ x = rng.integers(0, V - 1, size=L).astype(np.int32); x[rng.random(L) < 0.5] = mi
 H = torch.from_numpy(rng.standard_normal((L, d)).astype(np.float32)).to(dev).bfloat16()
 W = torch.from_numpy((rng.standard_normal((V, d)) * 0.05).astype(np.float32)).to(dev).bfloat16()
 for fg in (False, True):
-    head = MaskOnlyHead(W, seq_len=L, mask_id=mid, shift=True, fused_gather=fg)
-    head.step(torch.from_numpy(x).to(dev), H, 50)
+    for da in (False, True):  # default and die-aware unit schedules (registration + decision prologue)
+        head = MaskOnlyHead(W, seq_len=L, mask_id=mid, shift=True, fused_gather=fg, die_aware=da)
+        head.step(torch.from_numpy(x).to(dev), H, 50)
 head = MaskOnlyHead(W, seq_len=L, mask_id=mid, m_cap=100)  # M <= 128 -> cta_group::1
 xs = x.copy(); xs[:] = 1; xs[:90] = mid
 head.step(torch.from_numpy(xs).to(dev), H, 10)
