@@ -57,6 +57,9 @@ constexpr int kMaxSplits = 64;
 #ifndef MOSAIC_K3_EPI_SLEEP_NS
 #define MOSAIC_K3_EPI_SLEEP_NS 0   // epilogue poll backoff while the next accumulator fills
 #endif
+#ifndef MOSAIC_K3_DUP_B
+#define MOSAIC_K3_DUP_B 0  // experiment: also load every W tile a second time into a scratch slot (L2 feed cost)
+#endif
 #ifndef MOSAIC_K3_GFENCE
 #define MOSAIC_K3_GFENCE 1  // gather mode: proxy fence per stage (0 = none, experiment)
 #endif
@@ -80,7 +83,8 @@ struct Cfg {
 #define MOSAIC_K3_STAGES2 6
 #endif
   static constexpr int STAGES = CG == 1 ? 4 : MOSAIC_K3_STAGES2;
-  static constexpr int SMEM = STAGES * STAGE_BYTES + 1024 + 256 + BM * 4 + 16;  // + gather rows, die schedule
+  static constexpr int SMEM = STAGES * STAGE_BYTES + 1024 + 256 + BM * 4 + 16  // + gather rows, die schedule
+                              + (MOSAIC_K3_DUP_B ? 1024 + B_BYTES : 0);         // experiment: duplicate W reads
   static constexpr uint32_t IDESC = umma_idesc_bf16(ROWS, BN);
 };
 
@@ -376,11 +380,21 @@ __global__ void __launch_bounds__(kGather == kGatherCpAsync ? kThreadsCpAsync : 
           const int b_row = t * BN + rank * C::B_ROWS;
           for (int kb = 0; kb < k_blocks; ++kb) {
             mbar_wait_sleep(&empty[stage], phase ^ 1, MOSAIC_K3_PROD_SLEEP_NS);
-            if (rank == 0) mbar_arrive_expect_tx(&full[stage], C::STAGE_BYTES * CG);
+            if (rank == 0)
+              mbar_arrive_expect_tx(&full[stage], (C::STAGE_BYTES + (MOSAIC_K3_DUP_B ? C::B_BYTES : 0)) * CG);
             if constexpr (CG == 1)
               tma_load_2d(sB + stage * C::B_BYTES, &tmap_b, &full[stage], kb * BK, b_row, pol_b);
             else
               tma_load_2d_cg2(sB + stage * C::B_BYTES, &tmap_b, &full[stage], kb * BK, b_row, pol_b);
+            if (MOSAIC_K3_DUP_B) {  // same W box again into a slot nobody reads (L2 -> SM feed experiment)
+              uint8_t* dup = reinterpret_cast<uint8_t*>(
+                  (reinterpret_cast<uintptr_t>(smem + C::STAGES * C::STAGE_BYTES + 256 + BM * 4 + 16) + 1023) &
+                  ~static_cast<uintptr_t>(1023));
+              if constexpr (CG == 1)
+                tma_load_2d(dup, &tmap_b, &full[stage], kb * BK, b_row, pol_b);
+              else
+                tma_load_2d_cg2(dup, &tmap_b, &full[stage], kb * BK, b_row, pol_b);
+            }
             if constexpr (kGather == kGatherTma4) {
               const uint32_t rows_addr = smem_u32(sidx);
 #pragma unroll 4
@@ -648,7 +662,8 @@ int launch_cg(const CUtensorMap& ta, const CUtensorMap& tb, const Params& p, int
     attr_set = true;
   }
   const int64_t units_cap = ceil_div(m_cap, C::ROWS) * p.n_splits;
-  const int64_t workers = num_sms() / CG;
+  static const int max_clusters = env_int("MOSAIC_K3_MAX_CLUSTERS", 0);  // experiment: fewer SMs
+  const int64_t workers = max_clusters > 0 ? std::min<int64_t>(max_clusters, num_sms() / CG) : num_sms() / CG;
   const int64_t clusters = units_cap < workers ? units_cap : workers;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(static_cast<unsigned>(clusters * CG));
