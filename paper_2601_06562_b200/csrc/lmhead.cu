@@ -57,6 +57,9 @@ constexpr int kMaxSplits = 64;
 #ifndef MOSAIC_K3_EPI_SLEEP_NS
 #define MOSAIC_K3_EPI_SLEEP_NS 0   // epilogue poll backoff while the next accumulator fills
 #endif
+#ifndef MOSAIC_K3_HALF_A
+#define MOSAIC_K3_HALF_A 0  // experiment only (wrong results): skip A loads on odd tiles
+#endif
 #ifndef MOSAIC_K3_DUP_B
 #define MOSAIC_K3_DUP_B 0  // experiment: also load every W tile a second time into a scratch slot (L2 feed cost)
 #endif
@@ -380,8 +383,12 @@ __global__ void __launch_bounds__(kGather == kGatherCpAsync ? kThreadsCpAsync : 
           const int b_row = t * BN + rank * C::B_ROWS;
           for (int kb = 0; kb < k_blocks; ++kb) {
             mbar_wait_sleep(&empty[stage], phase ^ 1, MOSAIC_K3_PROD_SLEEP_NS);
+            // MOSAIC_K3_HALF_A (experiment, wrong results): skip the A load on odd tiles to
+            // measure what halving A's L2 feed (as A multicast across two pairs would) buys
+            const bool load_a = !(MOSAIC_K3_HALF_A && (t & 1));
             if (rank == 0)
-              mbar_arrive_expect_tx(&full[stage], (C::STAGE_BYTES + (MOSAIC_K3_DUP_B ? C::B_BYTES : 0)) * CG);
+              mbar_arrive_expect_tx(&full[stage], (C::STAGE_BYTES - (load_a ? 0 : C::A_BYTES) +
+                                                   (MOSAIC_K3_DUP_B ? C::B_BYTES : 0)) * CG);
             if constexpr (CG == 1)
               tma_load_2d(sB + stage * C::B_BYTES, &tmap_b, &full[stage], kb * BK, b_row, pol_b);
             else
@@ -407,9 +414,9 @@ __global__ void __launch_bounds__(kGather == kGatherCpAsync ? kThreadsCpAsync : 
                                 r4, pol_a);
               }
             } else if constexpr (CG == 1) {
-              tma_load_2d(sA + stage * C::A_BYTES, &tmap_a, &full[stage], kb * BK, a_row, pol_a);
+              if (load_a) tma_load_2d(sA + stage * C::A_BYTES, &tmap_a, &full[stage], kb * BK, a_row, pol_a);
             } else {
-              tma_load_2d_cg2(sA + stage * C::A_BYTES, &tmap_a, &full[stage], kb * BK, a_row, pol_a);
+              if (load_a) tma_load_2d_cg2(sA + stage * C::A_BYTES, &tmap_a, &full[stage], kb * BK, a_row, pol_a);
             }
             if (++stage == C::STAGES) {
               stage = 0;
