@@ -5,9 +5,9 @@
 // Reference counterpart: gather_gemm (mosaic/kernel.py:62-86) computes
 // logits[i, :] = H[mask_idx[i], :] @ W and materialises [m, V] (:68); the
 // `sample` op that consumes them is memory-only (mosaic/workload.py:306-308).
-// Here the gathered rows Hc (K2) -- or, in gather mode, the rows of H itself --
-// and the vocab shard W [V, d] (K-major) stream through TMA into a shared-memory
-// ring; one elected thread issues tcgen05.mma (BF16 -> FP32 in TMEM) and four
+// Here the gathered rows Hc (K2) and the vocab shard W [V, d] (K-major) stream
+// through TMA into a shared-memory ring (in gather mode the A rows come from H
+// itself through cp.async loader warps); one elected thread issues tcgen05.mma (BF16 -> FP32 in TMEM) and four
 // epilogue warps drain a double-buffered TMEM accumulator with tcgen05.ld while
 // the next tile's MMAs run. Default cta_group::2: a CTA pair computes 256 x 256
 // tiles (UMMA M=256, N=256, K=16) out of a 6-stage ring; cta_group::1 (128 x 256,
@@ -103,7 +103,7 @@ struct Params {
   int32_t group_m;
   int32_t seg_splits;  // vocab segments of this many splits, processed segment-major (0 = one segment)
   const uint8_t* die_of_sm;  // die-aware schedule: SM -> L2 die (null = off)
-  uint32_t* sched;           // die-aware schedule: [die0 pairs, die1 pairs, arrived], zeroed per launch
+  uint32_t* sched;           // die-aware schedule: [die0 pairs, die1 pairs, registered, decision], zeroed per launch
   int32_t policy;   // L2 policy of (A, B) loads: 0 = (evict_normal, evict_normal), 1 = (evict_last, evict_normal), 2 = (evict_normal, evict_first)
   int64_t v_offset;
   float* part_max;
