@@ -472,7 +472,9 @@ class MaskOnlyHead:
                         out_max=loc[0], out_sum=loc[1], out_arg=loc[2].view(torch.int32),
                         stream=stream)
             g = b["gathered"]
-            exchange_triples(loc, group=self.group, out=g)  # NCCL all-gather, 12 B/row/rank
+            # NCCL orders its collective after torch's current stream: make that the step's stream
+            with torch.cuda.stream(stream if stream is not None else torch.cuda.current_stream()):
+                exchange_triples(loc, group=self.group, out=g)  # NCCL all-gather, 12 B/row/rank
             stats_merge(g[0, 0], g[0, 1], g[0, 2].view(torch.int32), self.world, 3 * m, m,
                         m_dev=m_dev, token=b["token"], lse=b["lse"], conf=b["conf"], stream=stream)
         remask_commit(b["conf"], b["idx"], b["token"], int(k), x, b["remask_scratch"], m,
