@@ -139,6 +139,9 @@ class StepExecutor:
         self._die_aware = die_aware
         self._die_table = None
         self._sched = torch.zeros(4, dtype=torch.int32, device=dev)
+        if hotpath.die_aware_default(die_aware, 1 << 30, model.w_vocab.shape[0]):
+            # measured now (a one-off probe with ~250 MB of scratch), not mid-step next to a full arena
+            self._die_table = hotpath.die_map(dev)[0]
 
     def _die(self, m_cap: int):
         if not hotpath.die_aware_default(self._die_aware, m_cap, self.model.w_vocab.shape[0]):
