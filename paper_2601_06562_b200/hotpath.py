@@ -100,7 +100,10 @@ _DIE_MAPS: dict = {}
 def die_map(device=None) -> tuple[torch.Tensor, dict]:
     """The measured SM -> L2-die map of ``device`` (cached per process): a
     device uint8 tensor [num SMs] for K3's die-aware schedule, plus counts."""
-    dev = torch.device("cuda", torch.cuda.current_device() if device is None else torch.device(device).index or 0)
+    if device is None or torch.device(device).index is None:
+        dev = torch.device("cuda", torch.cuda.current_device())
+    else:
+        dev = torch.device("cuda", torch.device(device).index)
     if dev.index not in _DIE_MAPS:
         n_sm = torch.cuda.get_device_properties(dev).multi_processor_count
         scratch = torch.empty(int(_native.value("mosaic_die_map_scratch_bytes", n_sm)), dtype=torch.uint8, device=dev)
@@ -110,6 +113,8 @@ def die_map(device=None) -> tuple[torch.Tensor, dict]:
             _native.call("mosaic_die_map", host, n_sm, _p(scratch), ctypes.byref(n0), ctypes.byref(amb), _s(None))
         table = torch.tensor(list(host), dtype=torch.uint8, device=dev)
         _DIE_MAPS[dev.index] = (table, {"n_sm": n_sm, "die0_sms": n0.value, "ambiguous": amb.value})
+        del scratch  # ~2x L2 of probe scratch: hand it back to the driver, not to torch's cache
+        torch.cuda.empty_cache()
     return _DIE_MAPS[dev.index]
 
 
