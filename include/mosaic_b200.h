@@ -168,14 +168,17 @@ MOSAIC_API int mosaic_stats_merge(const float* in_max, const float* in_sum, cons
 /* ---------------------------------------------------------------- K4x -----
  * Vocab-shard exchange fused into the split merge, over NVLink peer memory:
  * push merges the S split triples of every row r < M (K4 rule) and stores the
- * merged (max, sum, arg-bits) into slot [rank] of every rank's gathered
- * buffer [world][3][m_cap] fp32 (peer_gathered: device array of `world`
- * pointers), then publishes `epoch` into every rank's signal pad slot [rank]
- * (peer_signal: device array of `world` uint32 pointers; release.sys);
- * wait blocks the stream until the local pad's `world` slots equal `epoch`
- * (acquire.sys, bounded: traps if a peer never arrives). Then
- * mosaic_stats_merge(gathered, S=world, stride=3*m_cap) finalises. Replaces
- * K4 + all-gather + K4 of the NCCL path. done_counter: one local uint32, 0. */
+ * merged (max, sum, arg-bits) into slot [epoch & 1][rank] of every rank's
+ * double-buffered gathered block [2][world][3][m_cap] fp32 (peer_gathered:
+ * device array of `world` pointers to those blocks), then publishes `epoch`
+ * into every rank's signal pad slot [rank] (peer_signal: device array of
+ * `world` uint32 pointers; release.sys); wait blocks the stream until the
+ * local pad's `world` slots equal `epoch` (acquire.sys, bounded: traps if a
+ * peer never arrives). Then mosaic_stats_merge over half (epoch & 1) of the
+ * local block (S=world, stride=3*m_cap) finalises. Alternating halves keep a
+ * rank that is one step ahead from overwriting triples a peer has not merged.
+ * Replaces K4 + all-gather + K4 of the NCCL path. done_counter: one local
+ * uint32, 0. epoch: 1, 2, 3, ... (never 0, the pads' initial value).      */
 MOSAIC_API int mosaic_stats_exchange_push(const float* in_max, const float* in_sum, const int32_t* in_arg,
                                int32_t S, int64_t stride, const int32_t* m_dev, int64_t m_host,
                                int64_t m_cap, float* const* peer_gathered, uint32_t* const* peer_signal,

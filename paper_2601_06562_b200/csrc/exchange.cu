@@ -3,8 +3,8 @@
 // the per-row triples -> K4 rank merge" by
 //
 //   push:  each row's S split triples are merged (the K4 rule) and the merged
-//          (max, sum, argmax) is stored straight into slot [rank] of EVERY
-//          rank's gathered buffer [P][3][m_cap] through its peer pointer
+//          (max, sum, argmax) is stored straight into slot [epoch & 1][rank] of
+//          EVERY rank's gathered buffer [2][P][3][m_cap] through its peer pointer
 //          (st.global over NVLink); the last CTA to finish publishes `epoch`
 //          into every rank's signal pad slot [rank] (release, system scope);
 //   wait:  one CTA spins until all P slots of the local signal pad carry
@@ -58,7 +58,12 @@ __global__ void __launch_bounds__(256)
         sum += si * expf(mi - m);
       }
     }
-    const int64_t slot = static_cast<int64_t>(rank) * 3 * m_cap + r;
+    // half (epoch & 1) of the double-buffered [2][P][3][m_cap] gathered block:
+    // a rank can be at most one step ahead of a peer's merge (its next push
+    // needs every rank's signal of this step, which each rank gives only after
+    // merging the previous one), so alternating halves rules out overwriting
+    // triples a slower peer has not merged yet
+    const int64_t slot = (static_cast<int64_t>(epoch & 1u) * world + rank) * 3 * m_cap + r;
     for (int p = 0; p < world; ++p) {  // peer stores over NVLink (p == rank: local)
       float* g = peer_gathered[p];
       g[slot] = m;

@@ -466,7 +466,7 @@ class MaskOnlyHead:
         elif self.p2p is not None:  # K4x: merge + peer stores + signal, then wait; no NCCL call
             self.p2p.push(b["part_max"], b["part_sum"], b["part_arg"], S, m, m_dev=m_dev, stream=stream)
             self.p2p.wait(stream)
-            g = self.p2p.gathered
+            g = self.p2p.current
             stats_merge(g[0, 0], g[0, 1], g[0, 2].view(torch.int32), self.world, 3 * m, m,
                         m_dev=m_dev, token=b["token"], lse=b["lse"], conf=b["conf"], stream=stream)
         else:

@@ -43,18 +43,19 @@ def exchange_triples(local: torch.Tensor, group=None, out: torch.Tensor | None =
 
 class P2PExchange:
     """The exchange fused into the split merge over NVLink peer memory (K4x,
-    csrc/exchange.cu): symmetric ``gathered`` [P, 3, m] fp32 and ``signal`` [P]
-    uint32 buffers (torch symmetric memory), their peers' device pointers, and
-    a per-step epoch. ``push`` merges this rank's S split triples per row and
-    stores them into every rank's gathered slot [rank], then signals; ``wait``
-    blocks the stream until every rank has signalled this epoch. No NCCL call
-    on the step path."""
+    csrc/exchange.cu): symmetric ``gathered`` [2, P, 3, m] fp32 (double-buffered
+    by epoch parity) and ``signal`` [P] uint32 buffers (torch symmetric memory),
+    their peers' device pointers, and a per-step epoch. ``push`` merges this
+    rank's S split triples per row and stores them into every rank's gathered
+    slot [epoch & 1, rank], then signals; ``wait`` blocks the stream until every
+    rank has signalled this epoch; :attr:`current` is the half to merge. No
+    NCCL call on the step path."""
 
     def __init__(self, m_cap: int, group, device):
         import torch.distributed._symmetric_memory as symm_mem
 
         world, rank = dist.get_world_size(group), dist.get_rank(group)
-        gathered = symm_mem.empty((world, 3, int(m_cap)), dtype=torch.float32, device=device)
+        gathered = symm_mem.empty((2, world, 3, int(m_cap)), dtype=torch.float32, device=device)
         signal = symm_mem.empty((world,), dtype=torch.int32, device=device)
         signal.zero_()
         torch.cuda.synchronize(device)
@@ -67,13 +68,15 @@ class P2PExchange:
     def from_buffers(cls, gathered: torch.Tensor, signal: torch.Tensor, peer_gathered: list, peer_signal: list,
                      rank: int, world: int) -> "P2PExchange":
         """Peers given as raw device pointers (e.g. CUDA-IPC mappings of the
-        other processes' buffers); ``signal`` must be zeroed on every rank
-        before the first push."""
+        other processes' [2, P, 3, m] gathered blocks); ``signal`` must be
+        zeroed on every rank before the first push."""
         self = cls.__new__(cls)
         self._init(gathered, signal, peer_gathered, peer_signal, rank, world)
         return self
 
     def _init(self, gathered, signal, peer_gathered, peer_signal, rank, world):
+        if gathered.dim() != 4 or gathered.shape[0] != 2 or gathered.shape[1] != world or gathered.shape[2] != 3:
+            raise ValueError("gathered must be [2, world, 3, m_cap] fp32 (double-buffered by epoch parity)")
         device = gathered.device
         self.world, self.rank, self.m_cap = int(world), int(rank), int(gathered.shape[-1])
         self.gathered, self.signal = gathered, signal
@@ -81,6 +84,11 @@ class P2PExchange:
         self._peer_signal = torch.tensor([int(p) for p in peer_signal], dtype=torch.int64, device=device)
         self._done = torch.zeros(1, dtype=torch.int32, device=device)
         self.epoch = 0
+
+    @property
+    def current(self) -> torch.Tensor:
+        """[P, 3, m] half of ``gathered`` written by the latest push."""
+        return self.gathered[self.epoch & 1]
 
     def push(self, part_max, part_sum, part_arg, S: int, stride: int, m_dev=None, m_host: int = 0, stream=None):
         import ctypes

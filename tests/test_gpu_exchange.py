@@ -93,7 +93,7 @@ def test_p2p_exchange_two_ranks_one_gpu(native_lib):
     dev = torch.device("cuda", 0)
     L, V, mask_id, k, x, H, W = _problem(dev)
     world = 2
-    gathered = [torch.zeros(world, 3, L, device=dev) for _ in range(world)]
+    gathered = [torch.zeros(2, world, 3, L, device=dev) for _ in range(world)]
     signal = [torch.zeros(world, dtype=torch.int32, device=dev) for _ in range(world)]
     torch.cuda.synchronize()
     ctx = mp.get_context("spawn")
