@@ -623,8 +623,13 @@ void plan_splits(int64_t m_cap, int64_t V, int32_t* n_splits, int32_t* tps) {
   const int64_t m_blocks = ceil_div(m_cap > 0 ? m_cap : 1, BM * cg);
   const int64_t workers = num_sms() / cg;
   int64_t best_cost = INT64_MAX, best_tps = n_tiles;
+  // Split cap: kMaxSplits bounds the [S][m_cap] partials for large M; with a
+  // single row block (M <= 256, e.g. semi-autoregressive block decoding) the
+  // splits are the only parallelism and the launch streams the whole W shard,
+  // so the cap rises to one split per worker (profiles/r01h_k3_small_m.txt).
+  const int64_t max_splits = std::max<int64_t>(kMaxSplits, ceil_div(workers, m_blocks));
   static const int forced_tps = env_int("MOSAIC_K3_TPS", 0);  // schedule experiments only
-  if (forced_tps > 0 && ceil_div(n_tiles, std::min<int64_t>(forced_tps, n_tiles)) <= kMaxSplits) {
+  if (forced_tps > 0 && ceil_div(n_tiles, std::min<int64_t>(forced_tps, n_tiles)) <= max_splits) {
     *tps = static_cast<int32_t>(std::min<int64_t>(forced_tps, n_tiles));
     *n_splits = static_cast<int32_t>(ceil_div(n_tiles, *tps));
     return;
@@ -638,14 +643,14 @@ void plan_splits(int64_t m_cap, int64_t V, int32_t* n_splits, int32_t* tps) {
   auto cost_of = [&](int64_t t) { return ceil_div(m_blocks * ceil_div(n_tiles, t), workers) * t; };
   for (int64_t t = n_tiles; t >= 1; --t) {
     const int64_t S = ceil_div(n_tiles, t);
-    if (S > kMaxSplits) break;
+    if (S > max_splits) break;
     if (ceil_div(n_tiles, S) != t) continue;  // same split count as a larger t
     best_cost = std::min(best_cost, cost_of(t));
   }
   int64_t best_dist = INT64_MAX;
   for (int64_t t = n_tiles; t >= 1; --t) {
     const int64_t S = ceil_div(n_tiles, t);
-    if (S > kMaxSplits) break;
+    if (S > max_splits) break;
     if (ceil_div(n_tiles, S) != t) continue;
     if (cost_of(t) * 1000 > best_cost * 1005) continue;
     const int64_t dist = t > kPreferTps ? t - kPreferTps : kPreferTps - t;

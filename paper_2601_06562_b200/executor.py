@@ -321,7 +321,7 @@ class StepExecutor:
             r0, r1 = _rows(M, b["K_logits"], op.iteration)
             hc, buf = v[op.inputs[0]], v[op.outputs[0]]
             cap = hc.shape[0]
-            S, _ = hotpath.lmhead_plan(cap, self.model.w_vocab.shape[0], d)
+            S, _ = hotpath.lmhead_plan(cap, self.model.w_vocab.shape[0], d, max_splits=buf.shape[1] // 3)
             if 3 * S > buf.shape[1]:
                 raise InputError(f"K3 wants {S} splits but the template reserved {buf.shape[1] // 3}")
             flat = buf.view(-1)
@@ -336,7 +336,7 @@ class StepExecutor:
             r0, r1 = _rows(M, b["K_logits"], op.iteration)
             h, buf = v[op.inputs[0]], v[op.outputs[0]]
             cap = buf.shape[0]
-            S, _ = hotpath.lmhead_plan(cap, self.model.w_vocab.shape[0], d)
+            S, _ = hotpath.lmhead_plan(cap, self.model.w_vocab.shape[0], d, max_splits=buf.shape[1] // 3)
             if 3 * S > buf.shape[1]:
                 raise InputError(f"K3 wants {S} splits but the template reserved {buf.shape[1] // 3}")
             flat = buf.view(-1)

@@ -87,11 +87,19 @@ def gather_rows(hidden: torch.Tensor, idx: torch.Tensor, out: torch.Tensor, m_de
 
 
 # ----------------------------------------------------------------- K3
-def lmhead_plan(m_cap: int, v_shard: int, d: int) -> tuple[int, int]:
+def lmhead_plan(m_cap: int, v_shard: int, d: int, max_splits: Optional[int] = None) -> tuple[int, int]:
+    """(n_splits, tiles_per_split) for K3 (mosaic_lmhead_plan). With
+    ``max_splits`` (e.g. a graph template's reserved partial width) the split
+    is coarsened to at most that many splits, still tiling the vocab evenly."""
     s = ctypes.c_int32()
     t = ctypes.c_int32()
     _native.call("mosaic_lmhead_plan", m_cap, v_shard, d, ctypes.byref(s), ctypes.byref(t))
-    return s.value, t.value
+    S, tps = s.value, t.value
+    if max_splits is not None and S > max_splits:
+        n_tiles = -(-int(v_shard) // 256)
+        tps = -(-n_tiles // int(max_splits))
+        S = -(-n_tiles // tps)
+    return S, tps
 
 
 _DIE_MAPS: dict = {}
