@@ -246,6 +246,12 @@ def gpu_main(args):
     if persist:
         from paper_2601_06562_b200 import hotpath as _hp
         _hp.l2_persisting_limit(persist)
+    if os.environ.get("MOSAIC_K3_WBLOCKED") == "1":  # experiment: W pre-tiled so each TMA box is contiguous
+        n_t = -(-(v1 - v0) // 256)
+        Wp = torch.zeros((n_t * 256, D), device=dev, dtype=torch.bfloat16)
+        Wp[: v1 - v0] = W
+        W = Wp.view(n_t, 256, D // 64, 64).permute(0, 2, 1, 3).contiguous().view(n_t * 256, D)
+        del Wp
     head = MaskOnlyHead(W, seq_len=SEQ, mask_id=MASK_ID, vocab_offset=v0, m_cap=M, group=group,
                         exchange=args.exchange)
     stream = torch.cuda.current_stream()

@@ -115,6 +115,7 @@ struct Params {
   const uint16_t* h;   // gather mode: H base (cp.async path)
   int64_t ld_h;        // gather mode: H row stride (elements)
   int32_t shift;       // gather mode: src(p) = max(p - 1, 0) (Dream token shift)
+  int32_t w_blocked;   // W pre-tiled as [n_tiles][K/64][256][64] (each TMA box contiguous)
 };
 
 // Unit order: vocab segments of `seg_splits` consecutive splits, outermost;
@@ -136,6 +137,18 @@ __device__ __forceinline__ void unit_coords(const Params& p, int m_blocks, int64
   const int64_t gm = min(static_cast<int64_t>(p.group_m), m_blocks - g * p.group_m);
   s = static_cast<int>(seg * seg_splits + rem / gm);
   mb = static_cast<int>(g * p.group_m + rem % gm);
+}
+
+// TMA coordinates (col, row) of this CTA's W box for vocab tile t, k-block kb.
+__device__ __forceinline__ void w_box(const Params& p, int t, int kb, int k_blocks, int b_rows_off, int& col,
+                                      int& row) {
+  if (p.w_blocked) {
+    col = 0;
+    row = (t * k_blocks + kb) * BN + b_rows_off;
+  } else {
+    col = kb * BK;
+    row = t * BN + b_rows_off;
+  }
 }
 
 __device__ __forceinline__ float fast_exp2(float x) {
@@ -350,15 +363,17 @@ __global__ void __launch_bounds__(kGather == kGatherCpAsync ? kThreadsCpAsync : 
           }
         }
         for (int t = t0; t < t1; ++t) {
-          const int b_row = t * BN + rank * C::B_ROWS;
+          const int b_row_off = rank * C::B_ROWS;
           for (int kb = 0; kb < k_blocks; ++kb) {
             mbar_wait_sleep(&empty[stage], phase ^ 1, MOSAIC_K3_PROD_SLEEP_NS);
+            int bc, br;
+            w_box(p, t, kb, k_blocks, b_row_off, bc, br);
             if (warp == 0 && lane == 0) {
               if (rank == 0) mbar_arrive_expect_tx(&full[stage], (C::B_BYTES + kTmaRows * BK * 2) * CG);
               if constexpr (CG == 1)
-                tma_load_2d(sB + stage * C::B_BYTES, &tmap_b, &full[stage], kb * BK, b_row, pol_b);
+                tma_load_2d(sB + stage * C::B_BYTES, &tmap_b, &full[stage], bc, br, pol_b);
               else
-                tma_load_2d_cg2(sB + stage * C::B_BYTES, &tmap_b, &full[stage], kb * BK, b_row, pol_b);
+                tma_load_2d_cg2(sB + stage * C::B_BYTES, &tmap_b, &full[stage], bc, br, pol_b);
 #pragma unroll
               for (int i = 0; i < kTmaRows / 4; ++i)
                 tma_gather4<CG>(sA + stage * C::A_BYTES + i * 4 * (BK * 2), &tmap_a, &full[stage], kb * BK,
@@ -380,9 +395,11 @@ __global__ void __launch_bounds__(kGather == kGatherCpAsync ? kThreadsCpAsync : 
         }
       } else if (lane == 0) {
         for (int t = t0; t < t1; ++t) {
-          const int b_row = t * BN + rank * C::B_ROWS;
+          const int b_row_off = rank * C::B_ROWS;
           for (int kb = 0; kb < k_blocks; ++kb) {
             mbar_wait_sleep(&empty[stage], phase ^ 1, MOSAIC_K3_PROD_SLEEP_NS);
+            int bc, br;
+            w_box(p, t, kb, k_blocks, b_row_off, bc, br);
             // MOSAIC_K3_HALF_A (experiment, wrong results): skip the A load on odd tiles to
             // measure what halving A's L2 feed (as A multicast across two pairs would) buys
             const bool load_a = !(MOSAIC_K3_HALF_A && (t & 1));
@@ -390,17 +407,17 @@ __global__ void __launch_bounds__(kGather == kGatherCpAsync ? kThreadsCpAsync : 
               mbar_arrive_expect_tx(&full[stage], (C::STAGE_BYTES - (load_a ? 0 : C::A_BYTES) +
                                                    (MOSAIC_K3_DUP_B ? C::B_BYTES : 0)) * CG);
             if constexpr (CG == 1)
-              tma_load_2d(sB + stage * C::B_BYTES, &tmap_b, &full[stage], kb * BK, b_row, pol_b);
+              tma_load_2d(sB + stage * C::B_BYTES, &tmap_b, &full[stage], bc, br, pol_b);
             else
-              tma_load_2d_cg2(sB + stage * C::B_BYTES, &tmap_b, &full[stage], kb * BK, b_row, pol_b);
+              tma_load_2d_cg2(sB + stage * C::B_BYTES, &tmap_b, &full[stage], bc, br, pol_b);
             if (MOSAIC_K3_DUP_B) {  // same W box again into a slot nobody reads (L2 -> SM feed experiment)
               uint8_t* dup = reinterpret_cast<uint8_t*>(
                   (reinterpret_cast<uintptr_t>(smem + C::STAGES * C::STAGE_BYTES + 256 + BM * 4 + 16) + 1023) &
                   ~static_cast<uintptr_t>(1023));
               if constexpr (CG == 1)
-                tma_load_2d(dup, &tmap_b, &full[stage], kb * BK, b_row, pol_b);
+                tma_load_2d(dup, &tmap_b, &full[stage], bc, br, pol_b);
               else
-                tma_load_2d_cg2(dup, &tmap_b, &full[stage], kb * BK, b_row, pol_b);
+                tma_load_2d_cg2(dup, &tmap_b, &full[stage], bc, br, pol_b);
             }
             if constexpr (kGather == kGatherTma4) {
               const uint32_t rows_addr = smem_u32(sidx);
@@ -721,7 +738,11 @@ int launch(const ASource& a, int64_t m_cap, const int32_t* m_dev, int64_t m_host
   CUtensorMap ta, tb;
   int st = gather ? encode_tma_bf16(&ta, a.base, a.rows, d, a.ld, 1, BK) : encode_tma_bf16(&ta, a.base, m_cap, d, a.ld, BM, BK);
   if (st) return st;
-  st = encode_tma_bf16(&tb, W, V, d, d, BN / cg, BK);
+  // experiment: W handed over pre-tiled as [n_tiles][d/64][256][64] (each TMA box one contiguous 32 KB block)
+  static const int w_blocked = env_int("MOSAIC_K3_WBLOCKED", 0);
+  p.w_blocked = w_blocked;
+  st = w_blocked ? encode_tma_bf16(&tb, W, ceil_div(V, BN) * (d / BK) * BN, BK, BK, BN / cg, BK)
+                 : encode_tma_bf16(&tb, W, V, d, d, BN / cg, BK);
   if (st) return st;
   p.m_dev = m_dev;
   p.m_host = m_host;

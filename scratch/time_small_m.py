@@ -9,6 +9,8 @@ dev = torch.device("cuda", 0)
 g = torch.Generator(device=dev).manual_seed(0)
 d, V = 4096, 126464
 W = (torch.randn(V, d, generator=g, device=dev) * 0.02).to(torch.bfloat16)
+if os.environ.get("MOSAIC_K3_WBLOCKED") == "1":  # pre-tiled W experiment (V is a multiple of 256 here)
+    W = W.view(V // 256, 256, d // 64, 64).permute(0, 2, 1, 3).contiguous().view(V, d)
 flush = torch.empty(512 << 20, dtype=torch.uint8, device=dev)
 for M in (1, 8, 32, 64, 128, 256, 512, 1024):
     hc = torch.randn(M, d, generator=g, device=dev).to(torch.bfloat16)
