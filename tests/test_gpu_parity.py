@@ -481,6 +481,36 @@ def test_full_size_step_properties(dev, name, L, d, V, shift, k):
     assert np.all(lse[rows] >= ref["max"] - 1e-3)
 
 
+@pytest.mark.parametrize("name,L,d,V,shift,k", [("llada_32k", 32768, 4096, 126464, False, 256),
+                                                ("dream_128k", 131072, 3584, 152064, True, 1024)])
+def test_full_size_k3_variants_bit_identical(dev, name, L, d, V, shift, k):
+    """At BASELINE sizes every K3 variant -- buffered (K2 + dense A) or gather
+    mode (A rows straight from H), default or die-aware unit schedule -- gives
+    the same tokens, lse, confidences and committed sequence bit for bit: same
+    operands, same MMA order, same epilogue, same fixed-order merge."""
+    from paper_2601_06562_b200 import MaskOnlyHead
+
+    g = torch.Generator(device=dev).manual_seed(L + 1)
+    mask_id = V - 1
+    H = torch.randn(L, d, generator=g, device=dev).to(torch.bfloat16)
+    W = (torch.randn(V, d, generator=g, device=dev) * 0.02).to(torch.bfloat16)
+    x0 = torch.randint(0, V - 1, (L,), generator=g, device=dev, dtype=torch.int32)
+    x0[torch.randperm(L, generator=g, device=dev)[: L // 2]] = mask_id
+    outs = []
+    for gather in (False, True):
+        for die in (False, True):
+            head = MaskOnlyHead(W, seq_len=L, mask_id=mask_id, shift=shift, fused_gather=gather, die_aware=die)
+            x = x0.clone()
+            o = head.step(x, H, k)
+            torch.cuda.synchronize()
+            M = int(o.m_dev.item())
+            outs.append((x.cpu(), o.token[:M].cpu(), o.lse[:M].cpu(), o.conf[:M].cpu(), o.selected[:M].cpu()))
+            del head
+    for other in outs[1:]:
+        for a, b in zip(outs[0], other):
+            assert torch.equal(a, b)
+
+
 def test_die_map_and_die_aware_k3(dev):
     """The measured SM -> die map splits the SMs into two halves (TPC pairs
     together), and K3 under the die-aware schedule is bit-identical to the
