@@ -408,6 +408,12 @@ def gpu_main(args):
         "clocks": clocks.summary(),
         "e2e": e2e,
         "workspace_bytes": head.workspace_bytes,
+        "memory": {"head_workspace_bytes": head.workspace_bytes,  # hc + partials + per-row outputs + scratch
+                   "inputs_bytes": W.numel() * 2 + H.numel() * 2,  # LM-head shard + hidden states (not activation)
+                   "torch_max_allocated_bytes": torch.cuda.max_memory_allocated(dev),
+                   "dense_logits_bytes_avoided": M * (v1 - v0) * 4,  # the fp32 [M, V] the reference materialises
+                   "note": "measured on this process; the full-model arena figures are peak_activation_gb (plan) "
+                           "and profiles/r01e_context_sweep.json (measured commits)"},
         **context_fields(),
     }
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
