@@ -366,11 +366,16 @@ def gpu_main(args):
                        "previous step's compute); updated x read back every step"}
 
     peaks = json.loads((ROOT / "MEASURED_PEAKS.json").read_text()) if (ROOT / "MEASURED_PEAKS.json").exists() else {}
-    # K3 runs back to back for the whole timed region (steps x ~12 ms) under the
-    # 1000 W cap, i.e. "a kernel timed inside a long step": the denominator is the
-    # measured sustained cuBLAS figure; the burst fraction is reported beside it.
+    # Denominator by the length of the timed region: K3 runs back to back for
+    # steps x ~12 ms; a region of seconds settles under the 1000 W cap like the
+    # driver's seconds-long cuBLAS loop (bf16_tflops_sustained), a shorter one
+    # (the default 20 steps, ~0.25 s) is compared with the burst figure. Both
+    # fractions are reported.
     burst = peaks.get("bf16_tflops", 1590.0)
-    peak = peaks.get("bf16_tflops_sustained", burst)
+    sustained = peaks.get("bf16_tflops_sustained", burst)
+    timed_s = ms_per_step * args.steps / 1e3
+    long_region = timed_s >= 2.0 and "bf16_tflops_sustained" in peaks
+    peak = sustained if long_region else burst
     flops = 2.0 * D * (v1 - v0) * M
     achieved = flops / (k3_ms / 1e3) / 1e12
     traffic = None
@@ -399,9 +404,12 @@ def gpu_main(args):
                    "l2": "inputs larger than L2 (W 1.04 GB, H 268 MB > 126 MB)"},
         "roofline": {"bound": "tensor", "kernel": "k3_lmhead (tcgen05 stats GEMM)",
                      "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
-                     "peak_source": ("MEASURED_PEAKS.json bf16_tflops_sustained (K3 timed inside a long, power-capped "
-                                     "step loop)") if "bf16_tflops_sustained" in peaks else "fallback 1590 (burst)",
+                     "peak_source": (("MEASURED_PEAKS.json bf16_tflops_sustained (timed region "
+                                      f"{timed_s:.2f} s >= 2 s: power-capped steady state)") if long_region else
+                                     (f"MEASURED_PEAKS.json bf16_tflops (burst; timed region {timed_s:.2f} s < 2 s)"
+                                      if "bf16_tflops" in peaks else "fallback 1590 (burst)")),
                      "peak_burst": burst, "frac_of_burst": achieved / burst,
+                     "peak_sustained": sustained, "frac_of_sustained": achieved / sustained,
                      "k3_ms": k3_ms, "k3_share_of_step": k3_ms / ms_per_step,
                      "flops_per_launch": flops, "traffic": traffic},
         "gpu_launches": launches_per_step * args.steps,
