@@ -14,6 +14,7 @@
 // towards the lower sequence position. Implemented as an exact radix select on
 // the 64-bit key (conf bits << 32 | ~pos), unique per row, 8 passes of 8 bits.
 #include <cfloat>
+#include <cstdlib>
 
 #include "common.cuh"
 
@@ -145,7 +146,7 @@ __global__ void __launch_bounds__(256) k5_commit(const float* __restrict__ conf,
 // radix select (one 8-bit digit of the 64-bit key per pass, histogram in
 // shared memory) and the commit, in one launch instead of 18 -- at LLaDA 32k
 // (M = 16384) the 18 dependent launches cost more than the work.
-constexpr int64_t kFusedRemaskCap = 65536;
+constexpr int64_t kFusedRemaskCap = 40960;  // measured crossover (profiles/r01i_k5_crossover.txt)
 constexpr int kFusedThreads = 1024;
 
 __global__ void __launch_bounds__(kFusedThreads) k5_fused(const float* __restrict__ conf,
@@ -250,7 +251,11 @@ extern "C" int mosaic_remask_commit(const float* conf, const int32_t* pos, const
   if (m_cap == 0) return MOSAIC_OK;
   MOSAIC_REQUIRE(conf && pos && token && x, "null inputs");
   cudaStream_t s = as_stream(stream);
-  if (m_cap <= kFusedRemaskCap) {
+  static const int64_t fused_cap = [] {  // experiment knob; default measured (profiles/r01i_k5_crossover.txt)
+    const char* e = getenv("MOSAIC_K5_FUSED_CAP");
+    return e ? static_cast<int64_t>(atoll(e)) : kFusedRemaskCap;
+  }();
+  if (m_cap <= fused_cap) {
     k5_fused<<<1, kFusedThreads, 0, s>>>(conf, pos, token, m_dev, m_host, m_cap, k, x, selected);
     return check_launch("mosaic_remask_commit");
   }
