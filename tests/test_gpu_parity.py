@@ -217,7 +217,7 @@ def test_vocab_shards_merge_equals_unsharded(dev):
 
 # ----------------------------------------------------------------------- K5
 @pytest.mark.parametrize("M,k", [(1, 1), (10, 0), (10, 10), (10, 25), (1024, 32), (16384, 256),
-                                 (65536, 683), (524288, 8192)])
+                                 (40960, 640), (40961, 641), (65536, 683), (524288, 8192)])  # both K5 paths
 def test_remask_commit_bitexact(dev, M, k):
     from paper_2601_06562_b200 import hotpath
 
