@@ -370,6 +370,12 @@ class MaskOnlyHead:
     vocab-sharded ranks (all-gather over NCCL + K4 in rank order), and commit the
     k most confident predictions into ``x`` in place (K5). ``[M, V]`` logits
     never exist. Every rank of ``group`` ends with identical ``x``.
+
+    ``m_cap`` (default ``seq_len``) sizes the per-row buffers; the masked count
+    M is read on the device every step, so a step with more than ``m_cap``
+    masked positions processes only the first ``m_cap`` of them (ascending
+    positions) -- size it for the largest M the caller will present (the step-0
+    count of the schedule, ``workload.ScenarioConfig.masked_at(0)``).
     """
 
     def __init__(self, weight_shard: torch.Tensor, *, seq_len: int, mask_id: int,
