@@ -6,6 +6,8 @@ schedule, single-SM or pair tiles). Tolerances as tests/test_gpu_parity.py:
 indices and selections bit-exact, tokens exact where the fp64 top-1 margin
 exceeds 1e-3, lse / confidence within 1e-3 relative.
 """
+import os
+
 import numpy as np
 import pytest
 import torch
@@ -14,7 +16,7 @@ import mosaic_oracle as orc
 
 pytestmark = pytest.mark.gpu
 
-N_CASES = 48
+N_CASES = int(os.environ.get("MOSAIC_FUZZ_CASES", "48"))
 
 
 @pytest.fixture(scope="module")
