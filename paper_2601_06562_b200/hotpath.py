@@ -128,18 +128,18 @@ def die_map(device=None) -> tuple[torch.Tensor, dict]:
 
 def die_aware_default(die_aware: Optional[bool] = None, m_cap: int = 0, v_shard: int = 0) -> bool:
     """Whether K3 takes the die-aware unit schedule. An explicit argument or
-    MOSAIC_DIE_AWARE=0/1 decides; otherwise it is on for large problems
-    (m_cap >= 4096 rows and a vocab shard >= 32768), where it was measured
-    faster (profiles/r01h_k3_die_aware.txt, r01h_kernels_die.json: Dream K3
-    -11%, MoE -3%, LLaDA steady step +2%), and off for small ones, where its
-    launch-time registration and the split's locality do not pay (tiny
-    +6 us, LLaDA 1/8 vocab shard +6%)."""
+    MOSAIC_DIE_AWARE=0/1 decides; otherwise it is on when m_cap >= 4096 rows
+    and the vocab shard >= 8192, where it was measured faster in the
+    power-capped steady state (profiles/r01i_k3_die_aware_steady.txt: Dream
+    +6.6%, LLaDA +3%, MoE-like +2.5%, the 1/4 and 1/8 LLaDA shards +1.1% /
+    +0.6%, neutral at M = 4096), and off for small heads, where the launch-time
+    registration (~6 us) is not repaid."""
     if die_aware is not None:
         return bool(die_aware)
     env = os.environ.get("MOSAIC_DIE_AWARE")
     if env in ("0", "1"):
         return env == "1"
-    return m_cap >= 4096 and v_shard >= 32768
+    return m_cap >= 4096 and v_shard >= 8192
 
 
 def lmhead_stats(hc: torch.Tensor, weight: torch.Tensor, n_splits: int, part_max: torch.Tensor,
