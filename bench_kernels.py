@@ -135,6 +135,15 @@ def main():
         graph = head.capture(xg, H, 64)
         graph_ms = timeit(lambda: (xg.copy_(x0), graph.replay()), iters=20)
         out[f"step_{name}"] = {"L": L, "d": d, "V": V, "eager_ms": eager_ms, "graph_ms": graph_ms}
+        if name == "llada":  # semi-autoregressive block decoding: one 32-position block of the masked half
+            lo = L // 2
+            xw = x0.clone()
+            wg = head.capture(xw, H, 4, window=(lo, lo + 32))
+            win_eager = timeit(lambda: (x.copy_(x0), head.step(x, H, 4, window=(lo, lo + 32))), iters=50)
+            win_graph = timeit(lambda: (xw.copy_(x0), wg.replay()), iters=50)
+            out["step_llada_block32"] = {"L": L, "window": 32, "eager_ms": win_eager, "graph_ms": win_graph,
+                                         "note": "step(window=(L/2, L/2+32)): K3 over <= 32 masked rows "
+                                                 "streams the whole 1.04 GB LM head"}
         del H, W
 
     # K5 ---------------------------------------------------------------------

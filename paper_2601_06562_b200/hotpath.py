@@ -359,6 +359,7 @@ class StepOutput:
     lse: torch.Tensor         # [m_cap] fp32 log-sum-exp
     conf: torch.Tensor        # [m_cap] fp32 p(token)
     selected: torch.Tensor    # [m_cap] int32 1 = unmasked this step
+    offset: int = 0           # positions are idx + offset (a windowed step's lo)
 
 
 class MaskOnlyHead:
@@ -392,6 +393,8 @@ class MaskOnlyHead:
         self.shift = bool(shift)
         self.group = group
         self.fused_gather = bool(fused_gather)  # K3 reads rows of `hidden` directly: no K2, no hc buffer
+        self._die_aware = die_aware
+        self._wplans: dict = {}
         self.die_table = (die_map(weight_shard.device)[0]
                           if die_aware_default(die_aware, self.m_cap, self.v_shard) else None)
         if not (exchange in ("nccl", "p2p") or hasattr(exchange, "push")):
@@ -439,7 +442,8 @@ class MaskOnlyHead:
     def workspace_bytes(self) -> int:
         return self.layout.size
 
-    def capture(self, x: torch.Tensor, hidden: torch.Tensor, k: int) -> "torch.cuda.CUDAGraph":
+    def capture(self, x: torch.Tensor, hidden: torch.Tensor, k: int,
+                window: Optional[tuple[int, int]] = None) -> "torch.cuda.CUDAGraph":
         """Capture one whole step (K1..K5) into a CUDA graph bound to these
         ``x`` / ``hidden`` buffers and this ``k``. Every launch reads the masked
         count from the device (K1's output), so one graph serves every step of
@@ -451,51 +455,87 @@ class MaskOnlyHead:
         g = torch.cuda.CUDAGraph()
         side = torch.cuda.Stream(device=x.device)
         side.wait_stream(torch.cuda.current_stream(x.device))
+        if window is not None:
+            self._window_plan(min(self.m_cap, int(window[1]) - int(window[0])))  # host planning before capture
         with torch.cuda.graph(g, stream=side):
-            self.step(x, hidden, k)
+            self.step(x, hidden, k, window=window)
         torch.cuda.current_stream(x.device).wait_stream(side)
         return g
 
-    def step(self, x: torch.Tensor, hidden: torch.Tensor, k: int, stream=None) -> StepOutput:
+    def _window_plan(self, m_w: int) -> tuple[int, Optional[torch.Tensor]]:
+        """Splits and die table for a windowed step of capacity m_w rows: planned
+        for m_w itself (a block of 32 masked rows wants one split per SM, not the
+        full-sequence split), coarsened if needed to fit the head's partials."""
+        if m_w not in self._wplans:
+            S_w, _ = lmhead_plan(m_w, self.v_shard, self.d)
+            if S_w * m_w > self.n_splits * self.m_cap:
+                S_w, _ = lmhead_plan(m_w, self.v_shard, self.d,
+                                     max_splits=max(1, self.n_splits * self.m_cap // m_w))
+            die = self.die_table if die_aware_default(self._die_aware, m_w, self.v_shard) else None
+            self._wplans[m_w] = (S_w, die)
+        return self._wplans[m_w]
+
+    def step(self, x: torch.Tensor, hidden: torch.Tensor, k: int, stream=None,
+             window: Optional[tuple[int, int]] = None) -> StepOutput:
+        """One step. ``window=(lo, hi)``: only masked positions in [lo, hi) are
+        predicted and only they can be committed (semi-autoregressive block
+        decoding: the current block); everything runs on views of ``x`` /
+        ``hidden``, so [M, V] work and buffers shrink to the window. The
+        returned ``idx`` is then relative to ``lo`` (``StepOutput.offset``)."""
         b = self.buf
         _req(x, torch.int32, "x", 1)
         if x.numel() != self.L or hidden.shape[0] != self.L or hidden.shape[1] != self.d:
             raise InputError("x/hidden do not match the configured sequence length / width")
+        lo, hi = (0, self.L) if window is None else (int(window[0]), int(window[1]))
+        if not 0 <= lo < hi <= self.L:
+            raise InputError(f"window {window} outside [0, {self.L})")
+        shift = self.shift
+        if (lo, hi) != (0, self.L):
+            x = x[lo:hi]
+            if shift and lo > 0:  # src(p) = p - 1 >= lo - 1: the shifted view needs no clamp
+                hidden, shift = hidden[lo - 1:hi - 1], False
+            else:
+                hidden = hidden[lo:hi]
+            m = min(self.m_cap, hi - lo)
+            S, die = self._window_plan(m)
+        else:
+            m, S, die = self.m_cap, self.n_splits, self.die_table
+        pmax = b["part_max"].view(-1)[:S * m].view(S, m)
+        psum = b["part_sum"].view(-1)[:S * m].view(S, m)
+        parg = b["part_arg"].view(-1)[:S * m].view(S, m)
         m_dev = b["m_dev"]
         mask_compact(x, self.mask_id, b["idx"], m_dev, b["compact_scratch"], stream)
         if self.fused_gather:
-            lmhead_stats_gather(hidden, b["idx"], self.weight, self.n_splits, b["part_max"], b["part_sum"],
-                                b["part_arg"], self.m_cap, m_dev=m_dev, shift=self.shift,
-                                v_offset=self.vocab_offset, stream=stream, die_of_sm=self.die_table,
-                                sched=b["sched"])
+            lmhead_stats_gather(hidden, b["idx"], self.weight, S, pmax, psum, parg, m, m_dev=m_dev, shift=shift,
+                                v_offset=self.vocab_offset, stream=stream, die_of_sm=die, sched=b["sched"])
         else:
-            gather_rows(hidden, b["idx"], b["hc"], m_dev=m_dev, shift=self.shift, stream=stream)
-            lmhead_stats(b["hc"], self.weight, self.n_splits, b["part_max"], b["part_sum"],
-                         b["part_arg"], m_dev=m_dev, v_offset=self.vocab_offset, stream=stream,
-                         die_of_sm=self.die_table, sched=b["sched"])
-        m, S = self.m_cap, self.n_splits
+            hc = b["hc"][:m]
+            gather_rows(hidden, b["idx"], hc, m_dev=m_dev, shift=shift, stream=stream)
+            lmhead_stats(hc, self.weight, S, pmax, psum, parg, m_dev=m_dev, v_offset=self.vocab_offset,
+                         stream=stream, die_of_sm=die, sched=b["sched"])
         if self.group is None and self.p2p is None:
-            stats_merge(b["part_max"], b["part_sum"], b["part_arg"], S, m, m, m_dev=m_dev,
-                        token=b["token"], lse=b["lse"], conf=b["conf"], stream=stream)
+            stats_merge(pmax, psum, parg, S, m, m, m_dev=m_dev, token=b["token"], lse=b["lse"], conf=b["conf"],
+                        stream=stream)
         elif self.p2p is not None:  # K4x: merge + peer stores + signal, then wait; no NCCL call
-            self.p2p.push(b["part_max"], b["part_sum"], b["part_arg"], S, m, m_dev=m_dev, stream=stream)
+            self.p2p.push(pmax, psum, parg, S, m, m_dev=m_dev, stream=stream)
             self.p2p.wait(stream)
             g = self.p2p.current
-            stats_merge(g[0, 0], g[0, 1], g[0, 2].view(torch.int32), self.world, 3 * m, m,
+            M3 = 3 * self.p2p.m_cap
+            stats_merge(g[0, 0], g[0, 1], g[0, 2].view(torch.int32), self.world, M3, m,
                         m_dev=m_dev, token=b["token"], lse=b["lse"], conf=b["conf"], stream=stream)
         else:
             from .shard import exchange_triples
 
             loc = b["local"]
-            stats_merge(b["part_max"], b["part_sum"], b["part_arg"], S, m, m, m_dev=m_dev,
+            stats_merge(pmax, psum, parg, S, m, m, m_dev=m_dev,
                         out_max=loc[0], out_sum=loc[1], out_arg=loc[2].view(torch.int32),
                         stream=stream)
             g = b["gathered"]
             # NCCL orders its collective after torch's current stream: make that the step's stream
             with torch.cuda.stream(stream if stream is not None else torch.cuda.current_stream()):
                 exchange_triples(loc, group=self.group, out=g)  # NCCL all-gather, 12 B/row/rank
-            stats_merge(g[0, 0], g[0, 1], g[0, 2].view(torch.int32), self.world, 3 * m, m,
+            stats_merge(g[0, 0], g[0, 1], g[0, 2].view(torch.int32), self.world, 3 * self.m_cap, m,
                         m_dev=m_dev, token=b["token"], lse=b["lse"], conf=b["conf"], stream=stream)
         remask_commit(b["conf"], b["idx"], b["token"], int(k), x, b["remask_scratch"], m,
                       m_dev=m_dev, selected=b["selected"], stream=stream)
-        return StepOutput(m_dev, b["idx"][:m], b["token"], b["lse"], b["conf"], b["selected"])
+        return StepOutput(m_dev, b["idx"][:m], b["token"], b["lse"], b["conf"], b["selected"], lo)

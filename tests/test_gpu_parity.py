@@ -640,3 +640,56 @@ def test_graph_captured_step_matches_eager(dev):
         assert int(graphed.buf["m_dev"].item()) == M
         assert torch.equal(xe.cpu(), xg.cpu())
         assert torch.equal(oe.conf[:M].cpu(), graphed.buf["conf"][:M].cpu())
+
+
+@pytest.mark.parametrize("L,d,V,lo,hi,shift,gather", [(4096, 512, 16384, 1024, 1056, False, False),
+                                                     (4096, 512, 16384, 1024, 1056, True, False),
+                                                     (4096, 512, 16384, 0, 32, True, False),
+                                                     (4096, 512, 16384, 2000, 2300, False, True),
+                                                     (4096, 512, 16384, 3000, 4096, True, True),
+                                                     (32768, 4096, 126464, 16384, 16416, False, False)])
+def test_windowed_step_semi_autoregressive(dev, L, d, V, lo, hi, shift, gather):
+    """step(window=(lo, hi)): only masked positions inside the block are
+    predicted and committed (LLaDA-style semi-autoregressive decoding); equals
+    the oracle step on the block with the hidden rows the full step would use
+    (Dream shift included), and nothing outside the block changes."""
+    from paper_2601_06562_b200 import MaskOnlyHead
+
+    rng = np.random.default_rng(L + lo)
+    mask_id = V - 1
+    x = rng.integers(0, V - 1, size=L).astype(np.int32)
+    x[rng.random(L) < 0.6] = mask_id
+    H = orc.bf16_round(rng.standard_normal((L, d)))
+    W = orc.bf16_round(rng.standard_normal((V, d)) * 0.03)
+    head = MaskOnlyHead(bf16_tensor(W, dev), seq_len=L, mask_id=mask_id, shift=shift, fused_gather=gather)
+    Hd = bf16_tensor(H, dev)
+    k = 7
+    for use_graph in (False, True):
+        xd = torch.from_numpy(x).to(dev)
+        if use_graph:
+            g = head.capture(xd, Hd, k, window=(lo, hi))
+            g.replay()
+            out = None
+        else:
+            out = head.step(xd, Hd, k, window=(lo, hi))
+        torch.cuda.synchronize()
+        xo = xd.cpu().numpy()
+        assert np.array_equal(xo[:lo], x[:lo]) and np.array_equal(xo[hi:], x[hi:])
+        # oracle on the block: positions in [lo, hi), hidden row p (or p - 1 with the shift)
+        idx = orc.mask_compact(x[lo:hi], mask_id) + lo
+        src = np.maximum(idx - 1, 0) if shift else idx
+        ref = orc.softmax_stats(orc.logits_f64(H[src], W))
+        if out is not None:
+            M = int(out.m_dev.item())
+            assert M == idx.size and out.offset == lo
+            assert np.array_equal(out.idx[:M].cpu().numpy() + lo, idx)
+            tok = out.token[:M].cpu().numpy()
+            ok = ref["margin"] > MARGIN
+            assert np.array_equal(tok[ok], ref["arg"][ok])
+            assert orc.isclose_rel(out.conf[:M].cpu().numpy().astype(np.float64), ref["conf"], CONF_REL)
+            sel = out.selected[:M].cpu().numpy().astype(bool)
+            assert np.array_equal(sel, orc.remask_select(out.conf[:M].cpu().numpy(), idx, k))
+            first = xo.copy()
+        else:
+            assert np.array_equal(xo, first)  # the captured windowed step commits the same tokens
+        assert int((xo[lo:hi] != x[lo:hi]).sum()) <= min(k, idx.size)
