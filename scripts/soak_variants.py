@@ -1,0 +1,60 @@
+"""Soak: many fused steps with every K3 variant (buffered / gather mode x default /
+die-aware schedule) on random inputs, each compared bit for bit with the buffered
+default-schedule step. Catches rare ordering bugs in the pair-gather relay and the
+die-aware registration that a single test run would miss.
+
+    python scripts/soak_variants.py [--iters N] [--seconds S]
+"""
+import argparse
+import os
+import sys
+import time
+
+sys.path.insert(0, os.getcwd())
+import torch
+
+from paper_2601_06562_b200 import MaskOnlyHead, _native
+
+ap = argparse.ArgumentParser()
+ap.add_argument("--iters", type=int, default=100000)
+ap.add_argument("--seconds", type=float, default=240.0)
+args = ap.parse_args()
+_native.load()
+dev = torch.device("cuda", 0)
+shapes = [(32768, 4096, 126464 // 4), (8192, 4096, 126464), (20000, 3584, 19008), (4096, 2048, 50000)]
+heads = {}
+rng = torch.Generator(device=dev).manual_seed(123)
+t0 = time.time()
+n = mismatches = 0
+while n < args.iters and time.time() - t0 < args.seconds:
+    L, d, V = shapes[n % len(shapes)]
+    shift = bool(n % 3 == 0)
+    mask_id = V - 1
+    if (L, d, V) not in heads:
+        W = (torch.randn(V, d, generator=rng, device=dev) * 0.02).to(torch.bfloat16)
+        heads[(L, d, V)] = (W, {})
+    W, hv = heads[(L, d, V)]
+    H = torch.randn(L, d, generator=rng, device=dev).to(torch.bfloat16)
+    x0 = torch.randint(0, V - 1, (L,), generator=rng, device=dev, dtype=torch.int32)
+    frac = float(torch.rand(1, generator=rng, device=dev)) * 0.9 + 0.05
+    x0[torch.rand(L, generator=rng, device=dev) < frac] = mask_id
+    outs = []
+    for gather in (False, True):
+        for die in (False, True):
+            key = (gather, die, shift)
+            if key not in hv:
+                hv[key] = MaskOnlyHead(W, seq_len=L, mask_id=mask_id, shift=shift, fused_gather=gather,
+                                       die_aware=die)
+            x = x0.clone()
+            o = hv[key].step(x, H, 64)
+            M = int(o.m_dev.item())
+            outs.append((x, o.token[:M].clone(), o.lse[:M].clone(), o.conf[:M].clone()))
+    ref = outs[0]
+    for i, o in enumerate(outs[1:], 1):
+        if not all(torch.equal(a, b) for a, b in zip(ref, o)):
+            mismatches += 1
+            print(f"MISMATCH iter {n} shape {(L, d, V)} shift {shift} variant {i}", flush=True)
+    n += 1
+torch.cuda.synchronize()
+print(f"soak: {n} iterations x 4 variants in {time.time() - t0:.0f} s, mismatches {mismatches}")
+sys.exit(1 if mismatches else 0)
