@@ -198,6 +198,19 @@ MOSAIC_API int mosaic_remask_commit(const float* conf, const int32_t* pos, const
                          const int32_t* m_dev, int64_t m_host, int64_t m_cap, int64_t k,
                          int32_t* x, int32_t* selected, void* scratch, void* stream);
 
+/* K5 per segment (batched sequences / semi-autoregressive blocks): the rows
+ * whose position pos[r] lies in [b * seg_len, (b + 1) * seg_len) form segment
+ * b (a contiguous run of the ascending compacted list; one CTA each), which
+ * keeps its own k_b most confident rows (ties -> lower position) and commits
+ * x[pos[r]] = token[r] for them. k_b = k_per_seg[b] (device int32 [n_seg]) or
+ * `k` when k_per_seg is null; k_b is clamped to the segment's row count.
+ * Extends the reference's single-sequence `commit` (workload.py:315) to a
+ * batch; no scratch needed.                                                  */
+MOSAIC_API int mosaic_remask_commit_segmented(const float* conf, const int32_t* pos, const int32_t* token,
+                                   const int32_t* m_dev, int64_t m_host, int64_t m_cap, int64_t seg_len,
+                                   int32_t n_seg, const int32_t* k_per_seg, int64_t k, int32_t* x,
+                                   int32_t* selected, void* stream);
+
 /* ---------------------------------------------------------------- K6 ------
  * Fused SwiGLU of one FFN chunk, in place: up[i] = silu(gate[i]) * up[i],
  * bf16, n elements (the in-place `glu` op of the chunked FFN loop,

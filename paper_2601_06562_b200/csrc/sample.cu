@@ -149,18 +149,19 @@ __global__ void __launch_bounds__(256) k5_commit(const float* __restrict__ conf,
 constexpr int64_t kFusedRemaskCap = 40960;  // measured crossover (profiles/r01i_k5_crossover.txt)
 constexpr int kFusedThreads = 1024;
 
-__global__ void __launch_bounds__(kFusedThreads) k5_fused(const float* __restrict__ conf,
-                                                          const int32_t* __restrict__ pos,
-                                                          const int32_t* __restrict__ token,
-                                                          const int32_t* __restrict__ m_dev, int64_t m_host,
-                                                          int64_t m_cap, int64_t k, int32_t* __restrict__ x,
-                                                          int32_t* __restrict__ selected) {
+// One CTA selects and commits among rows [r0, r1): the k most confident
+// (ties -> lower position), exactly, by an 8-pass radix select of the 64-bit
+// key with the histogram in shared memory.
+__device__ __forceinline__ void select_commit_cta(const float* __restrict__ conf, const int32_t* __restrict__ pos,
+                                                  const int32_t* __restrict__ token, int64_t r0, int64_t r1,
+                                                  int64_t k, int32_t* __restrict__ x,
+                                                  int32_t* __restrict__ selected) {
   __shared__ uint32_t h[256];
   __shared__ uint32_t cum[256];
   __shared__ unsigned long long s_prefix;
   __shared__ uint32_t s_krem;
   const int t = threadIdx.x;
-  const int64_t M = min(static_cast<int64_t>(load_count(m_dev, m_host)), m_cap);
+  const int64_t M = r1 - r0;
   const int64_t kk = k < M ? k : M;
   if (t == 0) {
     s_prefix = 0ull;
@@ -177,7 +178,7 @@ __global__ void __launch_bounds__(kFusedThreads) k5_fused(const float* __restric
     const unsigned long long prefix = s_prefix;
     const int hi_shift = 64 - 8 * pass;
     const int lo_shift = 56 - 8 * pass;
-    for (int64_t r = t; r < M; r += kFusedThreads) {
+    for (int64_t r = r0 + t; r < r1; r += kFusedThreads) {
       const unsigned long long key = remask_key(conf[r], pos[r]);
       if (pass == 0 || (key >> hi_shift) == (prefix >> hi_shift)) atomicAdd(&h[(key >> lo_shift) & 255u], 1u);
     }
@@ -205,12 +206,52 @@ __global__ void __launch_bounds__(kFusedThreads) k5_fused(const float* __restric
   }
   const bool active = kk > 0;
   const unsigned long long thr = s_prefix;
-  for (int64_t r = t; r < M; r += kFusedThreads) {
+  for (int64_t r = r0 + t; r < r1; r += kFusedThreads) {
     const int32_t p = pos[r];
     const bool sel = active && remask_key(conf[r], p) >= thr;
     if (sel) x[p] = token[r];
     if (selected) selected[r] = sel ? 1 : 0;
   }
+}
+
+__global__ void __launch_bounds__(kFusedThreads) k5_fused(const float* __restrict__ conf,
+                                                          const int32_t* __restrict__ pos,
+                                                          const int32_t* __restrict__ token,
+                                                          const int32_t* __restrict__ m_dev, int64_t m_host,
+                                                          int64_t m_cap, int64_t k, int32_t* __restrict__ x,
+                                                          int32_t* __restrict__ selected) {
+  const int64_t M = min(static_cast<int64_t>(load_count(m_dev, m_host)), m_cap);
+  select_commit_cta(conf, pos, token, 0, M, k, x, selected);
+}
+
+// Segmented K5 (batched sequences / blocks): CTA b owns the rows whose
+// position lies in [b * seg_len, (b + 1) * seg_len) -- a contiguous run of the
+// ascending compacted list, found by binary search -- and commits its own k_b.
+__device__ __forceinline__ int64_t lower_bound_pos(const int32_t* __restrict__ pos, int64_t n, int64_t v) {
+  int64_t lo = 0, hi = n;
+  while (lo < hi) {
+    const int64_t mid = (lo + hi) >> 1;
+    if (pos[mid] < v) lo = mid + 1;
+    else hi = mid;
+  }
+  return lo;
+}
+
+__global__ void __launch_bounds__(kFusedThreads) k5_segmented(const float* __restrict__ conf,
+                                                              const int32_t* __restrict__ pos,
+                                                              const int32_t* __restrict__ token,
+                                                              const int32_t* __restrict__ m_dev, int64_t m_host,
+                                                              int64_t m_cap, int64_t seg_len,
+                                                              const int32_t* __restrict__ k_per_seg, int64_t k,
+                                                              int32_t* __restrict__ x,
+                                                              int32_t* __restrict__ selected) {
+  __shared__ int64_t s_bounds[2];
+  const int64_t M = min(static_cast<int64_t>(load_count(m_dev, m_host)), m_cap);
+  const int64_t b = blockIdx.x;
+  if (threadIdx.x < 2) s_bounds[threadIdx.x] = lower_bound_pos(pos, M, (b + threadIdx.x) * seg_len);
+  __syncthreads();
+  const int64_t kb = k_per_seg ? static_cast<int64_t>(k_per_seg[b]) : k;
+  select_commit_cta(conf, pos, token, s_bounds[0], s_bounds[1], kb < 0 ? 0 : kb, x, selected);
 }
 
 int grid_for(int64_t n, int per_block) {
@@ -268,4 +309,19 @@ extern "C" int mosaic_remask_commit(const float* conf, const int32_t* pos, const
   }
   k5_commit<<<grid, 256, 0, s>>>(conf, pos, token, m_dev, m_host, m_cap, st, x, selected);
   return check_launch("mosaic_remask_commit");
+}
+
+extern "C" int mosaic_remask_commit_segmented(const float* conf, const int32_t* pos, const int32_t* token,
+                                              const int32_t* m_dev, int64_t m_host, int64_t m_cap, int64_t seg_len,
+                                              int32_t n_seg, const int32_t* k_per_seg, int64_t k, int32_t* x,
+                                              int32_t* selected, void* stream) {
+  MOSAIC_REQUIRE(k >= 0, "negative unmask count %lld", (long long)k);
+  MOSAIC_REQUIRE(seg_len >= 1 && n_seg >= 1 && n_seg <= (1 << 20), "bad segments (%lld x %d)", (long long)seg_len,
+                 n_seg);
+  MOSAIC_REQUIRE(m_dev != nullptr || (m_host >= 0 && m_host <= m_cap), "m_host > m_cap");
+  if (m_cap == 0) return MOSAIC_OK;
+  MOSAIC_REQUIRE(conf && pos && token && x, "null inputs");
+  k5_segmented<<<n_seg, kFusedThreads, 0, as_stream(stream)>>>(conf, pos, token, m_dev, m_host, m_cap, seg_len,
+                                                                k_per_seg, k, x, selected);
+  return check_launch("mosaic_remask_commit_segmented");
 }

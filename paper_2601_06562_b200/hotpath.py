@@ -233,6 +233,20 @@ def remask_commit(conf, pos, token, k: int, x, scratch, m_cap: int, m_dev=None, 
                  int(m_cap), int(k), _p(x), _p(selected), _p(scratch), _s(stream))
 
 
+def remask_commit_segmented(conf, pos, token, x, m_cap: int, seg_len: int, n_seg: int, k: int = 0,
+                            k_per_seg: Optional[torch.Tensor] = None, m_dev=None, m_host: int = 0,
+                            selected=None, stream=None) -> None:
+    """K5 per segment (batched sequences / blocks): rows whose position lies in
+    [b * seg_len, (b + 1) * seg_len) form segment b, which commits its own k_b
+    most confident rows (``k_per_seg[b]``, device int32, or ``k`` for all)."""
+    if k_per_seg is not None:
+        _req(k_per_seg, torch.int32, "k_per_seg", 1)
+        if k_per_seg.numel() < n_seg:
+            raise InputError("k_per_seg must hold one count per segment")
+    _native.call("mosaic_remask_commit_segmented", _p(conf), _p(pos), _p(token), _p(m_dev), int(m_host),
+                 int(m_cap), int(seg_len), int(n_seg), _p(k_per_seg), int(k), _p(x), _p(selected), _s(stream))
+
+
 # ----------------------------------------------------------------- K6
 def swiglu_(gate: torch.Tensor, up: torch.Tensor, stream=None) -> torch.Tensor:
     """In place: up = silu(gate) * up (bf16), the chunked FFN's `glu` op."""
@@ -442,6 +456,57 @@ class MaskOnlyHead:
     def workspace_bytes(self) -> int:
         return self.layout.size
 
+    def step_batch(self, x: torch.Tensor, hidden: torch.Tensor, k, stream=None,
+                   window: Optional[tuple[int, int]] = None) -> StepOutput:
+        """One step over a batch of B sequences at once: ``x`` [B, Ls] int32,
+        ``hidden`` [B, Ls, d] bf16 (contiguous), ``k`` an int or a device int32
+        [B] of per-sequence unmask counts, ``window=(lo, hi)`` the same block of
+        every sequence (semi-autoregressive decoding) or None for all of it.
+        All B x (hi - lo) positions share one LM-head pass -- so a batch of short
+        blocks streams W once instead of B times -- and every sequence commits
+        its own k most confident masked positions (segmented K5). The head must
+        be built with ``seq_len >= B * (hi - lo)``; the returned ``idx`` are the
+        flattened window coordinates b * (hi - lo) + (p - lo)."""
+        from contextlib import nullcontext
+
+        if x.dim() != 2 or x.dtype != torch.int32 or not x.is_cuda:
+            raise InputError("x must be a [B, Ls] int32 CUDA tensor")
+        B, Ls = x.shape
+        if hidden.shape != (B, Ls, self.d) or hidden.dtype != torch.bfloat16 or not hidden.is_contiguous():
+            raise InputError(f"hidden must be a contiguous [{B}, {Ls}, {self.d}] bf16 tensor")
+        lo, hi = (0, Ls) if window is None else (int(window[0]), int(window[1]))
+        if not 0 <= lo < hi <= Ls:
+            raise InputError(f"window {window} outside [0, {Ls})")
+        Wn = hi - lo
+        if B * Wn > self.L:
+            raise InputError(f"batch x window = {B * Wn} positions exceeds the head's seq_len {self.L}")
+        b = self.buf
+        m = min(self.m_cap, B * Wn)
+        S, die = self._window_plan(m)
+        if getattr(self, "_xs", None) is None:  # batch staging (first batched call)
+            self._xs = torch.empty(self.L, dtype=torch.int32, device=self.weight.device)
+            self._rows = torch.empty(self.m_cap, dtype=torch.int32, device=self.weight.device)
+        with torch.cuda.stream(stream) if stream is not None else nullcontext():
+            xs = self._xs[:B * Wn].view(B, Wn)
+            xs.copy_(x[:, lo:hi])
+            mask_compact(xs.view(-1), self.mask_id, b["idx"], b["m_dev"], b["compact_scratch"], stream)
+            q = b["idx"][:m]
+            if window is None and not self.shift:
+                rows = q  # flattened positions are the hidden rows
+            else:  # q = seq * Wn + j -> hidden row seq * Ls + src(lo + j), src(p) = max(p - 1, 0) with the shift
+                pos = q % Wn + lo
+                if self.shift:
+                    pos = (pos - 1).clamp_(min=0)
+                rows = self._rows[:m]
+                torch.add(torch.div(q, Wn, rounding_mode="floor") * Ls, pos, out=rows)
+            self._stats(hidden.view(B * Ls, self.d), rows, False, m, S, die, stream)
+            kt = k if isinstance(k, torch.Tensor) else None
+            remask_commit_segmented(b["conf"], q, b["token"], xs.view(-1), m, Wn, B,
+                                    k=0 if kt is not None else int(k), k_per_seg=kt, m_dev=b["m_dev"],
+                                    selected=b["selected"], stream=stream)
+            x[:, lo:hi].copy_(xs)
+        return StepOutput(b["m_dev"], b["idx"][:m], b["token"], b["lse"], b["conf"], b["selected"], lo)
+
     def capture(self, x: torch.Tensor, hidden: torch.Tensor, k: int,
                 window: Optional[tuple[int, int]] = None) -> "torch.cuda.CUDAGraph":
         """Capture one whole step (K1..K5) into a CUDA graph bound to these
@@ -475,42 +540,21 @@ class MaskOnlyHead:
             self._wplans[m_w] = (S_w, die)
         return self._wplans[m_w]
 
-    def step(self, x: torch.Tensor, hidden: torch.Tensor, k: int, stream=None,
-             window: Optional[tuple[int, int]] = None) -> StepOutput:
-        """One step. ``window=(lo, hi)``: only masked positions in [lo, hi) are
-        predicted and only they can be committed (semi-autoregressive block
-        decoding: the current block); everything runs on views of ``x`` /
-        ``hidden``, so [M, V] work and buffers shrink to the window. The
-        returned ``idx`` is then relative to ``lo`` (``StepOutput.offset``)."""
+    def _stats(self, hidden: torch.Tensor, rows: torch.Tensor, shift: bool, m: int, S: int, die, stream) -> None:
+        """K2 + K3 (or gather-mode K3) over the hidden rows ``rows[r]`` (src(p)
+        = p - 1 with ``shift``) of the M compacted rows, then K4 -- through the
+        vocab-shard exchange when the head is sharded -- into token/lse/conf."""
         b = self.buf
-        _req(x, torch.int32, "x", 1)
-        if x.numel() != self.L or hidden.shape[0] != self.L or hidden.shape[1] != self.d:
-            raise InputError("x/hidden do not match the configured sequence length / width")
-        lo, hi = (0, self.L) if window is None else (int(window[0]), int(window[1]))
-        if not 0 <= lo < hi <= self.L:
-            raise InputError(f"window {window} outside [0, {self.L})")
-        shift = self.shift
-        if (lo, hi) != (0, self.L):
-            x = x[lo:hi]
-            if shift and lo > 0:  # src(p) = p - 1 >= lo - 1: the shifted view needs no clamp
-                hidden, shift = hidden[lo - 1:hi - 1], False
-            else:
-                hidden = hidden[lo:hi]
-            m = min(self.m_cap, hi - lo)
-            S, die = self._window_plan(m)
-        else:
-            m, S, die = self.m_cap, self.n_splits, self.die_table
         pmax = b["part_max"].view(-1)[:S * m].view(S, m)
         psum = b["part_sum"].view(-1)[:S * m].view(S, m)
         parg = b["part_arg"].view(-1)[:S * m].view(S, m)
         m_dev = b["m_dev"]
-        mask_compact(x, self.mask_id, b["idx"], m_dev, b["compact_scratch"], stream)
         if self.fused_gather:
-            lmhead_stats_gather(hidden, b["idx"], self.weight, S, pmax, psum, parg, m, m_dev=m_dev, shift=shift,
+            lmhead_stats_gather(hidden, rows, self.weight, S, pmax, psum, parg, m, m_dev=m_dev, shift=shift,
                                 v_offset=self.vocab_offset, stream=stream, die_of_sm=die, sched=b["sched"])
         else:
             hc = b["hc"][:m]
-            gather_rows(hidden, b["idx"], hc, m_dev=m_dev, shift=shift, stream=stream)
+            gather_rows(hidden, rows, hc, m_dev=m_dev, shift=shift, stream=stream)
             lmhead_stats(hc, self.weight, S, pmax, psum, parg, m_dev=m_dev, v_offset=self.vocab_offset,
                          stream=stream, die_of_sm=die, sched=b["sched"])
         if self.group is None and self.p2p is None:
@@ -536,6 +580,34 @@ class MaskOnlyHead:
                 exchange_triples(loc, group=self.group, out=g)  # NCCL all-gather, 12 B/row/rank
             stats_merge(g[0, 0], g[0, 1], g[0, 2].view(torch.int32), self.world, 3 * self.m_cap, m,
                         m_dev=m_dev, token=b["token"], lse=b["lse"], conf=b["conf"], stream=stream)
+
+    def step(self, x: torch.Tensor, hidden: torch.Tensor, k: int, stream=None,
+             window: Optional[tuple[int, int]] = None) -> StepOutput:
+        """One step. ``window=(lo, hi)``: only masked positions in [lo, hi) are
+        predicted and only they can be committed (semi-autoregressive block
+        decoding: the current block); everything runs on views of ``x`` /
+        ``hidden``, so [M, V] work and buffers shrink to the window. The
+        returned ``idx`` is then relative to ``lo`` (``StepOutput.offset``)."""
+        b = self.buf
+        _req(x, torch.int32, "x", 1)
+        if x.numel() != self.L or hidden.shape[0] != self.L or hidden.shape[1] != self.d:
+            raise InputError("x/hidden do not match the configured sequence length / width")
+        lo, hi = (0, self.L) if window is None else (int(window[0]), int(window[1]))
+        if not 0 <= lo < hi <= self.L:
+            raise InputError(f"window {window} outside [0, {self.L})")
+        shift = self.shift
+        if (lo, hi) != (0, self.L):
+            x = x[lo:hi]
+            if shift and lo > 0:  # src(p) = p - 1 >= lo - 1: the shifted view needs no clamp
+                hidden, shift = hidden[lo - 1:hi - 1], False
+            else:
+                hidden = hidden[lo:hi]
+            m = min(self.m_cap, hi - lo)
+            S, die = self._window_plan(m)
+        else:
+            m, S, die = self.m_cap, self.n_splits, self.die_table
+        mask_compact(x, self.mask_id, b["idx"], b["m_dev"], b["compact_scratch"], stream)
+        self._stats(hidden, b["idx"], shift, m, S, die, stream)
         remask_commit(b["conf"], b["idx"], b["token"], int(k), x, b["remask_scratch"], m,
-                      m_dev=m_dev, selected=b["selected"], stream=stream)
-        return StepOutput(m_dev, b["idx"][:m], b["token"], b["lse"], b["conf"], b["selected"], lo)
+                      m_dev=b["m_dev"], selected=b["selected"], stream=stream)
+        return StepOutput(b["m_dev"], b["idx"][:m], b["token"], b["lse"], b["conf"], b["selected"], lo)

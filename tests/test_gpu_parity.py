@@ -693,3 +693,59 @@ def test_windowed_step_semi_autoregressive(dev, L, d, V, lo, hi, shift, gather):
         else:
             assert np.array_equal(xo, first)  # the captured windowed step commits the same tokens
         assert int((xo[lo:hi] != x[lo:hi]).sum()) <= min(k, idx.size)
+
+
+@pytest.mark.parametrize("B,Ls,d,V,window,shift,gather,per_seq_k", [
+    (8, 1024, 512, 16384, None, False, False, False),
+    (8, 1024, 512, 16384, None, True, False, True),
+    (16, 2048, 512, 16384, (512, 544), False, False, True),
+    (16, 2048, 512, 16384, (0, 32), True, True, False),
+    (5, 3000, 1024, 20000, (1000, 1777), True, False, True),
+    (64, 64, 4096, 126464, (32, 64), False, False, False)])
+def test_step_batch_vs_oracle(dev, B, Ls, d, V, window, shift, gather, per_seq_k):
+    """step_batch: B sequences share one LM-head pass and each commits its own
+    k most confident masked positions (segmented K5) -- per sequence equal to
+    the oracle step on that sequence (or its window), everything outside the
+    window untouched."""
+    from paper_2601_06562_b200 import MaskOnlyHead
+
+    rng = np.random.default_rng(B * Ls + d)
+    mask_id = V - 1
+    lo, hi = window if window is not None else (0, Ls)
+    x = rng.integers(0, V - 1, size=(B, Ls)).astype(np.int32)
+    x[rng.random((B, Ls)) < 0.5] = mask_id
+    x[1, lo:hi] = 5  # a sequence with nothing masked in the window
+    H = orc.bf16_round(rng.standard_normal((B, Ls, d)))
+    W = orc.bf16_round(rng.standard_normal((V, d)) * 0.03)
+    ks = rng.integers(0, 12, size=B).astype(np.int32) if per_seq_k else np.full(B, 6, np.int32)
+    head = MaskOnlyHead(bf16_tensor(W, dev), seq_len=B * (hi - lo), mask_id=mask_id, shift=shift,
+                        fused_gather=gather)
+    xd = torch.from_numpy(x).to(dev)
+    Hd = bf16_tensor(H.reshape(B * Ls, d), dev).view(B, Ls, d)
+    k_arg = torch.from_numpy(ks).to(dev) if per_seq_k else 6
+    out = head.step_batch(xd, Hd, k_arg, window=window)
+    torch.cuda.synchronize()
+    xo = xd.cpu().numpy()
+    assert np.array_equal(xo[:, :lo], x[:, :lo]) and np.array_equal(xo[:, hi:], x[:, hi:])
+    M = int(out.m_dev.item())
+    q = out.idx[:M].cpu().numpy()
+    tok, conf = out.token[:M].cpu().numpy(), out.conf[:M].cpu().numpy()
+    sel = out.selected[:M].cpu().numpy().astype(bool)
+    Wn = hi - lo
+    seq_of = q // Wn
+    for bi in range(B):
+        rows = np.flatnonzero(seq_of == bi)
+        p = q[rows] % Wn + lo
+        assert np.array_equal(p, orc.mask_compact(x[bi, lo:hi], mask_id) + lo)
+        if p.size == 0:
+            assert np.array_equal(xo[bi], x[bi])
+            continue
+        src = np.maximum(p - 1, 0) if shift else p
+        ref = orc.softmax_stats(orc.logits_f64(H[bi, src], W))
+        ok = ref["margin"] > MARGIN
+        assert np.array_equal(tok[rows][ok], ref["arg"][ok])
+        assert orc.isclose_rel(conf[rows].astype(np.float64), ref["conf"], CONF_REL)
+        # the segment commits its own k_b, by the rule on the device confidences
+        assert np.array_equal(sel[rows], orc.remask_select(conf[rows], p, int(ks[bi])))
+        assert int(sel[rows].sum()) == min(int(ks[bi]), p.size)
+        assert np.array_equal(xo[bi, p[sel[rows]]], tok[rows][sel[rows]])
