@@ -510,7 +510,8 @@ class MaskOnlyHead:
     def capture(self, x: torch.Tensor, hidden: torch.Tensor, k: int,
                 window: Optional[tuple[int, int]] = None) -> "torch.cuda.CUDAGraph":
         """Capture one whole step (K1..K5) into a CUDA graph bound to these
-        ``x`` / ``hidden`` buffers and this ``k``. Every launch reads the masked
+        ``x`` / ``hidden`` buffers and this ``k`` (a [B, Ls] ``x`` captures
+        :meth:`step_batch`). Every launch reads the masked
         count from the device (K1's output), so one graph serves every step of
         a run whatever M is: refill ``x`` / ``hidden`` in place and ``replay()``.
         Nothing runs during capture (``x`` is untouched until the first replay).
@@ -520,10 +521,21 @@ class MaskOnlyHead:
         g = torch.cuda.CUDAGraph()
         side = torch.cuda.Stream(device=x.device)
         side.wait_stream(torch.cuda.current_stream(x.device))
-        if window is not None:
+        batched = x.dim() == 2  # [B, Ls]: capture step_batch
+        if batched:
+            B, Ls = x.shape
+            lo, hi = (0, Ls) if window is None else window
+            self._window_plan(min(self.m_cap, B * (int(hi) - int(lo))))  # host planning before capture
+            if getattr(self, "_xs", None) is None:  # staging buffers must exist before capture
+                self._xs = torch.empty(self.L, dtype=torch.int32, device=self.weight.device)
+                self._rows = torch.empty(self.m_cap, dtype=torch.int32, device=self.weight.device)
+        elif window is not None:
             self._window_plan(min(self.m_cap, int(window[1]) - int(window[0])))  # host planning before capture
         with torch.cuda.graph(g, stream=side):
-            self.step(x, hidden, k, window=window)
+            if batched:
+                self.step_batch(x, hidden, k, window=window)
+            else:
+                self.step(x, hidden, k, window=window)
         torch.cuda.current_stream(x.device).wait_stream(side)
         return g
 

@@ -749,3 +749,26 @@ def test_step_batch_vs_oracle(dev, B, Ls, d, V, window, shift, gather, per_seq_k
         assert np.array_equal(sel[rows], orc.remask_select(conf[rows], p, int(ks[bi])))
         assert int(sel[rows].sum()) == min(int(ks[bi]), p.size)
         assert np.array_equal(xo[bi, p[sel[rows]]], tok[rows][sel[rows]])
+
+
+def test_step_batch_graph_capture(dev):
+    """A captured step_batch replays to the same commits as the eager call."""
+    from paper_2601_06562_b200 import MaskOnlyHead
+
+    rng = np.random.default_rng(11)
+    B, Ls, d, V, lo, hi = 12, 512, 512, 16384, 128, 160
+    mask_id = V - 1
+    x = rng.integers(0, V - 1, size=(B, Ls)).astype(np.int32)
+    x[:, 100:] = mask_id
+    Hd = bf16_tensor(rng.standard_normal((B * Ls, d)), dev).view(B, Ls, d)
+    W = bf16_tensor(rng.standard_normal((V, d)) * 0.03, dev)
+    head = MaskOnlyHead(W, seq_len=B * (hi - lo), mask_id=mask_id)
+    ks = torch.tensor(rng.integers(0, 9, size=B), dtype=torch.int32, device=dev)
+    xe = torch.from_numpy(x).to(dev)
+    head.step_batch(xe, Hd, ks, window=(lo, hi))
+    xg = torch.from_numpy(x).to(dev)
+    g = head.capture(xg, Hd, ks, window=(lo, hi))
+    g.replay()
+    torch.cuda.synchronize()
+    assert torch.equal(xe, xg)
+    assert not torch.equal(xg, torch.from_numpy(x).to(dev))  # something was committed
