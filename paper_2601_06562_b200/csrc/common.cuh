@@ -276,4 +276,49 @@ __host__ __device__ constexpr uint32_t umma_idesc_bf16(uint32_t M, uint32_t N) {
          | ((M >> 4) << 24);  // M / 16
 }
 
+
+// K4 merge of the S split (or rank) triples of row r, in ascending s -- the
+// fixed order every path uses, so results are bit-identical everywhere.
+// Loads are issued kChunk at a time ahead of the dependent merge chain: with
+// few rows and many splits (a 32-row block against 124 splits) the row loop is
+// latency-bound, and one L2 round trip per split made K4 cost ~70 us.
+__device__ __forceinline__ void merge_triples_row(const float* __restrict__ in_max, const float* __restrict__ in_sum,
+                                                  const int32_t* __restrict__ in_arg, int32_t S, int64_t stride,
+                                                  int64_t r, float& m_out, float& sum_out, int32_t& arg_out) {
+  constexpr int kChunk = 8;
+  float m = -INFINITY, sum = 0.f;
+  int32_t arg = INT32_MAX;
+  for (int s0 = 0; s0 < S; s0 += kChunk) {
+    float mi[kChunk], si[kChunk];
+    int32_t ai[kChunk];
+#pragma unroll
+    for (int j = 0; j < kChunk; ++j) {
+      if (s0 + j < S) {
+        const int64_t o = static_cast<int64_t>(s0 + j) * stride + r;
+        mi[j] = in_max[o];
+        si[j] = in_sum[o];
+        ai[j] = in_arg[o];
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < kChunk; ++j) {
+      if (s0 + j < S) {
+        if (mi[j] > m) {
+          sum = sum * expf(m - mi[j]) + si[j];
+          m = mi[j];
+          arg = ai[j];
+        } else if (mi[j] == m) {
+          sum += si[j];
+          arg = min(arg, ai[j]);
+        } else {
+          sum += si[j] * expf(mi[j] - m);
+        }
+      }
+    }
+  }
+  m_out = m;
+  sum_out = sum;
+  arg_out = arg;
+}
+
 }  // namespace mosaic

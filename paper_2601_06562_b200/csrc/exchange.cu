@@ -41,23 +41,9 @@ __global__ void __launch_bounds__(256)
   const int64_t M = min(static_cast<int64_t>(load_count(m_dev, m_host)), m_cap);
   for (int64_t r = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; r < M;
        r += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-    float m = -INFINITY, sum = 0.f;
-    int32_t arg = INT32_MAX;
-    for (int s = 0; s < S; ++s) {  // the K4 rule, fixed ascending split order
-      const int64_t o = s * stride + r;
-      const float mi = in_max[o], si = in_sum[o];
-      const int32_t ai = in_arg[o];
-      if (mi > m) {
-        sum = sum * expf(m - mi) + si;
-        m = mi;
-        arg = ai;
-      } else if (mi == m) {
-        sum += si;
-        arg = min(arg, ai);
-      } else {
-        sum += si * expf(mi - m);
-      }
-    }
+    float m, sum;
+    int32_t arg;
+    merge_triples_row(in_max, in_sum, in_arg, S, stride, r, m, sum, arg);  // the K4 rule, ascending splits
     // half (epoch & 1) of the double-buffered [2][P][3][m_cap] gathered block:
     // a rank can be at most one step ahead of a peer's merge (its next push
     // needs every rank's signal of this step, which each rank gives only after

@@ -30,29 +30,69 @@ __global__ void k4_merge(const float* __restrict__ in_max, const float* __restri
   const int64_t M = min(static_cast<int64_t>(load_count(m_dev, m_host)), m_cap);
   for (int64_t r = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; r < M;
        r += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-    float m = -INFINITY, sum = 0.f;
-    int32_t arg = INT32_MAX;
-    for (int s = 0; s < S; ++s) {
-      const int64_t o = s * stride + r;
-      const float mi = in_max[o], si = in_sum[o];
-      const int32_t ai = in_arg[o];
-      if (mi > m) {
-        sum = sum * expf(m - mi) + si;
-        m = mi;
-        arg = ai;
-      } else if (mi == m) {
-        sum += si;
-        arg = min(arg, ai);
-      } else {
-        sum += si * expf(mi - m);
-      }
-    }
+    float m, sum;
+    int32_t arg;
+    merge_triples_row(in_max, in_sum, in_arg, S, stride, r, m, sum, arg);
     if (out_max) out_max[r] = m;
     if (out_sum) out_sum[r] = sum;
     if (out_arg) out_arg[r] = arg;
     if (token) token[r] = arg;
     if (lse) lse[r] = m + logf(sum);
     if (conf) conf[r] = 1.f / sum;
+  }
+}
+
+// K4 for few rows and many splits (a decoding block against one split per SM):
+// one warp per row, the lanes load 32 splits' triples at once (one L2 round
+// trip instead of 32), and every lane replays the same ascending-order merge
+// from warp shuffles -- bit-identical to merge_triples_row.
+__global__ void __launch_bounds__(256) k4_merge_warp(const float* __restrict__ in_max, const float* __restrict__ in_sum,
+                                                     const int32_t* __restrict__ in_arg, int32_t S, int64_t stride,
+                                                     const int32_t* __restrict__ m_dev, int64_t m_host, int64_t m_cap,
+                                                     float* __restrict__ out_max, float* __restrict__ out_sum,
+                                                     int32_t* __restrict__ out_arg, int32_t* __restrict__ token,
+                                                     float* __restrict__ lse, float* __restrict__ conf) {
+  const int64_t M = min(static_cast<int64_t>(load_count(m_dev, m_host)), m_cap);
+  const int lane = threadIdx.x & 31;
+  const int64_t warps = static_cast<int64_t>(gridDim.x) * (blockDim.x >> 5);
+  for (int64_t r = blockIdx.x * static_cast<int64_t>(blockDim.x >> 5) + (threadIdx.x >> 5); r < M; r += warps) {
+    float m = -INFINITY, sum = 0.f;
+    int32_t arg = INT32_MAX;
+    for (int s0 = 0; s0 < S; s0 += 32) {
+      const int s = s0 + lane;
+      float mi_l = -INFINITY, si_l = 0.f;
+      int32_t ai_l = INT32_MAX;
+      if (s < S) {
+        const int64_t o = static_cast<int64_t>(s) * stride + r;
+        mi_l = in_max[o];
+        si_l = in_sum[o];
+        ai_l = in_arg[o];
+      }
+      const int n = min(32, S - s0);
+      for (int j = 0; j < n; ++j) {
+        const float mi = __shfl_sync(0xffffffffu, mi_l, j);
+        const float si = __shfl_sync(0xffffffffu, si_l, j);
+        const int32_t ai = __shfl_sync(0xffffffffu, ai_l, j);
+        if (mi > m) {
+          sum = sum * expf(m - mi) + si;
+          m = mi;
+          arg = ai;
+        } else if (mi == m) {
+          sum += si;
+          arg = min(arg, ai);
+        } else {
+          sum += si * expf(mi - m);
+        }
+      }
+    }
+    if (lane == 0) {
+      if (out_max) out_max[r] = m;
+      if (out_sum) out_sum[r] = sum;
+      if (out_arg) out_arg[r] = arg;
+      if (token) token[r] = arg;
+      if (lse) lse[r] = m + logf(sum);
+      if (conf) conf[r] = 1.f / sum;
+    }
   }
 }
 
@@ -275,9 +315,14 @@ extern "C" int mosaic_stats_merge(const float* in_max, const float* in_sum, cons
   MOSAIC_REQUIRE(in_max && in_sum && in_arg, "null partial inputs");
   MOSAIC_REQUIRE(m_dev != nullptr || (m_host >= 0 && m_host <= m_cap), "m_host > m_cap");
   if (m_cap == 0) return MOSAIC_OK;
-  k4_merge<<<grid_for(m_cap, 256), 256, 0, as_stream(stream)>>>(
-      in_max, in_sum, in_arg, S, stride, m_dev, m_host, m_cap, out_max, out_sum, out_arg, token,
-      lse, conf);
+  if (m_cap <= 8192 && S >= 8) {  // few rows, many splits: warp per row (r01i_k5_crossover.txt has the K4 note)
+    k4_merge_warp<<<grid_for(m_cap * 32, 256), 256, 0, as_stream(stream)>>>(
+        in_max, in_sum, in_arg, S, stride, m_dev, m_host, m_cap, out_max, out_sum, out_arg, token, lse, conf);
+  } else {
+    k4_merge<<<grid_for(m_cap, 256), 256, 0, as_stream(stream)>>>(
+        in_max, in_sum, in_arg, S, stride, m_dev, m_host, m_cap, out_max, out_sum, out_arg, token,
+        lse, conf);
+  }
   return check_launch("mosaic_stats_merge");
 }
 
