@@ -200,9 +200,27 @@ __device__ __forceinline__ void select_commit_cta(const float* __restrict__ conf
   __shared__ uint32_t cum[256];
   __shared__ unsigned long long s_prefix;
   __shared__ uint32_t s_krem;
+  __shared__ unsigned long long s_keys[kFusedThreads];
   const int t = threadIdx.x;
   const int64_t M = r1 - r0;
   const int64_t kk = k < M ? k : M;
+  if (M <= kFusedThreads) {
+    // at most one row per thread (decoding blocks, short segments): rank every
+    // key by counting the larger ones -- keys are unique (position tie-break),
+    // so exactly kk ranks fall below kk; one barrier instead of 8 radix passes
+    if (t < M) s_keys[t] = remask_key(conf[r0 + t], pos[r0 + t]);
+    __syncthreads();
+    if (t < M) {
+      const unsigned long long mine = s_keys[t];
+      int64_t rank = 0;
+      for (int64_t j = 0; j < M; ++j) rank += s_keys[j] > mine;
+      const bool sel = rank < kk;
+      const int32_t p = pos[r0 + t];
+      if (sel) x[p] = token[r0 + t];
+      if (selected) selected[r0 + t] = sel ? 1 : 0;
+    }
+    return;
+  }
   if (t == 0) {
     s_prefix = 0ull;
     s_krem = static_cast<uint32_t>(kk > 0 ? kk : 0);
