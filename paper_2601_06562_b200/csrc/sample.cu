@@ -188,6 +188,7 @@ __global__ void __launch_bounds__(256) k5_commit(const float* __restrict__ conf,
 // (M = 16384) the 18 dependent launches cost more than the work.
 constexpr int64_t kFusedRemaskCap = 40960;  // measured crossover (profiles/r01i_k5_crossover.txt)
 constexpr int kFusedThreads = 1024;
+constexpr int kRankCountRows = 256;  // rank-by-counting K5 up to this many rows per segment
 
 // One CTA selects and commits among rows [r0, r1): the k most confident
 // (ties -> lower position), exactly, by an 8-pass radix select of the 64-bit
@@ -200,14 +201,15 @@ __device__ __forceinline__ void select_commit_cta(const float* __restrict__ conf
   __shared__ uint32_t cum[256];
   __shared__ unsigned long long s_prefix;
   __shared__ uint32_t s_krem;
-  __shared__ unsigned long long s_keys[kFusedThreads];
+  __shared__ unsigned long long s_keys[kRankCountRows];
   const int t = threadIdx.x;
   const int64_t M = r1 - r0;
   const int64_t kk = k < M ? k : M;
-  if (M <= kFusedThreads) {
-    // at most one row per thread (decoding blocks, short segments): rank every
-    // key by counting the larger ones -- keys are unique (position tie-break),
-    // so exactly kk ranks fall below kk; one barrier instead of 8 radix passes
+  if (M <= kRankCountRows) {
+    // short segments (decoding blocks): rank every key by counting the larger
+    // ones -- keys are unique (position tie-break), so exactly kk ranks fall
+    // below kk; one barrier instead of 8 radix passes. O(M^2) compares, so
+    // only up to kRankCountRows (at 1024 rows it cost ~60 us more than radix)
     if (t < M) s_keys[t] = remask_key(conf[r0 + t], pos[r0 + t]);
     __syncthreads();
     if (t < M) {

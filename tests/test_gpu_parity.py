@@ -216,7 +216,7 @@ def test_vocab_shards_merge_equals_unsharded(dev):
 
 
 # ----------------------------------------------------------------------- K5
-@pytest.mark.parametrize("M,k", [(1, 1), (10, 0), (10, 10), (10, 25), (1000, 1000), (1024, 32), (1025, 40),
+@pytest.mark.parametrize("M,k", [(1, 1), (10, 0), (10, 10), (10, 25), (256, 17), (257, 18), (1000, 1000), (1024, 32),
                                  (16384, 256), (40960, 640), (40961, 641), (65536, 683),
                                  (524288, 8192)])  # all three K5 paths (rank count, single-CTA radix, grid radix)
 def test_remask_commit_bitexact(dev, M, k):
