@@ -104,7 +104,7 @@ struct Params {
   int32_t seg_splits;  // vocab segments of this many splits, processed segment-major (0 = one segment)
   const uint8_t* die_of_sm;  // die-aware schedule: SM -> L2 die (null = off)
   uint32_t* sched;           // die-aware schedule: [die0 pairs, die1 pairs, registered, decision], zeroed per launch
-  int32_t policy;   // L2 policy of (A, B) loads: 0 = (evict_normal, evict_normal), 1 = (evict_last, evict_normal), 2 = (evict_normal, evict_first)
+  int32_t policy;   // L2 policy of (A, B) loads: 0 = (normal, normal), 1 = (evict_last, normal), 2 = (normal, evict_first), 3 = (evict_last, evict_first)
   int64_t v_offset;
   float* part_max;
   float* part_sum;
@@ -312,8 +312,8 @@ __global__ void __launch_bounds__(kGather == kGatherCpAsync ? kThreadsCpAsync : 
     // ------------------------------------------------------------ TMA producer (both CTAs)
     // A is re-read for every tile of a unit and by the units of its m-group;
     // a W tile is shared by the m-blocks in flight at the same moment.
-    const uint64_t pol_a = p.policy == 1 ? policy_evict_last() : policy_evict_normal();
-    const uint64_t pol_b = p.policy == 2 ? policy_evict_first() : policy_evict_normal();
+    const uint64_t pol_a = (p.policy == 1 || p.policy == 3) ? policy_evict_last() : policy_evict_normal();
+    const uint64_t pol_b = (p.policy == 2 || p.policy == 3) ? policy_evict_first() : policy_evict_normal();
     uint32_t stage = 0, phase = 0;
     for (int64_t u = u_first; u < units_here; u += u_stride) {
       int mb, s;
