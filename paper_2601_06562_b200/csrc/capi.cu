@@ -88,6 +88,14 @@ int encode_tma_bf16(CUtensorMap* map, const void* base, int64_t rows, int64_t K,
   return MOSAIC_OK;
 }
 
+bool pdl_enabled() {
+  static const bool on = [] {
+    const char* e = getenv("MOSAIC_PDL");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
 }  // namespace mosaic
 
 extern "C" int mosaic_abi_version(void) { return 100; }

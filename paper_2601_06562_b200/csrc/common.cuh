@@ -321,4 +321,32 @@ __device__ __forceinline__ void merge_triples_row(const float* __restrict__ in_m
   arg_out = arg;
 }
 
+
+// Programmatic dependent launch (PDL). Hot-path kernels are launched with
+// cudaLaunchAttributeProgrammaticStreamSerialization, so a kernel may be
+// scheduled while its predecessor in the stream is still running; each one
+// calls pdl_wait() before touching memory a predecessor writes (or reads:
+// WAR), and pdl_trigger() once its own prologue no longer needs the SMs to
+// itself. Without the attribute both are no-ops. MOSAIC_PDL=0 turns it off.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
+bool pdl_enabled();
+
+template <typename... KArgs, typename... Args>
+cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t stream,
+                       Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...);
+}
+
 }  // namespace mosaic

@@ -55,6 +55,8 @@ __device__ __forceinline__ int block_sum(int v, int* red) {
 __global__ void __launch_bounds__(kThreads) k1_count(const int32_t* __restrict__ x, int64_t L,
                                                      int32_t mask_id, int32_t* __restrict__ counts) {
   __shared__ int red[kThreads / 32];
+  pdl_wait();  // x may come from the previous step's K5 (PDL, common.cuh)
+  pdl_trigger();
   const int64_t base = static_cast<int64_t>(blockIdx.x) * kTile;
   int c = 0;
 #pragma unroll
@@ -74,6 +76,8 @@ __global__ void __launch_bounds__(kThreads) k1_write(const int32_t* __restrict__
   __shared__ int red[kThreads / 32];
   __shared__ int warp_excl[kThreads / 32 + 1];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  pdl_wait();
+  pdl_trigger();
   // prefix over the tiles before this one (fixed order -> deterministic)
   int before = 0;
   for (int j = threadIdx.x; j < static_cast<int>(blockIdx.x); j += kThreads) before += counts[j];
@@ -120,6 +124,8 @@ __global__ void __launch_bounds__(256) k2_gather(const int4* __restrict__ H, int
                                                  const int32_t* __restrict__ m_dev, int64_t m_host,
                                                  int64_t m_cap, int32_t shift,
                                                  int4* __restrict__ Hc) {
+  pdl_wait();
+  pdl_trigger();
   const int64_t M = min(static_cast<int64_t>(load_count(m_dev, m_host)), m_cap);
   const int lane = threadIdx.x & 31;
   const int64_t warps = static_cast<int64_t>(gridDim.x) * (blockDim.x >> 5);
@@ -165,8 +171,8 @@ extern "C" int mosaic_mask_compact(const int32_t* x, int64_t L, int32_t mask_id,
   }
   const int tiles = static_cast<int>(ceil_div(L, kTile));
   int32_t* counts = static_cast<int32_t*>(scratch);
-  k1_count<<<tiles, kThreads, 0, s>>>(x, L, mask_id, counts);
-  k1_write<<<tiles, kThreads, 0, s>>>(x, L, mask_id, counts, idx_out, m_out);
+  MOSAIC_CUDA(launch_pdl(k1_count, dim3(tiles), dim3(kThreads), 0, s, x, L, mask_id, counts));
+  MOSAIC_CUDA(launch_pdl(k1_write, dim3(tiles), dim3(kThreads), 0, s, x, L, mask_id, counts, idx_out, m_out));
   return check_launch("mosaic_mask_compact");
 }
 
@@ -185,8 +191,8 @@ extern "C" int mosaic_gather_rows(const uint16_t* H, int64_t n_rows, int64_t ld_
   const int64_t rows_per_block = 8;
   const int64_t want = ceil_div(m_cap, rows_per_block);
   const int grid = static_cast<int>(want < num_sms() * 16 ? want : num_sms() * 16);
-  k2_gather<4><<<grid, 256, 0, as_stream(stream)>>>(
-      reinterpret_cast<const int4*>(H), n_rows, ld_h / 8, d / 8, idx, m_dev, m_host, m_cap, shift,
-      reinterpret_cast<int4*>(Hc));
+  MOSAIC_CUDA(launch_pdl(k2_gather<4>, dim3(grid), dim3(256), 0, as_stream(stream),
+                         reinterpret_cast<const int4*>(H), n_rows, ld_h / 8, d / 8, idx, m_dev, m_host, m_cap,
+                         shift, reinterpret_cast<int4*>(Hc)));
   return check_launch("mosaic_gather_rows");
 }

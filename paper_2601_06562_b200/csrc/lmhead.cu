@@ -226,8 +226,6 @@ __global__ void __launch_bounds__(kGather == kGatherCpAsync ? kThreadsCpAsync : 
   const uint32_t rank = CG == 2 ? cluster_ctarank() : 0u;  // position in the SM pair
   const int64_t cluster = blockIdx.x / CG;
   const int64_t n_clusters = gridDim.x / CG;
-  const int64_t M = min(static_cast<int64_t>(load_count(p.m_dev, p.m_host)), p.m_cap);
-  const int m_blocks = static_cast<int>((M + C::ROWS - 1) / C::ROWS);
   const int k_blocks = p.K / BK;
 
   if (warp == 0 && lane == 0) {
@@ -249,6 +247,12 @@ __global__ void __launch_bounds__(kGather == kGatherCpAsync ? kThreadsCpAsync : 
   if constexpr (CG == 2) cluster_sync(); else __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  // PDL: everything above (barriers, TMEM, descriptor prefetch) overlapped the
+  // predecessor's tail; from here on K2's rows and K1's count are read
+  pdl_wait();
+  pdl_trigger();
+  const int64_t M = min(static_cast<int64_t>(load_count(p.m_dev, p.m_host)), p.m_cap);
+  const int m_blocks = static_cast<int>((M + C::ROWS - 1) / C::ROWS);
 
   // Die-aware schedule: the units (in the usual m-group order, so a contiguous
   // unit range covers whole m-groups) are split between the two dies in
@@ -699,13 +703,15 @@ int launch_cg(const CUtensorMap& ta, const CUtensorMap& tb, const Params& p, int
   cfg.blockDim = dim3(kGather == kGatherCpAsync ? kThreadsCpAsync : kThreads);
   cfg.dynamicSmemBytes = C::SMEM;
   cfg.stream = stream;
-  cudaLaunchAttribute attr[1];
+  cudaLaunchAttribute attr[2];
   attr[0].id = cudaLaunchAttributeClusterDimension;
   attr[0].val.clusterDim.x = CG;
   attr[0].val.clusterDim.y = 1;
   attr[0].val.clusterDim.z = 1;
+  attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;  // PDL (common.cuh)
+  attr[1].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
   cfg.attrs = attr;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = 2;
   MOSAIC_CUDA(cudaLaunchKernelEx(&cfg, kern, ta, tb, p));
   return MOSAIC_OK;
 }

@@ -27,6 +27,8 @@ __global__ void k4_merge(const float* __restrict__ in_max, const float* __restri
                          float* __restrict__ out_max, float* __restrict__ out_sum,
                          int32_t* __restrict__ out_arg, int32_t* __restrict__ token,
                          float* __restrict__ lse, float* __restrict__ conf) {
+  pdl_wait();
+  pdl_trigger();
   const int64_t M = min(static_cast<int64_t>(load_count(m_dev, m_host)), m_cap);
   for (int64_t r = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; r < M;
        r += static_cast<int64_t>(gridDim.x) * blockDim.x) {
@@ -52,6 +54,8 @@ __global__ void __launch_bounds__(256) k4_merge_warp(const float* __restrict__ i
                                                      float* __restrict__ out_max, float* __restrict__ out_sum,
                                                      int32_t* __restrict__ out_arg, int32_t* __restrict__ token,
                                                      float* __restrict__ lse, float* __restrict__ conf) {
+  pdl_wait();
+  pdl_trigger();
   const int64_t M = min(static_cast<int64_t>(load_count(m_dev, m_host)), m_cap);
   const int lane = threadIdx.x & 31;
   const int64_t warps = static_cast<int64_t>(gridDim.x) * (blockDim.x >> 5);
@@ -280,6 +284,8 @@ __global__ void __launch_bounds__(kFusedThreads) k5_fused(const float* __restric
                                                           const int32_t* __restrict__ m_dev, int64_t m_host,
                                                           int64_t m_cap, int64_t k, int32_t* __restrict__ x,
                                                           int32_t* __restrict__ selected) {
+  pdl_wait();
+  pdl_trigger();
   const int64_t M = min(static_cast<int64_t>(load_count(m_dev, m_host)), m_cap);
   select_commit_cta(conf, pos, token, 0, M, k, x, selected);
 }
@@ -306,6 +312,8 @@ __global__ void __launch_bounds__(kFusedThreads) k5_segmented(const float* __res
                                                               int32_t* __restrict__ x,
                                                               int32_t* __restrict__ selected) {
   __shared__ int64_t s_bounds[2];
+  pdl_wait();
+  pdl_trigger();
   const int64_t M = min(static_cast<int64_t>(load_count(m_dev, m_host)), m_cap);
   const int64_t b = blockIdx.x;
   if (threadIdx.x < 2) s_bounds[threadIdx.x] = lower_bound_pos(pos, M, (b + threadIdx.x) * seg_len);
@@ -336,12 +344,12 @@ extern "C" int mosaic_stats_merge(const float* in_max, const float* in_sum, cons
   MOSAIC_REQUIRE(m_dev != nullptr || (m_host >= 0 && m_host <= m_cap), "m_host > m_cap");
   if (m_cap == 0) return MOSAIC_OK;
   if (m_cap <= 8192 && S >= 8) {  // few rows, many splits: warp per row (r01i_k5_crossover.txt has the K4 note)
-    k4_merge_warp<<<grid_for(m_cap * 32, 256), 256, 0, as_stream(stream)>>>(
-        in_max, in_sum, in_arg, S, stride, m_dev, m_host, m_cap, out_max, out_sum, out_arg, token, lse, conf);
+    MOSAIC_CUDA(launch_pdl(k4_merge_warp, dim3(grid_for(m_cap * 32, 256)), dim3(256), 0, as_stream(stream), in_max,
+                           in_sum, in_arg, S, stride, m_dev, m_host, m_cap, out_max, out_sum, out_arg, token, lse,
+                           conf));
   } else {
-    k4_merge<<<grid_for(m_cap, 256), 256, 0, as_stream(stream)>>>(
-        in_max, in_sum, in_arg, S, stride, m_dev, m_host, m_cap, out_max, out_sum, out_arg, token,
-        lse, conf);
+    MOSAIC_CUDA(launch_pdl(k4_merge, dim3(grid_for(m_cap, 256)), dim3(256), 0, as_stream(stream), in_max, in_sum,
+                           in_arg, S, stride, m_dev, m_host, m_cap, out_max, out_sum, out_arg, token, lse, conf));
   }
   return check_launch("mosaic_stats_merge");
 }
@@ -362,7 +370,8 @@ extern "C" int mosaic_remask_commit(const float* conf, const int32_t* pos, const
     return e ? static_cast<int64_t>(atoll(e)) : kFusedRemaskCap;
   }();
   if (m_cap <= fused_cap) {
-    k5_fused<<<1, kFusedThreads, 0, s>>>(conf, pos, token, m_dev, m_host, m_cap, k, x, selected);
+    MOSAIC_CUDA(launch_pdl(k5_fused, dim3(1), dim3(kFusedThreads), 0, s, conf, pos, token, m_dev, m_host, m_cap, k,
+                           x, selected));
     return check_launch("mosaic_remask_commit");
   }
   SelectState* st = static_cast<SelectState*>(scratch);
@@ -386,7 +395,7 @@ extern "C" int mosaic_remask_commit_segmented(const float* conf, const int32_t* 
   MOSAIC_REQUIRE(m_dev != nullptr || (m_host >= 0 && m_host <= m_cap), "m_host > m_cap");
   if (m_cap == 0) return MOSAIC_OK;
   MOSAIC_REQUIRE(conf && pos && token && x, "null inputs");
-  k5_segmented<<<n_seg, kFusedThreads, 0, as_stream(stream)>>>(conf, pos, token, m_dev, m_host, m_cap, seg_len,
-                                                                k_per_seg, k, x, selected);
+  MOSAIC_CUDA(launch_pdl(k5_segmented, dim3(n_seg), dim3(kFusedThreads), 0, as_stream(stream), conf, pos, token,
+                         m_dev, m_host, m_cap, seg_len, k_per_seg, k, x, selected));
   return check_launch("mosaic_remask_commit_segmented");
 }
