@@ -146,6 +146,25 @@ MOSAIC_API int mosaic_lmhead_stats_gather_die(const uint16_t* H, int64_t n_rows,
                                    int32_t n_splits, float* part_max, float* part_sum, int32_t* part_arg,
                                    const uint8_t* die_of_sm, uint32_t* sched_scratch, void* stream);
 
+/* Sampling variant of K3 (temperature > 0; the reference's `sample` op is
+ * memory-only, this follows LLaDA's generate): per masked row r the token is
+ * argmax_v (x_v + temperature * g), g = -ln(-ln u), u = ((h >> 9) + 0.5) / 2^23,
+ * h = fmix32(fmix32(pos[r] ^ seed) ^ (v * 0x9E3779B1)) with v the global vocab
+ * id (murmur3 finaliser; so samples do not depend on the split, the vocab
+ * shard or the chunking) -- lowest id on ties. Partials per split: the usual
+ * (max, sum-exp) of the untempered logits, part_arg = the noisy argmax,
+ * part_y = its noisy score, part_x = its raw logit. mosaic_sample_merge gives
+ * token, lse and conf = exp(x_token - lse) (the untempered p(token)).          */
+MOSAIC_API int mosaic_lmhead_sample(const uint16_t* Hc, int64_t m_cap, const int32_t* m_dev, int64_t m_host,
+                         const uint16_t* W, int64_t V_shard, int64_t d, int64_t v_offset,
+                         int32_t n_splits, const int32_t* pos, float temperature, uint32_t seed,
+                         float* part_max, float* part_sum, int32_t* part_arg, float* part_y,
+                         float* part_x, const uint8_t* die_of_sm, uint32_t* sched_scratch, void* stream);
+MOSAIC_API int mosaic_sample_merge(const float* in_max, const float* in_sum, const int32_t* in_arg,
+                        const float* in_y, const float* in_x, int32_t S, int64_t stride,
+                        const int32_t* m_dev, int64_t m_host, int64_t m_cap, int32_t* token,
+                        float* lse, float* conf, void* stream);
+
 /* Debug / parity path for the reference operator itself: out[r, v] =
  * <Hc[r, :], W[v, :]> in fp32, row stride ldo. Materialises the logits like
  * gather_gemm (kernel.py:68); the product path never calls it.               */

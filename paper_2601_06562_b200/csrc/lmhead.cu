@@ -116,6 +116,13 @@ struct Params {
   int64_t ld_h;        // gather mode: H row stride (elements)
   int32_t shift;       // gather mode: src(p) = max(p - 1, 0) (Dream token shift)
   int32_t w_blocked;   // W pre-tiled as [n_tiles][K/64][256][64] (each TMA box contiguous)
+  // sampling variant (temperature > 0): token = argmax_v (x_v + T * g(pos, v)),
+  // g Gumbel noise from a counter-based hash of (seed, position, vocab id)
+  const int32_t* spos;  // masked positions (K1 output), the noise's row key
+  float temperature;
+  uint32_t seed;
+  float* part_y;        // max noisy score per split
+  float* part_x;        // raw logit at that argmax
 };
 
 // Unit order: vocab segments of `seg_splits` consecutive splits, outermost;
@@ -149,6 +156,17 @@ __device__ __forceinline__ void w_box(const Params& p, int t, int kb, int k_bloc
     col = kb * BK;
     row = t * BN + b_rows_off;
   }
+}
+
+// Counter-based noise for the sampling variant (murmur3 finaliser); restated
+// bit for bit in oracle/mosaic_oracle.py (gumbel_u24).
+__device__ __forceinline__ uint32_t fmix32(uint32_t h) {
+  h ^= h >> 16;
+  h *= 0x85EBCA6Bu;
+  h ^= h >> 13;
+  h *= 0xC2B2AE35u;
+  h ^= h >> 16;
+  return h;
 }
 
 __device__ __forceinline__ float fast_exp2(float x) {
@@ -200,7 +218,7 @@ __device__ __forceinline__ void cp_async_arrive_noinc(uint64_t* bar) {
 }
 
 
-template <int CG, bool kStoreLogits, int kGather = kGatherNone>
+template <int CG, bool kStoreLogits, int kGather = kGatherNone, bool kSample = false>
 __global__ void __launch_bounds__(kGather == kGatherCpAsync ? kThreadsCpAsync : kThreads, 1)
     k3_lmhead(const __grid_constant__ CUtensorMap tmap_a, const __grid_constant__ CUtensorMap tmap_b,
               const Params p) {
@@ -538,6 +556,11 @@ __global__ void __launch_bounds__(kGather == kGatherCpAsync ? kThreadsCpAsync : 
       const int64_t row = static_cast<int64_t>(mb) * C::ROWS + rank * BM + row_local;
       float run_max = -INFINITY, run_sum = 0.f;
       int64_t run_arg = 0;
+      float s_ymax = -INFINITY, s_xarg = 0.f;  // sampling variant: noisy max and its raw logit
+      uint32_t row_key = 0;
+      if constexpr (kSample) {
+        if (row < M) row_key = fmix32(static_cast<uint32_t>(__ldg(p.spos + row)) ^ p.seed);
+      }
       for (int t = t0; t < t1; ++t) {
         mbar_wait_sleep(&tfull[acc], acc_phase, MOSAIC_K3_EPI_SLEEP_NS);
         tc_fence_after();
@@ -566,13 +589,15 @@ __global__ void __launch_bounds__(kGather == kGatherCpAsync ? kThreadsCpAsync : 
 #pragma unroll
             for (int j = 1; j < 32; ++j) cmax = fmaxf(cmax, v[j]);
             if (cmax > run_max) {  // strict: earlier columns win ties
-              int jf = 31;
+              if constexpr (!kSample) {  // (the sampling variant's token is the noisy argmax below)
+                int jf = 31;
 #pragma unroll
-              for (int j = 31; j >= 0; --j)
-                if (v[j] == cmax) jf = j;
+                for (int j = 31; j >= 0; --j)
+                  if (v[j] == cmax) jf = j;
+                run_arg = col0 + jf;
+              }
               run_sum *= fast_exp2((run_max - cmax) * kLog2e);
               run_max = cmax;
-              run_arg = col0 + jf;
             }
             const float mb2 = run_max * kLog2e;
             float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
@@ -584,6 +609,25 @@ __global__ void __launch_bounds__(kGather == kGatherCpAsync ? kThreadsCpAsync : 
               s3 += fast_exp2(fmaf(v[j + 3], kLog2e, -mb2));
             }
             run_sum += (s0 + s1) + (s2 + s3);
+            if constexpr (kSample) {
+              // y = x + T * g, g = -ln(-ln u), u from (seed, position, global vocab id);
+              // strict > in ascending columns: the lowest id wins ties
+              const uint32_t cg0 = static_cast<uint32_t>(p.v_offset + col0);
+#pragma unroll
+              for (int j = 0; j < 32; ++j) {
+                const uint32_t h = fmix32(row_key ^ (cg0 + j) * 0x9E3779B1u);
+                // u = (h23 + 0.5) / 2^23 is exact in fp32 and strictly inside (0, 1); the inner log
+                // is the accurate logf (u can sit within 2^-24 of 1), the outer one the fast MUFU form
+                const float u = (static_cast<float>(h >> 9) + 0.5f) * 1.1920928955078125e-7f;
+                const float g = -__logf(-logf(u));
+                const float y = fmaf(p.temperature, g, v[j]);
+                if (y > s_ymax) {  // v[j] = -inf past the vocab tail: never chosen
+                  s_ymax = y;
+                  s_xarg = v[j];
+                  run_arg = col0 + j;
+                }
+              }
+            }
           }
         }
         tc_fence_before();
@@ -602,7 +646,11 @@ __global__ void __launch_bounds__(kGather == kGatherCpAsync ? kThreadsCpAsync : 
           const int64_t o = static_cast<int64_t>(s) * p.m_cap + row;
           p.part_max[o] = run_max;
           p.part_sum[o] = run_sum;
-          p.part_arg[o] = static_cast<int32_t>(p.v_offset + run_arg);
+          p.part_arg[o] = static_cast<int32_t>(p.v_offset + run_arg);  // sampling: the noisy argmax
+          if constexpr (kSample) {
+            p.part_y[o] = s_ymax;
+            p.part_x[o] = s_xarg;
+          }
         }
       }
     }
@@ -684,11 +732,11 @@ void plan_splits(int64_t m_cap, int64_t V, int32_t* n_splits, int32_t* tps) {
   *n_splits = static_cast<int32_t>(ceil_div(n_tiles, best_tps));
 }
 
-template <int CG, bool kStore, int kGather>
+template <int CG, bool kStore, int kGather, bool kSample = false>
 int launch_cg(const CUtensorMap& ta, const CUtensorMap& tb, const Params& p, int64_t m_cap,
               cudaStream_t stream) {
   using C = Cfg<CG>;
-  auto kern = k3_lmhead<CG, kStore, kGather>;
+  auto kern = k3_lmhead<CG, kStore, kGather, kSample>;
   static bool attr_set = false;  // per instantiation
   if (!attr_set) {
     MOSAIC_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
@@ -782,8 +830,13 @@ int launch(const ASource& a, int64_t m_cap, const int32_t* m_dev, int64_t m_host
                    : launch_cg<1, false, kGatherCpAsync>(ta, tb, p, m_cap, s);
     }
   } else {
-    st = cg == 2 ? launch_cg<2, kStore, kGatherNone>(ta, tb, p, m_cap, s)
-                 : launch_cg<1, kStore, kGatherNone>(ta, tb, p, m_cap, s);
+    if (p.part_y != nullptr) {  // sampling variant (buffered A only)
+      st = cg == 2 ? launch_cg<2, false, kGatherNone, true>(ta, tb, p, m_cap, s)
+                   : launch_cg<1, false, kGatherNone, true>(ta, tb, p, m_cap, s);
+    } else {
+      st = cg == 2 ? launch_cg<2, kStore, kGatherNone>(ta, tb, p, m_cap, s)
+                   : launch_cg<1, kStore, kGatherNone>(ta, tb, p, m_cap, s);
+    }
   }
   if (st) return st;
   return check_launch(kStore ? "mosaic_lmhead_logits" : "mosaic_lmhead_stats");
@@ -839,6 +892,38 @@ extern "C" int mosaic_lmhead_stats_die(const uint16_t* Hc, int64_t m_cap, const 
   p.part_max = part_max;
   p.part_sum = part_sum;
   p.part_arg = part_arg;
+  p.die_of_sm = die_of_sm;
+  p.sched = sched_scratch;
+  return launch<false>(ASource{Hc, m_cap, d, nullptr, 0}, m_cap, m_dev, m_host, W, V_shard, d, p, stream);
+}
+
+extern "C" int mosaic_lmhead_sample(const uint16_t* Hc, int64_t m_cap, const int32_t* m_dev, int64_t m_host,
+                                    const uint16_t* W, int64_t V_shard, int64_t d, int64_t v_offset,
+                                    int32_t n_splits, const int32_t* pos, float temperature, uint32_t seed,
+                                    float* part_max, float* part_sum, int32_t* part_arg, float* part_y,
+                                    float* part_x, const uint8_t* die_of_sm, uint32_t* sched_scratch,
+                                    void* stream) {
+  MOSAIC_REQUIRE(part_max && part_sum && part_arg && part_y && part_x && pos, "null operands");
+  MOSAIC_REQUIRE(temperature > 0.f && temperature < 1e30f, "temperature must be positive (0 = argmax: use "
+                 "mosaic_lmhead_stats)");
+  MOSAIC_REQUIRE(die_of_sm == nullptr || sched_scratch != nullptr, "die-aware schedule needs its scratch");
+  const int64_t n_tiles = ceil_div(V_shard, BN);
+  MOSAIC_REQUIRE(n_splits >= 1 && n_splits <= n_tiles, "n_splits=%d not in [1, %lld]", n_splits,
+                 (long long)n_tiles);
+  Params p{};
+  p.tiles_per_split = static_cast<int32_t>(ceil_div(n_tiles, n_splits));
+  p.n_splits = static_cast<int32_t>(ceil_div(n_tiles, p.tiles_per_split));
+  MOSAIC_REQUIRE(p.n_splits == n_splits, "n_splits=%d does not tile %lld vocab tiles evenly; use mosaic_lmhead_plan",
+                 n_splits, (long long)n_tiles);
+  p.v_offset = v_offset;
+  p.part_max = part_max;
+  p.part_sum = part_sum;
+  p.part_arg = part_arg;
+  p.part_y = part_y;
+  p.part_x = part_x;
+  p.spos = pos;
+  p.temperature = temperature;
+  p.seed = seed;
   p.die_of_sm = die_of_sm;
   p.sched = sched_scratch;
   return launch<false>(ASource{Hc, m_cap, d, nullptr, 0}, m_cap, m_dev, m_host, W, V_shard, d, p, stream);

@@ -100,6 +100,43 @@ __global__ void __launch_bounds__(256) k4_merge_warp(const float* __restrict__ i
   }
 }
 
+// K4 for the sampling variant: (max, sum) merge as merge_triples_row; the
+// token is the noisy argmax (larger noisy score wins, lower vocab id on ties)
+// and conf = p(token) under the untempered logits = exp(x_token - lse), as
+// LLaDA's generate scores a sampled token.
+__global__ void __launch_bounds__(256) k4_sample_merge(const float* __restrict__ in_max, const float* __restrict__ in_sum,
+                                                       const int32_t* __restrict__ in_arg,
+                                                       const float* __restrict__ in_y, const float* __restrict__ in_x,
+                                                       int32_t S, int64_t stride, const int32_t* __restrict__ m_dev,
+                                                       int64_t m_host, int64_t m_cap, int32_t* __restrict__ token,
+                                                       float* __restrict__ lse, float* __restrict__ conf) {
+  pdl_wait();
+  pdl_trigger();
+  const int64_t M = min(static_cast<int64_t>(load_count(m_dev, m_host)), m_cap);
+  for (int64_t r = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; r < M;
+       r += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    float m, sum;
+    int32_t unused;
+    merge_triples_row(in_max, in_sum, in_arg, S, stride, r, m, sum, unused);
+    float ybest = -INFINITY, xbest = -INFINITY;
+    int32_t abest = INT32_MAX;
+    for (int s = 0; s < S; ++s) {
+      const int64_t o = static_cast<int64_t>(s) * stride + r;
+      const float y = in_y[o];
+      const int32_t a = in_arg[o];
+      if (y > ybest || (y == ybest && a < abest)) {
+        ybest = y;
+        abest = a;
+        xbest = in_x[o];
+      }
+    }
+    const float l = m + logf(sum);
+    token[r] = abest;
+    if (lse) lse[r] = l;
+    conf[r] = expf(xbest - l);
+  }
+}
+
 struct SelectState {
   unsigned long long prefix;
   uint32_t k_rem;
@@ -398,4 +435,16 @@ extern "C" int mosaic_remask_commit_segmented(const float* conf, const int32_t* 
   MOSAIC_CUDA(launch_pdl(k5_segmented, dim3(n_seg), dim3(kFusedThreads), 0, as_stream(stream), conf, pos, token,
                          m_dev, m_host, m_cap, seg_len, k_per_seg, k, x, selected));
   return check_launch("mosaic_remask_commit_segmented");
+}
+
+extern "C" int mosaic_sample_merge(const float* in_max, const float* in_sum, const int32_t* in_arg, const float* in_y,
+                                   const float* in_x, int32_t S, int64_t stride, const int32_t* m_dev, int64_t m_host,
+                                   int64_t m_cap, int32_t* token, float* lse, float* conf, void* stream) {
+  MOSAIC_REQUIRE(S >= 1 && stride >= m_cap, "bad split layout");
+  MOSAIC_REQUIRE(in_max && in_sum && in_arg && in_y && in_x && token && conf, "null operands");
+  MOSAIC_REQUIRE(m_dev != nullptr || (m_host >= 0 && m_host <= m_cap), "m_host > m_cap");
+  if (m_cap == 0) return MOSAIC_OK;
+  MOSAIC_CUDA(launch_pdl(k4_sample_merge, dim3(grid_for(m_cap, 256)), dim3(256), 0, as_stream(stream), in_max, in_sum,
+                         in_arg, in_y, in_x, S, stride, m_dev, m_host, m_cap, token, lse, conf));
+  return check_launch("mosaic_sample_merge");
 }

@@ -102,6 +102,39 @@ def lmhead_plan(m_cap: int, v_shard: int, d: int, max_splits: Optional[int] = No
     return S, tps
 
 
+def lmhead_sample(hc: torch.Tensor, weight: torch.Tensor, n_splits: int, pos: torch.Tensor, temperature: float,
+                  seed: int, part_max, part_sum, part_arg, part_y, part_x, m_dev=None, m_host: int = 0,
+                  v_offset: int = 0, stream=None, die_of_sm: Optional[torch.Tensor] = None,
+                  sched: Optional[torch.Tensor] = None) -> None:
+    """K3's sampling variant (mosaic_lmhead_sample): per split the untempered
+    (max, sum-exp) plus the Gumbel-max token over x + T * g(seed, pos, v)."""
+    _req(hc, torch.bfloat16, "hc", 2)
+    _req(weight, torch.bfloat16, "weight", 2)
+    _req(pos, torch.int32, "pos", 1)
+    m_cap, d = hc.shape
+    if weight.shape[1] != d or hc.stride(0) != d or weight.stride(0) != d:
+        raise InputError("hc [m, d] and weight [V, d] must be contiguous with the same d")
+    for t, dt, n in ((part_max, torch.float32, "part_max"), (part_sum, torch.float32, "part_sum"),
+                     (part_arg, torch.int32, "part_arg"), (part_y, torch.float32, "part_y"),
+                     (part_x, torch.float32, "part_x")):
+        _req(t, dt, n)
+        if t.numel() < n_splits * m_cap:
+            raise InputError(f"{n} must hold n_splits*m_cap entries")
+    if die_of_sm is not None and (sched is None or sched.numel() * sched.element_size() < 16):
+        raise InputError("the die-aware schedule needs a 16-byte sched scratch")
+    _native.call("mosaic_lmhead_sample", _p(hc), m_cap, _p(m_dev), int(m_host), _p(weight), weight.shape[0], d,
+                 int(v_offset), int(n_splits), _p(pos), ctypes.c_float(float(temperature)),
+                 ctypes.c_uint32(int(seed) & 0xFFFFFFFF), _p(part_max), _p(part_sum), _p(part_arg), _p(part_y),
+                 _p(part_x), _p(die_of_sm), _p(sched if die_of_sm is not None else None), _s(stream))
+
+
+def sample_merge(part_max, part_sum, part_arg, part_y, part_x, S: int, stride: int, m_cap: int, token, conf,
+                 lse=None, m_dev=None, m_host: int = 0, stream=None) -> None:
+    """K4 of the sampling variant: token = noisy argmax, conf = untempered p(token)."""
+    _native.call("mosaic_sample_merge", _p(part_max), _p(part_sum), _p(part_arg), _p(part_y), _p(part_x), int(S),
+                 int(stride), _p(m_dev), int(m_host), int(m_cap), _p(token), _p(lse), _p(conf), _s(stream))
+
+
 _DIE_MAPS: dict = {}
 
 
@@ -396,7 +429,7 @@ class MaskOnlyHead:
     def __init__(self, weight_shard: torch.Tensor, *, seq_len: int, mask_id: int,
                  vocab_offset: int = 0, m_cap: Optional[int] = None, shift: bool = False,
                  group=None, block: Optional[torch.Tensor] = None, fused_gather: bool = False,
-                 exchange="nccl", die_aware: Optional[bool] = None):
+                 exchange="nccl", die_aware: Optional[bool] = None, temperature: float = 0.0, seed: int = 0):
         _req(weight_shard, torch.bfloat16, "weight_shard", 2)
         self.weight = weight_shard
         self.v_shard, self.d = weight_shard.shape
@@ -407,6 +440,15 @@ class MaskOnlyHead:
         self.shift = bool(shift)
         self.group = group
         self.fused_gather = bool(fused_gather)  # K3 reads rows of `hidden` directly: no K2, no hc buffer
+        # temperature > 0: Gumbel-max sampling in K3's epilogue (LLaDA generate's sampler), one fresh
+        # noise draw per step from (seed, step counter); single-process, buffered A path
+        self.temperature = float(temperature)
+        self.seed = int(seed)
+        self._steps = 0
+        if self.temperature < 0:
+            raise InputError("temperature must be >= 0")
+        if self.temperature > 0 and (group is not None or hasattr(exchange, "push") or self.fused_gather):
+            raise InputError("sampling (temperature > 0) runs on single-process heads with the buffered A path")
         self._die_aware = die_aware
         self._wplans: dict = {}
         self.die_table = (die_map(weight_shard.device)[0]
@@ -429,6 +471,9 @@ class MaskOnlyHead:
         lay.add("part_max", (S, m), torch.float32)
         lay.add("part_sum", (S, m), torch.float32)
         lay.add("part_arg", (S, m), torch.int32)
+        if self.temperature > 0:
+            lay.add("part_y", (S, m), torch.float32)
+            lay.add("part_x", (S, m), torch.float32)
         if group is not None:  # the exchange path runs whenever a process group is given (even P = 1)
             lay.add("local", (3, m), torch.float32)     # merged (max, sum, arg-bits) of this shard
             lay.add("gathered", (P, 3, m), torch.float32)
@@ -518,6 +563,8 @@ class MaskOnlyHead:
         Single-process heads only (the exchange paths are not captured)."""
         if self.group is not None or self.p2p is not None:
             raise InputError("graph capture is for single-process heads")
+        if self.temperature > 0:
+            raise InputError("a captured sampling step would replay the same noise every step: use step()")
         g = torch.cuda.CUDAGraph()
         side = torch.cuda.Stream(device=x.device)
         side.wait_stream(torch.cuda.current_stream(x.device))
@@ -564,6 +611,18 @@ class MaskOnlyHead:
         if self.fused_gather:
             lmhead_stats_gather(hidden, rows, self.weight, S, pmax, psum, parg, m, m_dev=m_dev, shift=shift,
                                 v_offset=self.vocab_offset, stream=stream, die_of_sm=die, sched=b["sched"])
+        elif self.temperature > 0:  # Gumbel-max sampling in K3's epilogue, noise keyed by rows[r]
+            hc = b["hc"][:m]
+            gather_rows(hidden, rows, hc, m_dev=m_dev, shift=shift, stream=stream)
+            py = b["part_y"].view(-1)[:S * m].view(S, m)
+            px = b["part_x"].view(-1)[:S * m].view(S, m)
+            seed = (self.seed * 0x9E3779B1 + self._steps * 0x85EBCA6B + 0x27D4EB2F) & 0xFFFFFFFF
+            self._steps += 1
+            lmhead_sample(hc, self.weight, S, rows, self.temperature, seed, pmax, psum, parg, py, px, m_dev=m_dev,
+                          v_offset=self.vocab_offset, stream=stream, die_of_sm=die, sched=b["sched"])
+            sample_merge(pmax, psum, parg, py, px, S, m, m, b["token"], b["conf"], lse=b["lse"], m_dev=m_dev,
+                         stream=stream)
+            return
         else:
             hc = b["hc"][:m]
             gather_rows(hidden, rows, hc, m_dev=m_dev, shift=shift, stream=stream)
