@@ -23,6 +23,7 @@ Bx = torch.from_numpy(np.stack([x[:1000], x[1000:2000], x[2000:3000]])).to(dev)
 bh = MaskOnlyHead(W, seq_len=3 * 100, mask_id=mid, shift=True)
 bh.step_batch(Bx, H[:3000].reshape(3, 1000, d).contiguous(), torch.tensor([3, 0, 7], dtype=torch.int32, device=dev),
               window=(400, 500))
+MaskOnlyHead(W, seq_len=L, mask_id=mid, temperature=0.7, seed=3).step(torch.from_numpy(x).to(dev), H, 9)
 head = MaskOnlyHead(W, seq_len=L, mask_id=mid, m_cap=100)  # M <= 128 -> cta_group::1
 xs = x.copy(); xs[:] = 1; xs[:90] = mid
 head.step(torch.from_numpy(xs).to(dev), H, 10)
