@@ -854,3 +854,33 @@ def test_sampling_shard_invariant_and_distribution(dev):
     p /= p.sum()
     freq = np.bincount(outs[0][0], minlength=V) / M
     assert np.abs(freq - p).max() < 0.02  # M = 8192 draws: ~4 sigma for the largest p
+
+
+def test_step_batch_sampling(dev):
+    """Sampling inside a batched step: noise keyed by the hidden row b * Ls + p,
+    so each sequence draws its own noise; tokens equal the oracle's Gumbel-max
+    sample per sequence (margin rule) and each sequence commits its own k."""
+    from paper_2601_06562_b200 import MaskOnlyHead
+
+    rng = np.random.default_rng(21)
+    B, Ls, d, V, lo, hi, T, k = 6, 700, 512, 9000, 100, 164, 0.8, 5
+    mask_id = V - 1
+    x = rng.integers(0, V - 1, size=(B, Ls)).astype(np.int32)
+    x[rng.random((B, Ls)) < 0.6] = mask_id
+    H = orc.bf16_round(rng.standard_normal((B, Ls, d)))
+    W = orc.bf16_round(rng.standard_normal((V, d)) * 0.05)
+    head = MaskOnlyHead(bf16_tensor(W, dev), seq_len=B * (hi - lo), mask_id=mask_id, temperature=T, seed=9)
+    xd = torch.from_numpy(x).to(dev)
+    out = head.step_batch(xd, bf16_tensor(H.reshape(B * Ls, d), dev).view(B, Ls, d), k, window=(lo, hi))
+    torch.cuda.synchronize()
+    M = int(out.m_dev.item())
+    q = out.idx[:M].cpu().numpy()
+    tok, sel = out.token[:M].cpu().numpy(), out.selected[:M].cpu().numpy().astype(bool)
+    Wn = hi - lo
+    for bi in range(B):
+        rows = np.flatnonzero(q // Wn == bi)
+        p = q[rows] % Wn + lo
+        ref = orc.sample_stats(orc.logits_f64(H[bi, p], W), bi * Ls + p, _step_seed(9, 0), T)
+        ok = ref["margin"] > 1e-3
+        assert np.array_equal(tok[rows][ok], ref["arg"][ok])
+        assert int(sel[rows].sum()) == min(k, rows.size)
