@@ -54,6 +54,22 @@ while n < args.iters and time.time() - t0 < args.seconds:
         if not all(torch.equal(a, b) for a, b in zip(ref, o)):
             mismatches += 1
             print(f"MISMATCH iter {n} shape {(L, d, V)} shift {shift} variant {i}", flush=True)
+    # sampling variant: default vs die-aware schedule, same seed -> same bits
+    if n % 4 == 0:
+        souts = []
+        for die in (False, True):
+            key = ("sample", die, shift)
+            if key not in hv:
+                hv[key] = MaskOnlyHead(W, seq_len=L, mask_id=mask_id, shift=shift, die_aware=die, temperature=0.7,
+                                       seed=5)
+            hv[key]._steps = n  # same per-step seed on both heads
+            x = x0.clone()
+            o = hv[key].step(x, H, 64)
+            M = int(o.m_dev.item())
+            souts.append((x, o.token[:M].clone(), o.conf[:M].clone()))
+        if not all(torch.equal(a, b) for a, b in zip(*souts)):
+            mismatches += 1
+            print(f"MISMATCH (sampling) iter {n} shape {(L, d, V)}", flush=True)
     n += 1
 torch.cuda.synchronize()
 print(f"soak: {n} iterations x 4 variants in {time.time() - t0:.0f} s, mismatches {mismatches}")
