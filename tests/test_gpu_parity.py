@@ -854,6 +854,20 @@ def test_sampling_shard_invariant_and_distribution(dev):
     p /= p.sum()
     freq = np.bincount(outs[0][0], minlength=V) / M
     assert np.abs(freq - p).max() < 0.02  # M = 8192 draws: ~4 sigma for the largest p
+    # T = 0.5 samples softmax(x / T)
+    S, _ = hotpath.lmhead_plan(M, V, d)
+    bufs = [torch.empty(S, M, device=dev) for _ in range(4)]
+    pa = torch.empty(S, M, dtype=torch.int32, device=dev)
+    hotpath.lmhead_sample(Hc, W, S, pos, 0.5, 99, bufs[0], bufs[1], pa, bufs[2], bufs[3], m_host=M)
+    tok = torch.empty(M, dtype=torch.int32, device=dev)
+    conf = torch.empty(M, device=dev)
+    hotpath.sample_merge(bufs[0], bufs[1], pa, bufs[2], bufs[3], S, M, M, tok, conf, m_host=M)
+    torch.cuda.synchronize()
+    pT = np.exp((z[0] - z[0].max()) / 0.5)
+    pT /= pT.sum()
+    freqT = np.bincount(tok.cpu().numpy(), minlength=V) / M
+    assert np.abs(freqT - pT).max() < 0.025
+    assert np.allclose(conf.cpu().numpy(), p[tok.cpu().numpy()], rtol=1e-3)  # conf is the untempered p
 
 
 def test_step_batch_sampling(dev):
