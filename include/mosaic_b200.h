@@ -153,8 +153,10 @@ MOSAIC_API int mosaic_lmhead_stats_gather_die(const uint16_t* H, int64_t n_rows,
  * id (murmur3 finaliser; so samples do not depend on the split, the vocab
  * shard or the chunking) -- lowest id on ties. Partials per split: the usual
  * (max, sum-exp) of the untempered logits, part_arg = the noisy argmax,
- * part_y = its noisy score, part_x = its raw logit. mosaic_sample_merge gives
- * token, lse and conf = exp(x_token - lse) (the untempered p(token)).          */
+ * part_y = its noisy score, part_x = its raw logit; every partial buffer holds
+ * 2 * n_splits * m_cap entries (each split's two 128-column halves are written
+ * separately: merge with S = 2 * n_splits). mosaic_sample_merge gives token,
+ * lse and conf = exp(x_token - lse) (the untempered p(token)).                */
 MOSAIC_API int mosaic_lmhead_sample(const uint16_t* Hc, int64_t m_cap, const int32_t* m_dev, int64_t m_host,
                          const uint16_t* W, int64_t V_shard, int64_t d, int64_t v_offset,
                          int32_t n_splits, const int32_t* pos, float temperature, uint32_t seed,

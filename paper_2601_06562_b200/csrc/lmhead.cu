@@ -53,6 +53,14 @@ static_assert(kTmaRows % 4 == 0 && kTmaRows + kRowsPerAWarp * kAWarps == BM, "ga
 static_assert(kRowsPerAWarp % 4 == 0 && kRowsPerAWarp <= 32, "loader warp covers 4-row groups");
 constexpr int kThreadsCpAsync = kThreads + (kAWarps - 1) * 32;
 constexpr int kEpiWarps = 4;
+// The sampling variant's epilogue (hash + two logs per logit) runs 8 epilogue
+// warps: warps 2-5 take the first 128 columns of each tile, warps 6-9 the last
+// 128 (each warp still owns one TMEM lane quarter), and each half writes its
+// own partial, so the split count doubles for K4.
+constexpr int kSampleHalves = 2;
+constexpr int threads_for(int gather, bool sample) {
+  return gather == 2 ? kThreadsCpAsync : (sample ? kThreads + kEpiWarps * 32 : kThreads);
+}
 constexpr int kMaxSplits = 64;
 #ifndef MOSAIC_K3_EPI_SLEEP_NS
 #define MOSAIC_K3_EPI_SLEEP_NS 0   // epilogue poll backoff while the next accumulator fills
@@ -219,7 +227,7 @@ __device__ __forceinline__ void cp_async_arrive_noinc(uint64_t* bar) {
 
 
 template <int CG, bool kStoreLogits, int kGather = kGatherNone, bool kSample = false>
-__global__ void __launch_bounds__(kGather == kGatherCpAsync ? kThreadsCpAsync : kThreads, 1)
+__global__ void __launch_bounds__(threads_for(kGather, kSample), 1)
     k3_lmhead(const __grid_constant__ CUtensorMap tmap_a, const __grid_constant__ CUtensorMap tmap_b,
               const Params p) {
   using C = Cfg<CG>;
@@ -256,7 +264,7 @@ __global__ void __launch_bounds__(kGather == kGatherCpAsync ? kThreadsCpAsync : 
     }
     for (int i = 0; i < NUM_ACC; ++i) {
       mbar_init(&tfull[i], 1);
-      mbar_init(&tempty[i], kEpiWarps * CG);  // one arrive per epilogue warp of the pair
+      mbar_init(&tempty[i], kEpiWarps * (kSample ? kSampleHalves : 1) * CG);  // one arrive per epilogue warp of the pair
     }
     fence_mbar_init();
   }
@@ -545,6 +553,9 @@ __global__ void __launch_bounds__(kGather == kGatherCpAsync ? kThreadsCpAsync : 
     // ------------------------------------------------------------ epilogue (both CTAs)
     const int q = warp & 3;  // TMEM lane quarter accessible to this warp
     const int row_local = q * 32 + lane;
+    constexpr int kHalves = kSample ? kSampleHalves : 1;
+    const int half = (kSample && warp >= 2 + kEpiWarps) ? 1 : 0;  // sampling: which 128 columns of each tile
+    constexpr int kChunksPerHalf = BN / 32 / kHalves;
     // tempty lives in the pair leader: arrive locally or through the cluster window
     const uint32_t tempty_addr0 = CG == 2 ? mapa_shared(smem_u32(&tempty[0]), 0) : smem_u32(&tempty[0]);
     uint32_t acc = 0, acc_phase = 0;
@@ -567,7 +578,7 @@ __global__ void __launch_bounds__(kGather == kGatherCpAsync ? kThreadsCpAsync : 
         const uint32_t taddr = tmem_base + (static_cast<uint32_t>(q * 32) << 16) + acc * BN;
         const int64_t col_base = static_cast<int64_t>(t) * BN;
 #pragma unroll 1
-        for (int c = 0; c < BN / 32; ++c) {
+        for (int c = half * kChunksPerHalf; c < (half + 1) * kChunksPerHalf; ++c) {
           const int64_t col0 = col_base + c * 32;
           if (col0 >= p.V) break;  // warp-uniform: vocab tail
           float v[32];
@@ -643,7 +654,7 @@ __global__ void __launch_bounds__(kGather == kGatherCpAsync ? kThreadsCpAsync : 
       }
       if constexpr (!kStoreLogits) {
         if (row < M) {
-          const int64_t o = static_cast<int64_t>(s) * p.m_cap + row;
+          const int64_t o = (static_cast<int64_t>(s) * kHalves + half) * p.m_cap + row;
           p.part_max[o] = run_max;
           p.part_sum[o] = run_sum;
           p.part_arg[o] = static_cast<int32_t>(p.v_offset + run_arg);  // sampling: the noisy argmax
@@ -748,7 +759,7 @@ int launch_cg(const CUtensorMap& ta, const CUtensorMap& tb, const Params& p, int
   const int64_t clusters = units_cap < workers ? units_cap : workers;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(static_cast<unsigned>(clusters * CG));
-  cfg.blockDim = dim3(kGather == kGatherCpAsync ? kThreadsCpAsync : kThreads);
+  cfg.blockDim = dim3(threads_for(kGather, kSample));
   cfg.dynamicSmemBytes = C::SMEM;
   cfg.stream = stream;
   cudaLaunchAttribute attr[2];

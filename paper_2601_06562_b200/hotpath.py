@@ -106,8 +106,9 @@ def lmhead_sample(hc: torch.Tensor, weight: torch.Tensor, n_splits: int, pos: to
                   seed: int, part_max, part_sum, part_arg, part_y, part_x, m_dev=None, m_host: int = 0,
                   v_offset: int = 0, stream=None, die_of_sm: Optional[torch.Tensor] = None,
                   sched: Optional[torch.Tensor] = None) -> None:
-    """K3's sampling variant (mosaic_lmhead_sample): per split the untempered
-    (max, sum-exp) plus the Gumbel-max token over x + T * g(seed, pos, v)."""
+    """K3's sampling variant (mosaic_lmhead_sample): per split and 128-column
+    half the untempered (max, sum-exp) plus the Gumbel-max token over
+    x + T * g(seed, pos, v); partials hold 2 * n_splits rows (merge S = 2 n_splits)."""
     _req(hc, torch.bfloat16, "hc", 2)
     _req(weight, torch.bfloat16, "weight", 2)
     _req(pos, torch.int32, "pos", 1)
@@ -118,8 +119,8 @@ def lmhead_sample(hc: torch.Tensor, weight: torch.Tensor, n_splits: int, pos: to
                      (part_arg, torch.int32, "part_arg"), (part_y, torch.float32, "part_y"),
                      (part_x, torch.float32, "part_x")):
         _req(t, dt, n)
-        if t.numel() < n_splits * m_cap:
-            raise InputError(f"{n} must hold n_splits*m_cap entries")
+        if t.numel() < 2 * n_splits * m_cap:
+            raise InputError(f"{n} must hold 2*n_splits*m_cap entries (two column halves per split)")
     if die_of_sm is not None and (sched is None or sched.numel() * sched.element_size() < 16):
         raise InputError("the die-aware schedule needs a 16-byte sched scratch")
     _native.call("mosaic_lmhead_sample", _p(hc), m_cap, _p(m_dev), int(m_host), _p(weight), weight.shape[0], d,
@@ -468,12 +469,13 @@ class MaskOnlyHead:
         lay.add("compact_scratch", (mask_compact_scratch_bytes(self.L),), torch.uint8)
         if not self.fused_gather:
             lay.add("hc", (m, self.d), torch.bfloat16)
-        lay.add("part_max", (S, m), torch.float32)
-        lay.add("part_sum", (S, m), torch.float32)
-        lay.add("part_arg", (S, m), torch.int32)
+        Sp = 2 * S if self.temperature > 0 else S  # the sampling variant writes two halves per split
+        lay.add("part_max", (Sp, m), torch.float32)
+        lay.add("part_sum", (Sp, m), torch.float32)
+        lay.add("part_arg", (Sp, m), torch.int32)
         if self.temperature > 0:
-            lay.add("part_y", (S, m), torch.float32)
-            lay.add("part_x", (S, m), torch.float32)
+            lay.add("part_y", (Sp, m), torch.float32)
+            lay.add("part_x", (Sp, m), torch.float32)
         if group is not None:  # the exchange path runs whenever a process group is given (even P = 1)
             lay.add("local", (3, m), torch.float32)     # merged (max, sum, arg-bits) of this shard
             lay.add("gathered", (P, 3, m), torch.float32)
@@ -614,13 +616,15 @@ class MaskOnlyHead:
         elif self.temperature > 0:  # Gumbel-max sampling in K3's epilogue, noise keyed by rows[r]
             hc = b["hc"][:m]
             gather_rows(hidden, rows, hc, m_dev=m_dev, shift=shift, stream=stream)
-            py = b["part_y"].view(-1)[:S * m].view(S, m)
-            px = b["part_x"].view(-1)[:S * m].view(S, m)
+            S2 = 2 * S  # two 128-column halves per split
+            pm2, ps2, pa2 = (b[n].view(-1)[:S2 * m].view(S2, m) for n in ("part_max", "part_sum", "part_arg"))
+            py = b["part_y"].view(-1)[:S2 * m].view(S2, m)
+            px = b["part_x"].view(-1)[:S2 * m].view(S2, m)
             seed = (self.seed * 0x9E3779B1 + self._steps * 0x85EBCA6B + 0x27D4EB2F) & 0xFFFFFFFF
             self._steps += 1
-            lmhead_sample(hc, self.weight, S, rows, self.temperature, seed, pmax, psum, parg, py, px, m_dev=m_dev,
+            lmhead_sample(hc, self.weight, S, rows, self.temperature, seed, pm2, ps2, pa2, py, px, m_dev=m_dev,
                           v_offset=self.vocab_offset, stream=stream, die_of_sm=die, sched=b["sched"])
-            sample_merge(pmax, psum, parg, py, px, S, m, m, b["token"], b["conf"], lse=b["lse"], m_dev=m_dev,
+            sample_merge(pm2, ps2, pa2, py, px, S2, m, m, b["token"], b["conf"], lse=b["lse"], m_dev=m_dev,
                          stream=stream)
             return
         else:

@@ -11,8 +11,8 @@ hc = torch.randn(M, d, generator=g, device=dev).to(torch.bfloat16)
 W = (torch.randn(V, d, generator=g, device=dev) * 0.02).to(torch.bfloat16)
 pos = torch.arange(M, dtype=torch.int32, device=dev)
 S, _ = hotpath.lmhead_plan(M, V, d)
-b = [torch.empty(S, M, device=dev) for _ in range(4)]
-pa = torch.empty(S, M, device=dev, dtype=torch.int32)
+b = [torch.empty(2 * S, M, device=dev) for _ in range(4)]
+pa = torch.empty(2 * S, M, device=dev, dtype=torch.int32)
 die = hotpath.die_map(dev)[0]
 sched = torch.zeros(4, dtype=torch.int32, device=dev)
 fl = 2.0 * M * d * V

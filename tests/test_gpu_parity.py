@@ -835,9 +835,9 @@ def test_sampling_shard_invariant_and_distribution(dev):
         parts = []
         for a, b in zip(bounds[:-1], bounds[1:]):
             S, _ = hotpath.lmhead_plan(M, b - a, d)
-            bufs = [torch.empty(S, M, device=dev) for _ in range(2)] + [torch.empty(S, M, dtype=torch.int32,
-                                                                                     device=dev)]
-            py, px = torch.empty(S, M, device=dev), torch.empty(S, M, device=dev)
+            bufs = [torch.empty(2 * S, M, device=dev) for _ in range(2)] + [
+                torch.empty(2 * S, M, dtype=torch.int32, device=dev)]  # two column halves per split
+            py, px = torch.empty(2 * S, M, device=dev), torch.empty(2 * S, M, device=dev)
             hotpath.lmhead_sample(Hc, W[a:b].contiguous(), S, pos, 1.0, 1234, bufs[0], bufs[1], bufs[2], py, px,
                                   m_host=M, v_offset=a)
             parts.append((bufs[0], bufs[1], bufs[2], py, px))
@@ -856,12 +856,12 @@ def test_sampling_shard_invariant_and_distribution(dev):
     assert np.abs(freq - p).max() < 0.02  # M = 8192 draws: ~4 sigma for the largest p
     # T = 0.5 samples softmax(x / T)
     S, _ = hotpath.lmhead_plan(M, V, d)
-    bufs = [torch.empty(S, M, device=dev) for _ in range(4)]
-    pa = torch.empty(S, M, dtype=torch.int32, device=dev)
+    bufs = [torch.empty(2 * S, M, device=dev) for _ in range(4)]
+    pa = torch.empty(2 * S, M, dtype=torch.int32, device=dev)
     hotpath.lmhead_sample(Hc, W, S, pos, 0.5, 99, bufs[0], bufs[1], pa, bufs[2], bufs[3], m_host=M)
     tok = torch.empty(M, dtype=torch.int32, device=dev)
     conf = torch.empty(M, device=dev)
-    hotpath.sample_merge(bufs[0], bufs[1], pa, bufs[2], bufs[3], S, M, M, tok, conf, m_host=M)
+    hotpath.sample_merge(bufs[0], bufs[1], pa, bufs[2], bufs[3], 2 * S, M, M, tok, conf, m_host=M)
     torch.cuda.synchronize()
     pT = np.exp((z[0] - z[0].max()) / 0.5)
     pT /= pT.sum()
