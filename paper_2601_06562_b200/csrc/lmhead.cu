@@ -58,8 +58,12 @@ constexpr int kEpiWarps = 4;
 // 128 (each warp still owns one TMEM lane quarter), and each half writes its
 // own partial, so the split count doubles for K4.
 constexpr int kSampleHalves = 2;
+#ifndef MOSAIC_K3_EPI_HALVES
+#define MOSAIC_K3_EPI_HALVES 1  // experiment: 2 = eight epilogue warps on the argmax path too (partials x2)
+#endif
 constexpr int threads_for(int gather, bool sample) {
-  return gather == 2 ? kThreadsCpAsync : (sample ? kThreads + kEpiWarps * 32 : kThreads);
+  return gather == 2 ? kThreadsCpAsync
+                     : ((sample || MOSAIC_K3_EPI_HALVES == 2) ? kThreads + kEpiWarps * 32 : kThreads);
 }
 constexpr int kMaxSplits = 64;
 #ifndef MOSAIC_K3_EPI_SLEEP_NS
@@ -264,7 +268,7 @@ __global__ void __launch_bounds__(threads_for(kGather, kSample), 1)
     }
     for (int i = 0; i < NUM_ACC; ++i) {
       mbar_init(&tfull[i], 1);
-      mbar_init(&tempty[i], kEpiWarps * (kSample ? kSampleHalves : 1) * CG);  // one arrive per epilogue warp of the pair
+      mbar_init(&tempty[i], kEpiWarps * ((kSample || (kGather != 2 && MOSAIC_K3_EPI_HALVES == 2)) ? 2 : 1) * CG);
     }
     fence_mbar_init();
   }
@@ -553,8 +557,8 @@ __global__ void __launch_bounds__(threads_for(kGather, kSample), 1)
     // ------------------------------------------------------------ epilogue (both CTAs)
     const int q = warp & 3;  // TMEM lane quarter accessible to this warp
     const int row_local = q * 32 + lane;
-    constexpr int kHalves = kSample ? kSampleHalves : 1;
-    const int half = (kSample && warp >= 2 + kEpiWarps) ? 1 : 0;  // sampling: which 128 columns of each tile
+    constexpr int kHalves = (kSample || (kGather != 2 && MOSAIC_K3_EPI_HALVES == 2)) ? kSampleHalves : 1;
+    const int half = (kHalves == 2 && warp >= 2 + kEpiWarps) ? 1 : 0;  // which 128 columns of each tile
     constexpr int kChunksPerHalf = BN / 32 / kHalves;
     // tempty lives in the pair leader: arrive locally or through the cluster window
     const uint32_t tempty_addr0 = CG == 2 ? mapa_shared(smem_u32(&tempty[0]), 0) : smem_u32(&tempty[0]);

@@ -12,8 +12,8 @@ g = torch.Generator(device=dev).manual_seed(0)
 hc = torch.randn(M, d, generator=g, device=dev).to(torch.bfloat16)
 W = (torch.randn(V, d, generator=g, device=dev) * 0.02).to(torch.bfloat16)
 S, _ = hotpath.lmhead_plan(M, V, d)
-pm = torch.empty(S, M, device=dev); ps = torch.empty(S, M, device=dev)
-pa = torch.empty(S, M, device=dev, dtype=torch.int32)
+pm = torch.empty(2 * S, M, device=dev); ps = torch.empty(2 * S, M, device=dev)  # room for the halves experiment
+pa = torch.empty(2 * S, M, device=dev, dtype=torch.int32)
 die = hotpath.die_map(dev)[0]
 sched = torch.zeros(4, dtype=torch.int32, device=dev)
 fl = 2.0 * M * d * V
