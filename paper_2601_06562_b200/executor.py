@@ -138,16 +138,19 @@ class StepExecutor:
         # problem size as in MaskOnlyHead (hotpath.die_aware_default)
         self._die_aware = die_aware
         self._die_table = None
+        self._die_tried = False
         self._sched = torch.zeros(4, dtype=torch.int32, device=dev)
         if hotpath.die_aware_default(die_aware, 1 << 30, model.w_vocab.shape[0]):
             # measured now (a one-off probe with ~250 MB of scratch), not mid-step next to a full arena
-            self._die_table = hotpath.die_map(dev)[0]
+            self._die_table = hotpath.die_table_or_none(dev)
+            self._die_tried = True
 
     def _die(self, m_cap: int):
         if not hotpath.die_aware_default(self._die_aware, m_cap, self.model.w_vocab.shape[0]):
             return None
-        if self._die_table is None:
-            self._die_table = hotpath.die_map(self.device)[0]
+        if not self._die_tried:  # one probe per executor; None = the default schedule
+            self._die_table = hotpath.die_table_or_none(self.device)
+            self._die_tried = True
         return self._die_table
 
     # ---------------------------------------------------------------- buffers

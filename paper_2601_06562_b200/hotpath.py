@@ -21,7 +21,7 @@ from typing import Optional
 import torch
 
 from . import _native
-from .errors import InputError
+from .errors import InputError, MosaicError
 
 ALIGN = 256
 
@@ -158,6 +158,19 @@ def die_map(device=None) -> tuple[torch.Tensor, dict]:
         del scratch  # ~2x L2 of probe scratch: hand it back to the driver, not to torch's cache
         torch.cuda.empty_cache()
     return _DIE_MAPS[dev.index]
+
+
+def die_table_or_none(device) -> Optional[torch.Tensor]:
+    """The die map for K3's die-aware schedule, or None (default schedule) if
+    the probe cannot run here -- e.g. too little free memory for its ~2x-L2
+    scratch. The schedule is an optimisation only; the result is the same."""
+    try:
+        return die_map(device)[0]
+    except (MosaicError, RuntimeError) as exc:  # torch OOM is a RuntimeError subclass
+        import sys
+
+        print(f"mosaic_b200: die map probe unavailable ({exc}); K3 uses the default schedule", file=sys.stderr)
+        return None
 
 
 def die_aware_default(die_aware: Optional[bool] = None, m_cap: int = 0, v_shard: int = 0) -> bool:
@@ -452,7 +465,7 @@ class MaskOnlyHead:
             raise InputError("sampling (temperature > 0) runs on single-process heads with the buffered A path")
         self._die_aware = die_aware
         self._wplans: dict = {}
-        self.die_table = (die_map(weight_shard.device)[0]
+        self.die_table = (die_table_or_none(weight_shard.device)
                           if die_aware_default(die_aware, self.m_cap, self.v_shard) else None)
         if not (exchange in ("nccl", "p2p") or hasattr(exchange, "push")):
             raise InputError(f"exchange must be 'nccl', 'p2p' or a P2PExchange, got {exchange!r}")
