@@ -626,8 +626,12 @@ __global__ void __launch_bounds__(threads_for(kGather, kSample), 1)
             run_sum += (s0 + s1) + (s2 + s3);
             if constexpr (kSample) {
               // y = x + T * g, g = -ln(-ln u), u from (seed, position, global vocab id);
-              // strict > in ascending columns: the lowest id wins ties
+              // strict > in ascending columns: the lowest id wins ties. g <= 16.64 for every
+              // u the hash can produce, so a chunk with cmax + T * 16.7 < s_ymax cannot win
+              // and its noise is skipped when that holds for all 32 rows of the warp (exact)
+              const bool cannot_win = cmax + p.temperature * 16.7f < s_ymax;
               const uint32_t cg0 = static_cast<uint32_t>(p.v_offset + col0);
+              if (!__all_sync(0xffffffffu, cannot_win))
 #pragma unroll
               for (int j = 0; j < 32; ++j) {
                 const uint32_t h = fmix32(row_key ^ (cg0 + j) * 0x9E3779B1u);

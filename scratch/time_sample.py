@@ -18,7 +18,9 @@ sched = torch.zeros(4, dtype=torch.int32, device=dev)
 fl = 2.0 * M * d * V
 fns = {"argmax": lambda: hotpath.lmhead_stats(hc, W, S, b[0], b[1], pa, m_host=M, die_of_sm=die, sched=sched),
        "sample": lambda: hotpath.lmhead_sample(hc, W, S, pos, 1.0, 7, b[0], b[1], pa, b[2], b[3], m_host=M,
-                                               die_of_sm=die, sched=sched)}
+                                               die_of_sm=die, sched=sched),
+       "T0.3": lambda: hotpath.lmhead_sample(hc, W, S, pos, 0.3, 7, b[0], b[1], pa, b[2], b[3], m_host=M,
+                                             die_of_sm=die, sched=sched)}
 for rep in range(2):
     for name, f in fns.items():
         for _ in range(10): f()
