@@ -8,7 +8,7 @@ dev = torch.device("cuda", 0)
 g = torch.Generator(device=dev).manual_seed(0)
 M, d, V = 16384, 4096, 126464
 hc = torch.randn(M, d, generator=g, device=dev).to(torch.bfloat16)
-W = (torch.randn(V, d, generator=g, device=dev) * 0.02).to(torch.bfloat16)
+W = (torch.randn(V, d, generator=g, device=dev) * 0.02 * float(os.environ.get("WSCALE", "1"))).to(torch.bfloat16)
 pos = torch.arange(M, dtype=torch.int32, device=dev)
 S, _ = hotpath.lmhead_plan(M, V, d)
 b = [torch.empty(2 * S, M, device=dev) for _ in range(4)]
