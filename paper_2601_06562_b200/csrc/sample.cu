@@ -120,14 +120,26 @@ __global__ void __launch_bounds__(256) k4_sample_merge(const float* __restrict__
     merge_triples_row(in_max, in_sum, in_arg, S, stride, r, m, sum, unused);
     float ybest = -INFINITY, xbest = -INFINITY;
     int32_t abest = INT32_MAX;
-    for (int s = 0; s < S; ++s) {
-      const int64_t o = static_cast<int64_t>(s) * stride + r;
-      const float y = in_y[o];
-      const int32_t a = in_arg[o];
-      if (y > ybest || (y == ybest && a < abest)) {
-        ybest = y;
-        abest = a;
-        xbest = in_x[o];
+    constexpr int kChunk = 8;  // loads issued ahead of the compare chain (few rows, many splits)
+    for (int s0 = 0; s0 < S; s0 += kChunk) {
+      float y[kChunk], xv[kChunk];
+      int32_t a[kChunk];
+#pragma unroll
+      for (int j = 0; j < kChunk; ++j) {
+        if (s0 + j < S) {
+          const int64_t o = static_cast<int64_t>(s0 + j) * stride + r;
+          y[j] = in_y[o];
+          a[j] = in_arg[o];
+          xv[j] = in_x[o];
+        }
+      }
+#pragma unroll
+      for (int j = 0; j < kChunk; ++j) {
+        if (s0 + j < S && (y[j] > ybest || (y[j] == ybest && a[j] < abest))) {
+          ybest = y[j];
+          abest = a[j];
+          xbest = xv[j];
+        }
       }
     }
     const float l = m + logf(sum);
