@@ -78,6 +78,12 @@ MOSAIC_API int mosaic_mask_compact(const int32_t* x, int64_t L, int32_t mask_id,
                         int32_t* idx_out, int32_t* m_out,
                         void* scratch, void* stream);
 
+/* Batched windows (MaskOnlyHead.step_batch): rows[r] = b * ls + src(lo + j)
+ * for the compacted window coordinate q[r] = b * wn + j, r < M; src(p) =
+ * max(p - 1, 0) with shift = 1. One launch instead of host-side index math. */
+MOSAIC_API int mosaic_window_rows(const int32_t* q, const int32_t* m_dev, int64_t m_host, int64_t m_cap,
+                       int64_t wn, int64_t ls, int64_t lo, int32_t shift, int32_t* rows, void* stream);
+
 /* ---------------------------------------------------------------- K2 ------
  * Row gather: Hc[i, :] = H[src(idx[i]), :] for i < M, src(p) = p (shift=0) or
  * max(p-1, 0) (shift=1, Dream's token-level shift, workload.py:295-303).

@@ -148,10 +148,41 @@ __global__ void __launch_bounds__(256) k2_gather(const int4* __restrict__ H, int
   }
 }
 
+// Batched windows: compacted window coordinate q = b * wn + j -> hidden row
+// b * ls + src(lo + j), src(p) = max(p - 1, 0) with the token shift.
+__global__ void __launch_bounds__(256) k1_window_rows(const int32_t* __restrict__ q, const int32_t* __restrict__ m_dev,
+                                                      int64_t m_host, int64_t m_cap, int64_t wn, int64_t ls,
+                                                      int64_t lo, int32_t shift, int32_t* __restrict__ rows) {
+  pdl_wait();
+  pdl_trigger();
+  const int64_t M = min(static_cast<int64_t>(load_count(m_dev, m_host)), m_cap);
+  for (int64_t r = blockIdx.x * 256ll + threadIdx.x; r < M; r += gridDim.x * 256ll) {
+    const int64_t v = q[r];
+    const int64_t b = v / wn;
+    int64_t p = lo + (v - b * wn);
+    if (shift) p = p > 0 ? p - 1 : 0;
+    rows[r] = static_cast<int32_t>(b * ls + p);
+  }
+}
+
 }  // namespace
 }  // namespace mosaic
 
 using namespace mosaic;
+
+extern "C" int mosaic_window_rows(const int32_t* q, const int32_t* m_dev, int64_t m_host, int64_t m_cap, int64_t wn,
+                                  int64_t ls, int64_t lo, int32_t shift, int32_t* rows, void* stream) {
+  MOSAIC_REQUIRE(q && rows, "null operands");
+  MOSAIC_REQUIRE(wn >= 1 && ls >= wn && lo >= 0 && lo + wn <= ls, "bad window (wn %lld, ls %lld, lo %lld)",
+                 (long long)wn, (long long)ls, (long long)lo);
+  MOSAIC_REQUIRE(m_dev != nullptr || (m_host >= 0 && m_host <= m_cap), "m_host > m_cap");
+  if (m_cap == 0) return MOSAIC_OK;
+  const int64_t want = ceil_div(m_cap, 256);
+  const int grid = static_cast<int>(want < num_sms() * 4 ? want : num_sms() * 4);
+  MOSAIC_CUDA(launch_pdl(k1_window_rows, dim3(grid), dim3(256), 0, as_stream(stream), q, m_dev, m_host, m_cap, wn, ls,
+                         lo, shift, rows));
+  return check_launch("mosaic_window_rows");
+}
 
 extern "C" size_t mosaic_mask_compact_scratch_bytes(int64_t L) {
   const int64_t tiles = L > 0 ? ceil_div(L, kTile) : 1;

@@ -554,11 +554,9 @@ class MaskOnlyHead:
             if window is None and not self.shift:
                 rows = q  # flattened positions are the hidden rows
             else:  # q = seq * Wn + j -> hidden row seq * Ls + src(lo + j), src(p) = max(p - 1, 0) with the shift
-                pos = q % Wn + lo
-                if self.shift:
-                    pos = (pos - 1).clamp_(min=0)
                 rows = self._rows[:m]
-                torch.add(torch.div(q, Wn, rounding_mode="floor") * Ls, pos, out=rows)
+                _native.call("mosaic_window_rows", _p(q), _p(b["m_dev"]), 0, m, Wn, Ls, lo, int(self.shift),
+                             _p(rows), _s(stream))
             self._stats(hidden.view(B * Ls, self.d), rows, False, m, S, die, stream)
             kt = k if isinstance(k, torch.Tensor) else None
             remask_commit_segmented(b["conf"], q, b["token"], xs.view(-1), m, Wn, B,
