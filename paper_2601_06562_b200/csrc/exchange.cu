@@ -7,9 +7,11 @@
 //          EVERY rank's gathered buffer [2][P][3][m_cap] through its peer pointer
 //          (st.global over NVLink); the last CTA to finish publishes `epoch`
 //          into every rank's signal pad slot [rank] (release, system scope);
-//   wait:  one CTA spins until all P slots of the local signal pad carry
-//          `epoch` (acquire, system scope), bounded so a missing peer traps
-//          instead of hanging;
+//   wait:  one CTA spins until all P slots of the local signal pad have
+//          reached `epoch` (acquire, system scope; wraparound-safe "not
+//          behind" test, since a peer may already have published epoch + 1
+//          -- it needs only this rank's push of `epoch`, not this wait),
+//          bounded so a missing peer traps instead of hanging;
 //
 // after which the ordinary K4 (mosaic_stats_merge) merges the P triples in
 // rank order on the local buffer, exactly as after the all-gather. Buffers and
@@ -74,7 +76,10 @@ __global__ void k4x_wait(const uint32_t* __restrict__ local_signal, int32_t worl
   const int p = threadIdx.x;
   if (p < world) {
     uint32_t spins = 0;
-    while (ld_acquire_sys(local_signal + p) != epoch) {
+    // a peer is at most one epoch ahead (its next push needs this rank's push
+    // of the next epoch, which follows this wait), so "slot - epoch >= 0" in
+    // wraparound arithmetic is exactly "the peer's push of `epoch` landed"
+    while (static_cast<int32_t>(ld_acquire_sys(local_signal + p) - epoch) < 0) {
       if (++spins == (1u << 27)) __trap();  // a peer never arrived (~tens of s): fail the launch, do not hang
     }
   }

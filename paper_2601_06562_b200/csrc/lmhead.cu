@@ -69,12 +69,6 @@ constexpr int kMaxSplits = 64;
 #ifndef MOSAIC_K3_EPI_SLEEP_NS
 #define MOSAIC_K3_EPI_SLEEP_NS 0   // epilogue poll backoff while the next accumulator fills
 #endif
-#ifndef MOSAIC_K3_HALF_A
-#define MOSAIC_K3_HALF_A 0  // experiment only (wrong results): skip A loads on odd tiles
-#endif
-#ifndef MOSAIC_K3_DUP_B
-#define MOSAIC_K3_DUP_B 0  // experiment: also load every W tile a second time into a scratch slot (L2 feed cost)
-#endif
 #ifndef MOSAIC_K3_GFENCE
 #define MOSAIC_K3_GFENCE 1  // gather mode: proxy fence per stage (0 = none, experiment)
 #endif
@@ -98,8 +92,7 @@ struct Cfg {
 #define MOSAIC_K3_STAGES2 6
 #endif
   static constexpr int STAGES = CG == 1 ? 4 : MOSAIC_K3_STAGES2;
-  static constexpr int SMEM = STAGES * STAGE_BYTES + 1024 + 256 + BM * 4 + 16  // + gather rows, die schedule
-                              + (MOSAIC_K3_DUP_B ? 1024 + B_BYTES : 0);         // experiment: duplicate W reads
+  static constexpr int SMEM = STAGES * STAGE_BYTES + 1024 + 256 + BM * 4 + 16;  // + gather rows, die schedule
   static constexpr uint32_t IDESC = umma_idesc_bf16(ROWS, BN);
 };
 
@@ -115,6 +108,7 @@ struct Params {
   int32_t group_m;
   int32_t seg_splits;  // vocab segments of this many splits, processed segment-major (0 = one segment)
   const uint8_t* die_of_sm;  // die-aware schedule: SM -> L2 die (null = off)
+  int32_t n_sm;              // entries of die_of_sm (%smid need not be below it: treated as die 0)
   uint32_t* sched;           // die-aware schedule: [die0 pairs, die1 pairs, registered, decision], zeroed per launch
   int32_t policy;   // L2 policy of (A, B) loads: 0 = (normal, normal), 1 = (evict_last, normal), 2 = (normal, evict_first), 3 = (evict_last, evict_first)
   int64_t v_offset;
@@ -305,7 +299,7 @@ __global__ void __launch_bounds__(threads_for(kGather, kSample), 1)
     if (threadIdx.x == 0 && rank == 0) {
       uint32_t smid;
       asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
-      const int d = p.die_of_sm[smid] == 1 ? 1 : 0;
+      const int d = (static_cast<int32_t>(smid) < p.n_sm && p.die_of_sm[smid] == 1) ? 1 : 0;
       const uint32_t slot = atomicAdd(p.sched + d, 1u);
       __threadfence();
       volatile uint32_t* decision = p.sched + 3;
@@ -434,25 +428,11 @@ __global__ void __launch_bounds__(threads_for(kGather, kSample), 1)
             mbar_wait_sleep(&empty[stage], phase ^ 1, MOSAIC_K3_PROD_SLEEP_NS);
             int bc, br;
             w_box(p, t, kb, k_blocks, b_row_off, bc, br);
-            // MOSAIC_K3_HALF_A (experiment, wrong results): skip the A load on odd tiles to
-            // measure what halving A's L2 feed (as A multicast across two pairs would) buys
-            const bool load_a = !(MOSAIC_K3_HALF_A && (t & 1));
-            if (rank == 0)
-              mbar_arrive_expect_tx(&full[stage], (C::STAGE_BYTES - (load_a ? 0 : C::A_BYTES) +
-                                                   (MOSAIC_K3_DUP_B ? C::B_BYTES : 0)) * CG);
+            if (rank == 0) mbar_arrive_expect_tx(&full[stage], C::STAGE_BYTES * CG);
             if constexpr (CG == 1)
               tma_load_2d(sB + stage * C::B_BYTES, &tmap_b, &full[stage], bc, br, pol_b);
             else
               tma_load_2d_cg2(sB + stage * C::B_BYTES, &tmap_b, &full[stage], bc, br, pol_b);
-            if (MOSAIC_K3_DUP_B) {  // same W box again into a slot nobody reads (L2 -> SM feed experiment)
-              uint8_t* dup = reinterpret_cast<uint8_t*>(
-                  (reinterpret_cast<uintptr_t>(smem + C::STAGES * C::STAGE_BYTES + 256 + BM * 4 + 16) + 1023) &
-                  ~static_cast<uintptr_t>(1023));
-              if constexpr (CG == 1)
-                tma_load_2d(dup, &tmap_b, &full[stage], bc, br, pol_b);
-              else
-                tma_load_2d_cg2(dup, &tmap_b, &full[stage], bc, br, pol_b);
-            }
             if constexpr (kGather == kGatherTma4) {
               const uint32_t rows_addr = smem_u32(sidx);
 #pragma unroll 4
@@ -465,9 +445,9 @@ __global__ void __launch_bounds__(threads_for(kGather, kSample), 1)
                                 r4, pol_a);
               }
             } else if constexpr (CG == 1) {
-              if (load_a) tma_load_2d(sA + stage * C::A_BYTES, &tmap_a, &full[stage], kb * BK, a_row, pol_a);
+              tma_load_2d(sA + stage * C::A_BYTES, &tmap_a, &full[stage], kb * BK, a_row, pol_a);
             } else {
-              if (load_a) tma_load_2d_cg2(sA + stage * C::A_BYTES, &tmap_a, &full[stage], kb * BK, a_row, pol_a);
+              tma_load_2d_cg2(sA + stage * C::A_BYTES, &tmap_a, &full[stage], kb * BK, a_row, pol_a);
             }
             if (++stage == C::STAGES) {
               stage = 0;
@@ -833,6 +813,7 @@ int launch(const ASource& a, int64_t m_cap, const int32_t* m_dev, int64_t m_host
   cudaStream_t s = as_stream(stream);
   if (p.die_of_sm != nullptr) {
     MOSAIC_REQUIRE(p.sched != nullptr, "die-aware schedule needs its 16-byte scratch");
+    p.n_sm = num_sms();  // the die table holds one entry per SM (hotpath.die_map)
     MOSAIC_CUDA(cudaMemsetAsync(p.sched, 0, 16, s));
   }
   if (gather) {

@@ -159,7 +159,9 @@ class StepExecutor:
         K1/K5 scratch (mosaic/liveness.py:52-53 excludes graph inputs)."""
         if L not in self._side:
             self._side = {L: {
-                "mask_idx": torch.empty(L, dtype=torch.int32, device=self.device),
+                # zero-filled once: every entry is always a valid position, so a
+                # count below the graph's M can never send K2 out of bounds
+                "mask_idx": torch.zeros(L, dtype=torch.int32, device=self.device),
                 "m_dev": torch.zeros(1, dtype=torch.int32, device=self.device),
                 "compact": torch.empty(hotpath.mask_compact_scratch_bytes(L), dtype=torch.uint8, device=self.device),
                 "remask": torch.empty(hotpath.remask_scratch_bytes(), dtype=torch.uint8, device=self.device),
@@ -246,6 +248,10 @@ class StepExecutor:
                 kept["confidence"] = views[("confidence", None)].clone()
         end.record()
         end.synchronize()
+        m_seen = int(side["m_dev"].item())  # K1's count; the step was planned for the binding M
+        if m_seen != M:
+            raise InputError(f"x holds {m_seen} masked positions but the step graph was instantiated for M={M} "
+                             "(only the first min(count, M) masked rows were eligible for the commit)")
         by_kind: dict[str, float] = {}
         for kind, e0, e1 in marks:
             by_kind[kind] = by_kind.get(kind, 0.0) + e0.elapsed_time(e1)
@@ -373,8 +379,10 @@ class StepExecutor:
             if self._mode == "eager":  # rows are all positions: pick the masked ones
                 tok = tok.index_select(0, mask_idx.long())
                 conf = conf.index_select(0, mask_idx.long())
+            # the device count (capped at the planned M) bounds the commit, so rows
+            # past K1's count never reach x even if x disagrees with the binding
             hotpath.remask_commit(conf[:M].contiguous(), mask_idx, tok[:M].contiguous(), k_unmask, x,
-                                  side["remask"], M, m_host=M)
+                                  side["remask"], M, m_dev=side["m_dev"])
         else:
             raise InputError(f"no executor for op kind {kind!r} ({op.label})")
 
@@ -476,59 +484,3 @@ class StepExecutor:
         lse = torch.logsumexp(zf, dim=1)
         tok[r0:r1] = arg.to(torch.int32) + self.model.vocab_offset
         conf[r0:r1] = torch.exp(mx - lse)
-
-
-def reference_forward(model: RandomDLLM, x: torch.Tensor) -> torch.Tensor:
-    """Plain-PyTorch forward of the same model (no arena, no chunking): the
-    final hidden states [L, d], used as the executor's numerics reference."""
-    cfg = model.cfg
-    L, d, H = x.numel(), cfg.d_model, cfg.n_heads
-    h = model.w_embed.index_select(0, x)
-    for i in range(cfg.n_layers):
-        lw = model.layer(i)
-        q, k, v = (h @ lw["w_qkv"][:, j * d:(j + 1) * d] for j in range(3))
-        qh, kh, vh = (t.view(L, H, d // H).transpose(0, 1).unsqueeze(0) for t in (q, k, v))
-        a = F.scaled_dot_product_attention(qh, kh, vh).squeeze(0).transpose(0, 1).reshape(L, d)
-        h = h + a @ lw["w_attn_out"]
-        if cfg.moe is not None:
-            h = h + _moe_reference(cfg, lw, h)
-            continue
-        if "w_gate_up" in lw:  # fused_ffn layout -> torch layout
-            wg, wu = _split_gate_up(lw["w_gate_up"], cfg.d_ff)
-            lw = {**lw, "w_gate": wg, "w_up": wu}
-        up = h @ lw["w_up"]
-        act = F.silu((h @ lw["w_gate"]).float()).mul(up.float()).to(torch.bfloat16) if cfg.gated_ffn else F.silu(up)
-        h = h + act @ lw["w_down"]
-    return h
-
-
-def _moe_reference(cfg: ModelConfig, lw: dict, h: torch.Tensor) -> torch.Tensor:
-    """Plain-PyTorch MoE FFN with the routing rule of K8: top-k by (logit desc,
-    expert asc) over fp32 router logits, softmax over the selected logits,
-    per-expert SwiGLU FFN, weighted fp32 sum."""
-    E, k = cfg.moe.n_experts, cfg.moe.top_k
-    d, f = cfg.d_model, cfg.d_ff
-    wg, wu = _split_gate_up(lw["w_gate_up"].view(E, 2 * f, d), f)              # [E, d, f] each
-    wd = lw["w_down"].view(E, d, f).transpose(1, 2)                           # [E, f, d]
-    logits = torch.mm(h, lw["w_router"], out_dtype=torch.float32)
-    vals, idx = torch.sort(logits, dim=1, descending=True, stable=True)
-    sel, wts = idx[:, :k], torch.softmax(vals[:, :k], dim=1)
-    out = torch.zeros(h.shape, dtype=torch.float32, device=h.device)
-    for e in range(E):
-        rows, j = (sel == e).nonzero(as_tuple=True)
-        if rows.numel() == 0:
-            continue
-        x = h.index_select(0, rows)
-        up = x @ wu[e]
-        act = F.silu((x @ wg[e]).float()).mul(up.float()).to(torch.bfloat16)
-        out.index_add_(0, rows, wts[rows, j].unsqueeze(1) * (act @ wd[e]).float())
-    return out.to(torch.bfloat16)
-
-
-def _split_gate_up(w_gu: torch.Tensor, f: int) -> tuple[torch.Tensor, torch.Tensor]:
-    """Inverse of hotpath.interleave_gate_up: [.., 2f, d] -> gate, up [.., d, f]."""
-    *lead, _, d = w_gu.shape
-    blocks = w_gu.reshape(*lead, f // 128, 2, 128, d)
-    gate = blocks[..., 0, :, :].reshape(*lead, f, d).transpose(-1, -2)
-    up = blocks[..., 1, :, :].reshape(*lead, f, d).transpose(-1, -2)
-    return gate, up

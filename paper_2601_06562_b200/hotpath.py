@@ -557,7 +557,7 @@ class MaskOnlyHead:
                 rows = self._rows[:m]
                 _native.call("mosaic_window_rows", _p(q), _p(b["m_dev"]), 0, m, Wn, Ls, lo, int(self.shift),
                              _p(rows), _s(stream))
-            self._stats(hidden.view(B * Ls, self.d), rows, False, m, S, die, stream)
+            self._stats(hidden.view(B * Ls, self.d), rows, False, m, S, die, stream, keys=q)
             kt = k if isinstance(k, torch.Tensor) else None
             remask_commit_segmented(b["conf"], q, b["token"], xs.view(-1), m, Wn, B,
                                     k=0 if kt is not None else int(k), k_per_seg=kt, m_dev=b["m_dev"],
@@ -612,10 +612,15 @@ class MaskOnlyHead:
             self._wplans[m_w] = (S_w, die)
         return self._wplans[m_w]
 
-    def _stats(self, hidden: torch.Tensor, rows: torch.Tensor, shift: bool, m: int, S: int, die, stream) -> None:
+    def _stats(self, hidden: torch.Tensor, rows: torch.Tensor, shift: bool, m: int, S: int, die, stream,
+               keys: Optional[torch.Tensor] = None) -> None:
         """K2 + K3 (or gather-mode K3) over the hidden rows ``rows[r]`` (src(p)
         = p - 1 with ``shift``) of the M compacted rows, then K4 -- through the
-        vocab-shard exchange when the head is sharded -- into token/lse/conf."""
+        vocab-shard exchange when the head is sharded -- into token/lse/conf.
+        ``keys[r]`` (default ``rows``) keys the sampling noise: the window
+        coordinate of the row, never the hidden row it reads, so two positions
+        sharing a hidden row (the shift at p = 0, 1) draw independent noise and
+        ``step_batch`` with B = 1 draws what ``step`` draws."""
         b = self.buf
         pmax = b["part_max"].view(-1)[:S * m].view(S, m)
         psum = b["part_sum"].view(-1)[:S * m].view(S, m)
@@ -624,7 +629,7 @@ class MaskOnlyHead:
         if self.fused_gather:
             lmhead_stats_gather(hidden, rows, self.weight, S, pmax, psum, parg, m, m_dev=m_dev, shift=shift,
                                 v_offset=self.vocab_offset, stream=stream, die_of_sm=die, sched=b["sched"])
-        elif self.temperature > 0:  # Gumbel-max sampling in K3's epilogue, noise keyed by rows[r]
+        elif self.temperature > 0:  # Gumbel-max sampling in K3's epilogue, noise keyed by keys[r]
             hc = b["hc"][:m]
             gather_rows(hidden, rows, hc, m_dev=m_dev, shift=shift, stream=stream)
             S2 = 2 * S  # two 128-column halves per split
@@ -633,7 +638,7 @@ class MaskOnlyHead:
             px = b["part_x"].view(-1)[:S2 * m].view(S2, m)
             seed = (self.seed * 0x9E3779B1 + self._steps * 0x85EBCA6B + 0x27D4EB2F) & 0xFFFFFFFF
             self._steps += 1
-            lmhead_sample(hc, self.weight, S, rows, self.temperature, seed, pm2, ps2, pa2, py, px, m_dev=m_dev,
+            lmhead_sample(hc, self.weight, S, rows if keys is None else keys, self.temperature, seed, pm2, ps2, pa2, py, px, m_dev=m_dev,
                           v_offset=self.vocab_offset, stream=stream, die_of_sm=die, sched=b["sched"])
             sample_merge(pm2, ps2, pa2, py, px, S2, m, m, b["token"], b["conf"], lse=b["lse"], m_dev=m_dev,
                          stream=stream)

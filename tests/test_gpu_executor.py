@@ -46,7 +46,7 @@ def _step(cfg, ex, x, M, k, K=(1, 1), mode="fused", keep=()):
 
 
 def test_forward_in_arena_matches_plain_torch(env):
-    from paper_2601_06562_b200.executor import reference_forward
+    from torch_reference import reference_forward
 
     cfg, model, ex, dev = env
     L, M = 2048, 1024
@@ -151,7 +151,8 @@ def test_fused_ffn_forward_matches_plain_torch(native_lib):
     """fused_ffn=True: K10 gate/up GEMM with the SwiGLU epilogue inside the
     arena, against the plain-PyTorch forward of the same weights."""
     from paper_2601_06562_b200 import vmm, workload
-    from paper_2601_06562_b200.executor import RandomDLLM, StepExecutor, reference_forward
+    from paper_2601_06562_b200.executor import RandomDLLM, StepExecutor
+    from torch_reference import reference_forward
 
     cfg = replace(workload.toy_configs()["tiny_llada"], fused_ffn=True)
     dev = torch.device("cuda", 0)

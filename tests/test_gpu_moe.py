@@ -117,7 +117,7 @@ def _x(L, n_masked, dev, seed=0):
 
 @pytest.mark.parametrize("K_ffn", [1, 3, 7])
 def test_moe_forward_in_arena_matches_plain_torch(env, dev, K_ffn):
-    from paper_2601_06562_b200.executor import reference_forward
+    from torch_reference import reference_forward
 
     cfg, model, ex = env
     L, M = 2048, 1024

@@ -871,9 +871,10 @@ def test_sampling_shard_invariant_and_distribution(dev):
 
 
 def test_step_batch_sampling(dev):
-    """Sampling inside a batched step: noise keyed by the hidden row b * Ls + p,
-    so each sequence draws its own noise; tokens equal the oracle's Gumbel-max
-    sample per sequence (margin rule) and each sequence commits its own k."""
+    """Sampling inside a batched step: noise keyed by the window coordinate
+    q = b * (hi - lo) + (p - lo), so each sequence draws its own noise; tokens
+    equal the oracle's Gumbel-max sample per sequence (margin rule) and each
+    sequence commits its own k."""
     from paper_2601_06562_b200 import MaskOnlyHead
 
     rng = np.random.default_rng(21)
@@ -894,7 +895,42 @@ def test_step_batch_sampling(dev):
     for bi in range(B):
         rows = np.flatnonzero(q // Wn == bi)
         p = q[rows] % Wn + lo
-        ref = orc.sample_stats(orc.logits_f64(H[bi, p], W), bi * Ls + p, _step_seed(9, 0), T)
+        ref = orc.sample_stats(orc.logits_f64(H[bi, p], W), q[rows], _step_seed(9, 0), T)
         ok = ref["margin"] > 1e-3
         assert np.array_equal(tok[rows][ok], ref["arg"][ok])
         assert int(sel[rows].sum()) == min(k, rows.size)
+
+
+def test_sampling_keys_batch_of_one_equals_step(dev):
+    """With the Dream shift, positions 0 and 1 read the same hidden row but are
+    different window coordinates, so they draw independent noise; and a batch of
+    one sequence draws exactly the noise of ``step`` on the same window."""
+    from paper_2601_06562_b200 import MaskOnlyHead
+
+    rng = np.random.default_rng(23)
+    Ls, d, V, lo, hi, T, k = 512, 256, 4096, 0, 96, 1.0, 7
+    mask_id = V - 1
+    x = rng.integers(0, V - 1, size=Ls).astype(np.int32)
+    x[lo:hi][rng.random(hi - lo) < 0.7] = mask_id
+    x[0] = x[1] = mask_id
+    H = orc.bf16_round(rng.standard_normal((Ls, d)))
+    W = orc.bf16_round(rng.standard_normal((V, d)) * 0.05)
+    outs = []
+    for batched in (False, True):
+        head = MaskOnlyHead(bf16_tensor(W, dev), seq_len=Ls, mask_id=mask_id, shift=True, temperature=T, seed=3)
+        xd = torch.from_numpy(x).to(dev)
+        hd = bf16_tensor(H, dev)
+        if batched:
+            o = head.step_batch(xd.view(1, Ls), hd.view(1, Ls, d), k, window=(lo, hi))
+        else:
+            o = head.step(xd, hd, k, window=(lo, hi))
+        torch.cuda.synchronize()
+        M = int(o.m_dev.item())
+        outs.append((o.idx[:M].cpu().numpy(), o.token[:M].cpu().numpy(), xd.cpu().numpy()))
+    assert np.array_equal(outs[0][0], outs[1][0])
+    assert np.array_equal(outs[0][1], outs[1][1]) and np.array_equal(outs[0][2], outs[1][2])
+    q = outs[0][0]
+    src = np.maximum(q + lo - 1, 0)
+    ref = orc.sample_stats(orc.logits_f64(H[src], W), q, _step_seed(3, 0), T)
+    ok = ref["margin"] > 1e-3
+    assert np.array_equal(outs[0][1][ok], ref["arg"][ok])

@@ -41,7 +41,7 @@ def test_interleave_gate_up_layout():
     with pytest.raises(InputError):
         hotpath.interleave_gate_up(torch.zeros(3, 100), torch.zeros(3, 100))
     # the executor's inverse restores the torch layout
-    from paper_2601_06562_b200.executor import _split_gate_up
+    from torch_reference import _split_gate_up
 
     g2, u2 = _split_gate_up(w, F)
     assert torch.equal(g2, g) and torch.equal(u2, u)
