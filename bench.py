@@ -39,8 +39,12 @@ def parse():
     ap.add_argument("--impl", choices=["b200", "reference"], default="b200")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-activation", action="store_true", help="skip the measured full-model activation step")
     ap.add_argument("--exchange", choices=["nccl", "p2p"], default="nccl",
                     help="N>1: NCCL all-gather of the triples, or K4x peer-memory push (symmetric memory)")
+    ap.add_argument("--backend", choices=["nccl", "gloo"], default="nccl",
+                    help="process-group backend for N>1 (gloo: the multi-rank test on one shared GPU, since NCCL "
+                         "refuses two ranks on one device)")
     return ap.parse_args()
 
 
@@ -108,18 +112,41 @@ CPU_COLS_PER_CORE = 2048  # vocab columns each host core owns in a sample
 _CPU_STATE: dict = {}
 
 
+REF_DIR = ROOT / "baseline" / "_ref"  # the unmodified reference package (pip --target, git-ignored)
+
+
+def reference_kernel():
+    """The reference's own operator, ``mosaic.kernel.gather_gemm`` (mosaic/kernel.py:
+    62-86), imported from the offline install under baseline/_ref; None when the
+    install is absent (then the oracle restatement of the same loop is timed)."""
+    if not (REF_DIR / "mosaic" / "kernel.py").exists():
+        return None
+    if str(REF_DIR) not in sys.path:
+        sys.path.insert(0, str(REF_DIR))
+    from mosaic.kernel import GatherGemmProblem, gather_gemm
+
+    return GatherGemmProblem, gather_gemm
+
+
 def _cpu_task(args):
-    """One core's share of a sample: the reference algorithm (oracle
-    restatement of gather_gemm, mosaic/kernel.py:62-86, tiles 128) on a
-    128-row masked tile x this core's vocab slice, reduced to per-row softmax
-    triples (the `sample` op restatement)."""
+    """One core's share of a sample: the reference operator on a 128-row masked
+    tile x this core's vocab slice -- the reference's own ``gather_gemm``
+    through its public API (tiles 128, the fastest measured setting) when
+    baseline/_ref is installed, else the oracle restatement of the same loop --
+    reduced to per-row softmax triples (the `sample` op restatement; the
+    reference's `sample` is memory-only)."""
     step_idx, core = args
     import numpy as np
 
     import mosaic_oracle as orc
 
     rows = np.random.default_rng(step_idx).standard_normal((CPU_TILE_ROWS, D))
-    logits = orc.gather_gemm(rows, _CPU_STATE["W"], tuple(range(CPU_TILE_ROWS)), 128, 128, 128)
+    ref = reference_kernel()
+    if ref is not None:
+        Problem, gather_gemm = ref
+        logits, _ = gather_gemm(Problem(rows, _CPU_STATE["W"], tuple(range(CPU_TILE_ROWS)), 128, 128, 128))
+    else:
+        logits = orc.gather_gemm(rows, _CPU_STATE["W"], tuple(range(CPU_TILE_ROWS)), 128, 128, 128)
     return orc.split_stats(logits, [0, CPU_COLS_PER_CORE], v_offset=core * CPU_COLS_PER_CORE)[0]
 
 
@@ -163,11 +190,13 @@ def run_cpu_reference(steps: int, warmup: int) -> dict:
             sample(st)
         dt = time.perf_counter() - t0
     tokens = steps * CPU_TILE_ROWS * cores * CPU_COLS_PER_CORE / VOCAB
-    return {"tokens": tokens, "seconds": dt, "value": tokens / dt, "cores": cores,
+    kind = "reference" if reference_kernel() is not None else "port"
+    what = ("the reference's own mosaic.kernel.gather_gemm (baseline/_ref, unmodified, public API, tiles 128, "
+            "fp64)" if kind == "reference" else "the oracle restatement of gather_gemm (tiles 128, fp64)")
+    return {"tokens": tokens, "seconds": dt, "value": tokens / dt, "cores": cores, "kind": kind,
             "sample": f"{CPU_TILE_ROWS} masked rows x {cores * CPU_COLS_PER_CORE} vocab columns "
-                      f"({cores} cores x {CPU_COLS_PER_CORE}) per step, d={D}, through the oracle "
-                      "restatement of gather_gemm (tiles 128, fp64) + softmax stats + remask; "
-                      f"{steps} steps in {dt:.1f} s; value in full-vocab masked-token equivalents"}
+                      f"({cores} cores x {CPU_COLS_PER_CORE}) per step, d={D}, through {what} + softmax stats "
+                      f"+ remask; {steps} steps in {dt:.1f} s; value in full-vocab masked-token equivalents"}
 
 
 def _cpu_init_probe(i):
@@ -217,11 +246,19 @@ def gpu_main(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if os.environ.get("MOSAIC_BENCH_SHARE_GPU") == "1":  # test hook: every rank on GPU 0 (tests/test_gpu_bench_multirank.py)
+        local = 0
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     group = None
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if args.backend == "nccl":
+            # communicator-init lines stay visible (rank / nranks / cudaDev per rank) unless the caller chose
+            os.environ.setdefault("NCCL_DEBUG", "INFO")
+            os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group("gloo")
         group = dist.group.WORLD
     if rank == 0:
         _build.build()
@@ -281,8 +318,14 @@ def gpu_main(args):
         for _ in range(max(3, args.warmup)):
             one_step()
         torch.cuda.synchronize()
-        # correctness guard on the benchmark's own data: exactly k unmasked
+        # correctness guard on the benchmark's own data: exactly k unmasked, and with
+        # vocab shards every rank committed the identical sequence
         assert int((x == MASK_ID).sum().item()) == M - k
+        if world > 1:
+            digest = (x.to(torch.int64) * torch.arange(1, SEQ + 1, device=dev)).sum().view(1)
+            lo_hi = torch.cat([digest, -digest]).double()
+            dist.all_reduce(lo_hi, op=dist.ReduceOp.MAX)
+            assert float(lo_hi[0]) == -float(lo_hi[1]), "vocab-sharded ranks committed different tokens"
         k3_events.clear()
         if world > 1:
             dist.barrier()
@@ -378,10 +421,7 @@ def gpu_main(args):
     peak = sustained if long_region else burst
     flops = 2.0 * D * (v1 - v0) * M
     achieved = flops / (k3_ms / 1e3) / 1e12
-    traffic = None
-    tf = ROOT / "profiles" / "k3_traffic.json"
-    if tf.exists():
-        traffic = json.loads(tf.read_text()).get("bytes_per_launch")
+    traffic, traffic_src = k3_traffic()
 
     line = {
         "metric": "masked tokens/s (logits+remask)",
@@ -398,7 +438,8 @@ def gpu_main(args):
         "data": "synthetic (seeded N(0,1) hidden, N(0,0.02^2) LM head, random-init; no checkpoint)",
         "config": {"workload": "llada8b_32k_mask50", "d_model": D, "vocab": VOCAB, "seq_len": SEQ,
                    "masked": M, "unmask_k": k, "mask_layout": "suffix (step 0)",
-                   "parallelism": f"vocab-sharded x{world} ({args.exchange} exchange)" if world > 1 else "single GPU",
+                   "parallelism": (f"vocab-sharded x{world} ({args.exchange} exchange, {args.backend} group)"
+                                   if world > 1 else "single GPU"),
                    "vocab_shard": v1 - v0, "n_splits": head.n_splits,
                    "k3_schedule": "die-aware" if head.die_table is not None else "default",
                    "l2": "inputs larger than L2 (W 1.04 GB, H 268 MB > 126 MB)"},
@@ -411,7 +452,7 @@ def gpu_main(args):
                      "peak_burst": burst, "frac_of_burst": achieved / burst,
                      "peak_sustained": sustained, "frac_of_sustained": achieved / sustained,
                      "k3_ms": k3_ms, "k3_share_of_step": k3_ms / ms_per_step,
-                     "flops_per_launch": flops, "traffic": traffic},
+                     "flops_per_launch": flops, "traffic": traffic, "traffic_source": traffic_src},
         "gpu_launches": launches_per_step * args.steps,
         "clocks": clocks.summary(),
         "e2e": e2e,
@@ -420,19 +461,82 @@ def gpu_main(args):
                    "inputs_bytes": W.numel() * 2 + H.numel() * 2,  # LM-head shard + hidden states (not activation)
                    "torch_max_allocated_bytes": torch.cuda.max_memory_allocated(dev),
                    "dense_logits_bytes_avoided": M * (v1 - v0) * 4,  # the fp32 [M, V] the reference materialises
-                   "note": "measured on this process; the full-model arena figures are peak_activation_gb (plan) "
-                           "and profiles/r01e_context_sweep.json (measured commits)"},
+                   "note": "head figures of this process; memory.activation is the measured full-model step"},
         **context_fields(),
     }
+    if world == 1 and not args.no_activation:
+        line["memory"]["activation"] = measure_activation(dev)
+        line["peak_activation_gb"] = line["memory"]["activation"]["peak_activation_gb"]
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cpu = run_cpu_reference(steps=8, warmup=1)  # ~10 s of host work (bounded sample)
         line["cpu_baseline"] = {"value": cpu["value"], "unit": "masked tokens/s", "cores": cpu["cores"],
-                                "kind": "port", "sample": cpu["sample"]}
+                                "kind": cpu["kind"], "sample": cpu["sample"]}
         line["cpu_dense_blas"] = run_cpu_blas()
     if rank == 0:
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
+
+
+def k3_traffic() -> tuple:
+    """DRAM bytes per K3 launch from the ncu --set full capture of the bench
+    command (profiles/k3_traffic.json), reported only when that capture measured
+    the code being benchmarked (same hash of csrc/lmhead.cu + common.cuh + nvcc
+    flags); otherwise null with the reason."""
+    from paper_2601_06562_b200 import _build
+
+    tf = ROOT / "profiles" / "k3_traffic.json"
+    now = _build.source_hash(_build.K3_SOURCES)
+    if not tf.exists():
+        return None, {"reason": "no capture", "code_hash": now}
+    t = json.loads(tf.read_text())
+    src = {"capture": t.get("source"), "code_hash": t.get("code_hash"), "current_code_hash": now}
+    if t.get("code_hash") != now:
+        src["reason"] = "capture measured other K3 code: traffic not reported"
+        return None, src
+    return t.get("bytes_per_launch"), src
+
+
+def measure_activation(dev) -> dict:
+    """Peak activation of the full LLaDA-8B step (32 layers, d 4096, d_ff 12288,
+    fused logits + fused FFN) at this workload's sequence, MEASURED on the
+    device: one step through the executor in a fresh cuMem arena, K = (1, 1).
+    Activation = the arena's committed bytes (the torch-scratch region holding
+    the attention temporaries + the first-fit plan) + whatever the step grew
+    torch's own pool by outside the arena (graph-input side buffers). Weights
+    are excluded; one weight set serves all 32 layers (per-layer activations
+    are identical)."""
+    import torch
+
+    from paper_2601_06562_b200 import vmm, workload
+    from paper_2601_06562_b200.executor import RandomDLLM, StepExecutor
+
+    cfg = workload.ModelConfig("llada_8b", 32, D, 12288, 32, VOCAB, 2, 0, True, "fused", "none", fused_ffn=True)
+    M = round(MASK_RATIO * SEQ)
+    model = RandomDLLM(cfg, dev, seed=5, distinct_layers=1)
+    ws = vmm.reserve(16 << 30, backend="cuda", device=dev.index)
+    try:
+        ex = StepExecutor(model, ws, MASK_ID)
+        g = workload.build_layer_template(cfg).instantiate({"L": SEQ, "M": M, "K_logits": 1, "K_FFN": 1})
+        table, plan = ex.plan(g)
+        x = torch.randint(0, MASK_ID, (SEQ,), dtype=torch.int32, device=dev)
+        x[SEQ - M:] = MASK_ID
+        torch.cuda.synchronize(dev)
+        base = torch.cuda.memory_reserved(dev)
+        torch.cuda.reset_peak_memory_stats(dev)
+        r = ex.run(g, x, unmask_k(), table=table, plan=plan)
+        torch.cuda.synchronize(dev)
+        grown = torch.cuda.max_memory_reserved(dev) - base
+        outside = max(0, grown - r["pool"]["in_use"])  # MemPool segments live inside the arena
+        return {"peak_activation_gb": (r["committed_bytes"] + outside) / 1e9,
+                "arena_committed_bytes": r["committed_bytes"], "plan_workspace_bytes": plan.workspace_size,
+                "torch_scratch_region_bytes": r["scratch_bytes"], "torch_scratch_high_water": r["pool"]["high_water"],
+                "outside_arena_bytes": outside, "step_ms": r["ms"],
+                "how": "measured: one full-depth step (32 layers, K=(1,1)) through StepExecutor on this device"}
+    finally:
+        ws.close()
+        del model
+        torch.cuda.empty_cache()
 
 
 def context_fields() -> dict:
@@ -448,14 +552,21 @@ def context_fields() -> dict:
     dense = chunker.evaluate_peak(workload.build_layer_template(
         workload.ModelConfig("llada_8b", 32, D, 12288, 32, VOCAB, 2, 16 * 2 ** 30, True, "eager", "none")),
         {"L": SEQ, "M": round(MASK_RATIO * SEQ)}, chunker.ChunkConfig(1, 1))
-    out = {"peak_activation_gb": peak.total_peak / 1e9, "peak_activation_gb_dense_logits_plan": dense.total_peak / 1e9}
-    sweep = ROOT / "profiles" / "r01e_context_sweep.json"
-    if sweep.exists():
+    out = {"peak_activation_gb_plan": peak.total_peak / 1e9,
+           "peak_activation_gb_dense_logits_plan": dense.total_peak / 1e9}
+    from paper_2601_06562_b200 import _build
+
+    sweeps = sorted((ROOT / "profiles").glob("r*_context_sweep.json"))
+    if sweeps:
+        sweep = sweeps[-1]
         d = json.loads(sweep.read_text())
         out["max_seq_len"] = d.get("pipeline_lmax_measured")
         out["max_seq_len_planned"] = d.get("planned_lmax", {}).get("fused_chunking")
         out["max_seq_len_dense_baseline"] = d.get("baseline_lmax")
-        out["max_seq_len_source"] = "profiles/r01e_context_sweep.json (bench_context.py on one B200)"
+        out["max_seq_len_provenance"] = {
+            "source": f"profiles/{sweep.name} (bench_context.py on one B200, not this run)",
+            "code_hash": d.get("code_hash"), "current_code_hash": _build.source_hash(),
+            "same_code": d.get("code_hash") == _build.source_hash()}
     return out
 
 
@@ -474,7 +585,7 @@ def reference_main(args):
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic", "config": {"workload": "llada8b_32k_mask50", "d_model": D, "vocab": VOCAB,
                                         "seq_len": SEQ},
-        "cpu_baseline": {"value": v, "unit": "masked tokens/s", "cores": r["cores"], "kind": "port",
+        "cpu_baseline": {"value": v, "unit": "masked tokens/s", "cores": r["cores"], "kind": r["kind"],
                          "sample": r["sample"]},
         "e2e": {"value": v, "unit": "masked tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "cpu_dense_blas": run_cpu_blas(),

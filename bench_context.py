@@ -35,13 +35,14 @@ ROOT = Path(__file__).resolve().parent
 sys.path.insert(0, str(ROOT))
 
 MASK_ID = 126336
-RESERVE = 4 << 30  # CUDA context, cuBLAS workspace, attention temporaries, side buffers
+RESERVE = 4 << 30  # CUDA context, cuBLAS workspace, side buffers (attention temporaries: the arena's scratch)
 
 
 def llada_cfg(weights_bytes: int):
     from paper_2601_06562_b200 import workload
 
-    return workload.ModelConfig("llada_8b", 32, 4096, 12288, 32, 126464, 2, weights_bytes, True, "fused", "none")
+    return workload.ModelConfig("llada_8b", 32, 4096, 12288, 32, 126464, 2, weights_bytes, True, "fused", "none",
+                                fused_ffn=True)
 
 
 def make_x(L: int, M: int, dev) -> torch.Tensor:
@@ -56,7 +57,8 @@ def pipeline_probe(ex, cfg, L: int, act_budget: int) -> dict:
     M = round(0.5 * L)
     tmpl = workload.build_layer_template(cfg)
     t0 = time.time()
-    out = chunker.search_bottleneck(tmpl, {"L": L, "M": M}, act_budget)
+    scratch = ex.scratch_bytes_for(L)  # the arena's torch-scratch region comes out of the same budget
+    out = chunker.search_bottleneck(tmpl, {"L": L, "M": M}, act_budget - scratch)
     plan_s = time.time() - t0
     rec = {"L": L, "M": M, "feasible_plan": out.feasible, "reason": out.reason, "planned_peak": out.final_peak,
            "floor": out.floor, "plan_seconds": plan_s}
@@ -66,15 +68,19 @@ def pipeline_probe(ex, cfg, L: int, act_budget: int) -> dict:
     table, plan = ex.plan(g)
     x = make_x(L, M, ex.device)
     torch.cuda.reset_peak_memory_stats()
-    base_alloc = torch.cuda.memory_allocated()
+    base_res = torch.cuda.memory_reserved()
     k = max(1, M // 64)
     try:
         r = ex.run(g, x, k, table=table, plan=plan)
         ok = int((x == MASK_ID).sum()) == M - k
+        # torch-side temporaries are served from the arena's scratch region (MemPool): only
+        # growth of torch's reserve beyond those segments lies outside the arena
+        outside = max(0, torch.cuda.max_memory_reserved() - base_res - r["pool"]["in_use"])
         rec.update({"ran": True, "ok": ok, "ms": r["ms"], "k": [out.config.k_logits, out.config.k_ffn],
                     "workspace_bytes": plan.workspace_size, "committed_bytes": r["committed_bytes"],
-                    "torch_extra_bytes": torch.cuda.max_memory_allocated() - base_alloc,
-                    "activation_gb": (r["committed_bytes"] + torch.cuda.max_memory_allocated() - base_alloc) / 1e9})
+                    "scratch_region_bytes": r["scratch_bytes"], "scratch_high_water": r["pool"]["high_water"],
+                    "outside_arena_bytes": outside,
+                    "activation_gb": (r["committed_bytes"] + outside) / 1e9})
     except torch.cuda.OutOfMemoryError as exc:
         rec.update({"ran": False, "ok": False, "error": str(exc).splitlines()[0]})
     del x
@@ -95,8 +101,10 @@ def eager_step(model, x: torch.Tensor, M: int, exec_layers: int) -> None:
         del q, kk, v, qh, kh, vh
         h = h + a @ lw["w_attn_out"]
         del a
-        act = F.silu(h @ lw["w_gate"]) * (h @ lw["w_up"])
-        h = h + act @ lw["w_down"]
+        f = cfg.d_ff  # the same weights, from the K10 layouts (gate/up interleaved in 128-row blocks, down K-major)
+        gu = lw["w_gate_up"].view(f // 128, 2, 128, d)
+        act = F.silu(h @ gu[:, 0].reshape(f, d).t()) * (h @ gu[:, 1].reshape(f, d).t())
+        h = h + act @ lw["w_down"].t()
         del act
     logits = h @ model.w_vocab.t()                      # [L, V] bf16, every position
     probs = torch.softmax(logits.float(), dim=-1)      # fp32 sampler
@@ -133,6 +141,7 @@ def main():
     from paper_2601_06562_b200.executor import RandomDLLM, StepExecutor
 
     _build.build()
+    code_hash = _build.source_hash()
     dev = torch.device("cuda", 0)
     torch.cuda.set_device(dev)
     total = torch.cuda.get_device_properties(dev).total_memory
@@ -145,7 +154,7 @@ def main():
     act_budget = free - RESERVE
     result = {"device_total_bytes": total, "weights_bytes": wbytes, "free_after_weights": free,
               "reserve_bytes": RESERVE, "activation_budget": act_budget, "exec_layers": args.exec_layers,
-              "model": cfg.to_json_dict()}
+              "model": cfg.to_json_dict(), "code_hash": code_hash}
     t0 = time.time()
     result["planned_lmax"] = {
         "fused_chunking": workload.find_lmax(cfg, 0.5, act_budget + wbytes, logits_mode="fused",

@@ -28,6 +28,7 @@
 
 #include <stddef.h>
 #include <stdint.h>
+#include <sys/types.h> /* ssize_t (the pluggable-allocator signature) */
 
 #if defined(__GNUC__)
 #define MOSAIC_API __attribute__((visibility("default")))
@@ -176,6 +177,20 @@ MOSAIC_API int mosaic_sample_merge(const float* in_max, const float* in_sum, con
 /* Debug / parity path for the reference operator itself: out[r, v] =
  * <Hc[r, :], W[v, :]> in fp32, row stride ldo. Materialises the logits like
  * gather_gemm (kernel.py:68); the product path never calls it.               */
+/* Materialised logits with the A rows read from H at idx (gather mode: no
+ * [m, d] gathered copy), the parity form of gather_gemm (kernel.py:62-86)
+ * under the ScratchAccount contract ("no [m x d] gathered copy is
+ * ever materialized"). out [m_cap, ldo] fp32; shift = Dream src(p)=max(p-1,0). */
+MOSAIC_API int mosaic_lmhead_logits_gather(const uint16_t* H, int64_t n_rows, int64_t ld_h, const int32_t* idx,
+                                           int32_t shift, int64_t m_cap, const int32_t* m_dev, int64_t m_host,
+                                           const uint16_t* W, int64_t V_shard, int64_t d, float* out, int64_t ldo,
+                                           void* stream);
+/* The launched K3 configuration for a problem of m_cap rows, the device
+ * counterpart of ScratchAccount (kernel.py:52-59): out[8] = {cta_group,
+ * smem stages, A rows per CTA, K per stage, W rows per CTA, TMEM columns,
+ * dynamic shared memory bytes per CTA, threads per CTA}; gather != 0 selects
+ * the gather-mode (cp.async A) kernel.                                        */
+MOSAIC_API int mosaic_lmhead_config(int64_t m_cap, int32_t gather, int64_t* out);
 MOSAIC_API int mosaic_lmhead_logits(const uint16_t* Hc, int64_t m_cap, const int32_t* m_dev, int64_t m_host,
                          const uint16_t* W, int64_t V_shard, int64_t d,
                          float* out, int64_t ldo, void* stream);
@@ -244,6 +259,16 @@ MOSAIC_API int mosaic_remask_commit_segmented(const float* conf, const int32_t* 
  * workload.py:249-259). gate/up 16-byte aligned.                              */
 MOSAIC_API int mosaic_swiglu(const uint16_t* gate, uint16_t* up, int64_t n, void* stream);
 
+/* ---------------------------------------------------------------- K11 -----
+ * Rotary position embedding (rotate-half, LLaDA/LLaMA form) of the attention
+ * queries and keys, in place: q, k [L, ld] bf16 rows of n_heads x head_dim;
+ * inv_freq [head_dim / 2] fp32 (theta^(-2i/head_dim)); row r has position
+ * pos0 + r. The reference's `fused_attention` op (workload.py:207-229) is
+ * memory-only; the executor applies this before the attention so masked rows
+ * carry their positions. head_dim a multiple of 16, q/k 16-byte aligned.     */
+MOSAIC_API int mosaic_rope_qk(uint16_t* q, uint16_t* k, int64_t L, int32_t n_heads, int32_t head_dim, int64_t ld,
+                              const float* inv_freq, int64_t pos0, void* stream);
+
 /* ---------------------------------------------------------------- K8/K9 ---
  * MoE expert routing and combine for the chunked expert FFN (BASELINE
  * configs[3]). The reference models MoE only as a top_k multiplier on the FFN
@@ -281,6 +306,13 @@ MOSAIC_API int mosaic_moe_combine(const uint16_t* src, int64_t ld_src, const int
 MOSAIC_API int mosaic_ffn_gemm(const uint16_t* A, int64_t rows_cap, int64_t lda, const int32_t* group_off,
                     int32_t G, int64_t m_host, const uint16_t* W, int64_t N, int64_t K, int32_t swiglu,
                     uint16_t* C, int64_t ldc, void* stream);
+/* The same GEMM with an epilogue selector: 0 store C = A W^T, 1 SwiGLU (as
+ * swiglu = 1 above), 2 residual C += A W^T in place (fp32 sum rounded once):
+ * the dense chunk's ffn_down + chunk_write + ffn_res add (workload.py:261-272)
+ * in one launch, written straight into the chunk's rows of the hidden state.  */
+MOSAIC_API int mosaic_ffn_gemm_ex(const uint16_t* A, int64_t rows_cap, int64_t lda, const int32_t* group_off,
+                                  int32_t G, int64_t m_host, const uint16_t* W, int64_t N, int64_t K,
+                                  int32_t epilogue, uint16_t* C, int64_t ldc, void* stream);
 
 /* ---------------------------------------------------------------- K7 ------
  * Contiguous device workspace with lazy physical commitment (cuMem VMM):
@@ -293,6 +325,26 @@ MOSAIC_API int mosaic_arena_commit(mosaic_arena* arena, uint64_t target_bytes);
 MOSAIC_API int mosaic_arena_info(const mosaic_arena* arena, uint64_t* base, uint64_t* reserved,
                       uint64_t* committed, uint64_t* granularity);
 MOSAIC_API int mosaic_arena_release(mosaic_arena* arena);
+
+/* The arena's torch-scratch region as a PyTorch pluggable allocator
+ * (torch.cuda.memory.CUDAPluggableAllocator(lib, "mosaic_pool_alloc",
+ * "mosaic_pool_free") inside a torch.cuda.MemPool): library temporaries of the
+ * step (attention outputs) are carved from a committed region at the start of
+ * the executor's own arena instead of fresh cudaMallocs -- the reference's
+ * single-workspace contract (vmm.py:48-147, budget workload.py:362-369).
+ * Regions are keyed by base address (one per arena): bind creates or resizes
+ * one in place (live blocks stay valid; a shrink below one fails), select
+ * picks the region new allocations come from, unbind forgets one whose arena
+ * is released. alloc returns NULL when the selected region is exhausted (torch
+ * then raises out-of-memory); stats reports bytes in use, the high-water
+ * mark, allocations served and refused.                                      */
+MOSAIC_API int mosaic_pool_bind(int32_t device, void* base, uint64_t size);
+MOSAIC_API int mosaic_pool_select(int32_t device, void* base);
+MOSAIC_API int mosaic_pool_unbind(int32_t device, void* base);
+MOSAIC_API void* mosaic_pool_alloc(ssize_t size, int device, void* stream);
+MOSAIC_API void mosaic_pool_free(void* ptr, ssize_t size, int device, void* stream);
+MOSAIC_API int mosaic_pool_stats(int32_t device, void* base, uint64_t* in_use, uint64_t* high_water,
+                                 uint64_t* n_alloc, uint64_t* n_fail);
 
 /* Plan-executor canaries (execute_plan, mosaic/vmm.py:188-291) on device
  * memory: fill [ptr, ptr+nbytes) with the 8-byte tag repeated from ptr; check

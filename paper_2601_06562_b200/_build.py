@@ -45,6 +45,24 @@ def sources() -> list[Path]:
     return sorted(CSRC.glob("*.cu"))
 
 
+def source_hash(names: tuple[str, ...] | None = None) -> str:
+    """sha256 (16 hex digits) of kernel sources -- ``names`` inside csrc/, or
+    every csrc/ file plus the C-ABI header -- and the nvcc flags. Evidence
+    recorded from a profiler capture (profiles/k3_traffic.json) carries the hash
+    of the code it measured; bench.py reports it only while the hash matches."""
+    import hashlib
+
+    files = ([CSRC / n for n in names] if names else sorted(CSRC.glob("*")) + [REPO / "include" / "mosaic_b200.h"])
+    h = hashlib.sha256(" ".join(NVCC_FLAGS).encode())
+    for f in files:
+        h.update(f.name.encode())
+        h.update(f.read_bytes())
+    return h.hexdigest()[:16]
+
+
+K3_SOURCES = ("lmhead.cu", "common.cuh")
+
+
 def _stale(objs: list[Path]) -> bool:
     if not LIB.exists():
         return True

@@ -93,7 +93,14 @@ SIGNATURES: dict[str, tuple[object, list[object]]] = {
         [c_void_p, c_void_p, c_void_p, c_void_p, c_int64, c_int64, c_int64, c_void_p, c_void_p,
          c_void_p, c_void_p],
     ),
+    "mosaic_lmhead_logits_gather": (
+        c_int,
+        [c_void_p, c_int64, c_int64, c_void_p, c_int32, c_int64, c_void_p, c_int64, c_void_p, c_int64, c_int64,
+         c_void_p, c_int64, c_void_p],
+    ),
+    "mosaic_lmhead_config": (c_int, [c_int64, c_int32, c_void_p]),
     "mosaic_swiglu": (c_int, [c_void_p, c_void_p, c_int64, c_void_p]),
+    "mosaic_rope_qk": (c_int, [c_void_p, c_void_p, c_int64, c_int32, c_int32, c_int64, c_void_p, c_int64, c_void_p]),
     "mosaic_moe_route_scratch_bytes": (c_size_t, [c_int64, c_int32]),
     "mosaic_moe_route": (
         c_int,
@@ -109,10 +116,21 @@ SIGNATURES: dict[str, tuple[object, list[object]]] = {
         [c_void_p, c_int64, c_int64, c_void_p, c_int32, c_int64, c_void_p, c_int64, c_int64, c_int32, c_void_p,
          c_int64, c_void_p],
     ),
+    "mosaic_ffn_gemm_ex": (
+        c_int,
+        [c_void_p, c_int64, c_int64, c_void_p, c_int32, c_int64, c_void_p, c_int64, c_int64, c_int32, c_void_p,
+         c_int64, c_void_p],
+    ),
     "mosaic_arena_reserve": (c_int, [c_int32, c_uint64, POINTER(c_void_p)]),
     "mosaic_arena_commit": (c_int, [c_void_p, c_uint64]),
     "mosaic_arena_info": (c_int, [c_void_p, _u64p, _u64p, _u64p, _u64p]),
     "mosaic_arena_release": (c_int, [c_void_p]),
+    "mosaic_pool_bind": (c_int, [c_int32, c_void_p, c_uint64]),
+    "mosaic_pool_select": (c_int, [c_int32, c_void_p]),
+    "mosaic_pool_unbind": (c_int, [c_int32, c_void_p]),
+    "mosaic_pool_alloc": (c_void_p, [ctypes.c_ssize_t, c_int, c_void_p]),
+    "mosaic_pool_free": (None, [c_void_p, ctypes.c_ssize_t, c_int, c_void_p]),
+    "mosaic_pool_stats": (c_int, [c_int32, c_void_p, _u64p, _u64p, _u64p, _u64p]),
     "mosaic_tag_fill": (c_int, [c_void_p, c_int64, c_uint64, c_void_p]),
     "mosaic_tag_check": (c_int, [c_void_p, c_int64, c_uint64, c_void_p, c_void_p]),
 }

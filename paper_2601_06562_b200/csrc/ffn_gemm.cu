@@ -15,7 +15,11 @@
 // transpose of torch's [K, N] weight), C [rows, N or N/2] bf16 (row stride
 // ldc). SwiGLU mode expects W rows interleaved in 128-row blocks (gate block
 // j, then up block j) so one 256-column tile holds matching gate and up
-// columns; it writes 128 act columns per tile.
+// columns; it writes 128 act columns per tile. Residual mode (the dense FFN's
+// down projection) accumulates in place, C = C + A W^T, rounding the fp32 sum
+// once to bf16: the chunk's `ffn_down` -> `chunk_write` -> `ffn_res` add
+// (mosaic/workload.py:261-272) in one epilogue, so neither the chunk's `down`
+// rows nor the [L, d] `ffn_acc` accumulator is ever written.
 //
 // Structure as K3 (csrc/lmhead.cu): warp 0 TMA producer, warp 1 TMEM
 // allocator + single-thread tcgen05.mma issuer (cta_group::2 256x256 tiles over
@@ -65,6 +69,7 @@ struct GParams {
   int32_t K;
   int32_t n_tiles;  // ceil(N / BN)
   int32_t swiglu;
+  int32_t residual;  // C += A W^T (read-modify-write of each output vector)
   uint16_t* C;
   int64_t ldc;
 };
@@ -264,6 +269,21 @@ __global__ void __launch_bounds__(kThreads, 1)
           tmem_ld32(taddr + c * 32, v32);
           if (live) {
             uint4* dst = reinterpret_cast<uint4*>(p.C + row * p.ldc + col0);
+            if (p.residual) {
+              uint4 r[4];
+#pragma unroll
+              for (int v = 0; v < 4; ++v) r[v] = dst[v];  // all four loads in flight before the adds
+#pragma unroll
+              for (int v = 0; v < 4; ++v) {
+                const __nv_bfloat162* r2 = reinterpret_cast<const __nv_bfloat162*>(&r[v]);
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                  const float2 rf = __bfloat1622float2(r2[j]);
+                  v32[8 * v + 2 * j] += rf.x;
+                  v32[8 * v + 2 * j + 1] += rf.y;
+                }
+              }
+            }
 #pragma unroll
             for (int v = 0; v < 4; ++v) {
               uint4 o;
@@ -333,6 +353,14 @@ using namespace mosaic;
 extern "C" int mosaic_ffn_gemm(const uint16_t* A, int64_t rows_cap, int64_t lda, const int32_t* group_off, int32_t G,
                                int64_t m_host, const uint16_t* W, int64_t N, int64_t K, int32_t swiglu, uint16_t* C,
                                int64_t ldc, void* stream) {
+  return mosaic_ffn_gemm_ex(A, rows_cap, lda, group_off, G, m_host, W, N, K, swiglu ? 1 : 0, C, ldc, stream);
+}
+
+extern "C" int mosaic_ffn_gemm_ex(const uint16_t* A, int64_t rows_cap, int64_t lda, const int32_t* group_off,
+                                  int32_t G, int64_t m_host, const uint16_t* W, int64_t N, int64_t K, int32_t epilogue,
+                                  uint16_t* C, int64_t ldc, void* stream) {
+  MOSAIC_REQUIRE(epilogue >= 0 && epilogue <= 2, "epilogue %d not in {0 store, 1 SwiGLU, 2 residual}", epilogue);
+  const int32_t swiglu = epilogue == 1;
   MOSAIC_REQUIRE(A && W && C, "null operands");
   MOSAIC_REQUIRE(G >= 1 && G <= kMaxGroups, "G=%d not in [1, %d]", G, kMaxGroups);
   MOSAIC_REQUIRE(group_off != nullptr || G == 1, "several groups need device offsets");
@@ -365,6 +393,7 @@ extern "C" int mosaic_ffn_gemm(const uint16_t* A, int64_t rows_cap, int64_t lda,
   p.K = static_cast<int32_t>(K);
   p.n_tiles = static_cast<int32_t>(ceil_div(N, BN));
   p.swiglu = swiglu ? 1 : 0;
+  p.residual = epilogue == 2 ? 1 : 0;
   p.C = C;
   p.ldc = ldc;
   st = cg == 2 ? launch_k10<2>(ta, tb, p, rows_cap, as_stream(stream))

@@ -69,9 +69,6 @@ constexpr int kMaxSplits = 64;
 #ifndef MOSAIC_K3_EPI_SLEEP_NS
 #define MOSAIC_K3_EPI_SLEEP_NS 0   // epilogue poll backoff while the next accumulator fills
 #endif
-#ifndef MOSAIC_K3_GFENCE
-#define MOSAIC_K3_GFENCE 1  // gather mode: proxy fence per stage (0 = none, experiment)
-#endif
 #ifndef MOSAIC_K3_PROD_SLEEP_NS
 #define MOSAIC_K3_PROD_SLEEP_NS 0  // producer poll backoff while the ring is full
 #endif
@@ -217,10 +214,26 @@ __device__ __forceinline__ void cp_async16(uint32_t dst, const void* src, uint64
   asm volatile("cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %2;" ::"r"(dst), "l"(src), "l"(policy)
                : "memory");
 }
-// Arrive on a local mbarrier once all of this thread's prior cp.async copies
-// have landed (no blocking; the barrier's count includes these arrivals).
-__device__ __forceinline__ void cp_async_arrive_noinc(uint64_t* bar) {
-  asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(bar)) : "memory");
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
+
+// cp.async A path: a slot is released LAG stages after it is issued, so up to
+// LAG + 1 stages of each loader thread's copies stay in flight. LAG < STAGES
+// leaves the producer a free slot to issue into (no deadlock): 4 of 6 stages
+// on pairs, 2 of 4 on single CTAs.
+template <int STAGES>
+constexpr int a_lag() { return STAGES - 2 < 4 ? STAGES - 2 : 4; }
+
+// Release the slot issued LAG stages before `stage`: wait until at most LAG of
+// this thread's copy groups are pending (so that slot's group has landed),
+// fence its generic-proxy writes to the async proxy, then arrive (release).
+template <int STAGES>
+__device__ __forceinline__ void a_release(uint64_t* afull, uint32_t stage) {
+  constexpr int LAG = a_lag<STAGES>();
+  static_assert(LAG >= 1 && LAG < STAGES, "bad lag");
+  asm volatile("cp.async.wait_group %0;" ::"n"(LAG) : "memory");
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  mbar_arrive(&afull[(stage + STAGES - LAG) % STAGES]);
 }
 
 
@@ -343,6 +356,7 @@ __global__ void __launch_bounds__(threads_for(kGather, kSample), 1)
     const uint64_t pol_a = (p.policy == 1 || p.policy == 3) ? policy_evict_last() : policy_evict_normal();
     const uint64_t pol_b = (p.policy == 2 || p.policy == 3) ? policy_evict_first() : policy_evict_normal();
     uint32_t stage = 0, phase = 0;
+    int64_t a_issued = 0;  // cp.async A path: stages issued by this thread
     for (int64_t u = u_first; u < units_here; u += u_stride) {
       int mb, s;
       unit_coords(p, m_blocks, u, mb, s);
@@ -414,7 +428,14 @@ __global__ void __launch_bounds__(threads_for(kGather, kSample), 1)
               const int r = row0 + 4 * i + (lane >> 3);  // row within the CTA's 128-row block
               cp_async16(dst0 + r * (BK * 2) + ((chunk ^ (r & 7)) << 4), hk + off[i], pol_a);
             }
-            cp_async_arrive_noinc(&afull[stage]);
+            // writer-side release of the slot issued kALag stages ago: this
+            // thread's copies of it have landed (wait_group), its generic-proxy
+            // smem writes are ordered before the tensor core's async-proxy
+            // reads (fence.proxy.async by the writing thread), then a release
+            // arrive that the MMA issuer acquires (PTX memory model: proxy
+            // fence after the writes, before the synchronising release)
+            cp_async_commit();
+            if (++a_issued > a_lag<C::STAGES>()) a_release<C::STAGES>(afull, stage);
             if (++stage == C::STAGES) {
               stage = 0;
               phase ^= 1;
@@ -458,6 +479,16 @@ __global__ void __launch_bounds__(threads_for(kGather, kSample), 1)
       }
       __syncwarp();
     }
+    if constexpr (kGather == kGatherCpAsync) {
+      // drain: release the last min(issued, kALag) slots, oldest first
+      cp_async_wait_all();
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      const int64_t pend = a_issued < a_lag<C::STAGES>() ? a_issued : a_lag<C::STAGES>();
+      for (int64_t i = pend; i >= 1; --i) {
+        const uint32_t st = static_cast<uint32_t>((stage + C::STAGES - i) % C::STAGES);
+        mbar_arrive(&afull[st]);
+      }
+    }
   } else if (warp == 1) {
     // ------------------------------------------------------------ MMA issuer (pair leader)
     if (lane == 0 && rank == 0) {
@@ -483,7 +514,6 @@ __global__ void __launch_bounds__(threads_for(kGather, kSample), 1)
               // serialised the pair ring at ~0.9 us per stage
               // (profiles/r01_k3_gather_modes.txt).
               mbar_wait(&afull[stage], phase);
-              if (MOSAIC_K3_GFENCE) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
             }
             tc_fence_after();
             const uint32_t a0 = smem_u32(sA + stage * C::A_BYTES);
@@ -518,10 +548,10 @@ __global__ void __launch_bounds__(threads_for(kGather, kSample), 1)
           for (int t = t0; t < t1; ++t)
             for (int kb = 0; kb < k_blocks; ++kb) {
               mbar_wait(&afull[stage], phase);
-              // peer rows -> async proxy, then a CTA-scope (release.cta) arrive on
-              // the leader's barrier: the form CUTLASS's cluster pipelines use for
+              // the peer's writers fenced their rows to the async proxy before
+              // arriving; forward with a default-semantics remote arrive on the
+              // leader's barrier: the form CUTLASS's cluster pipelines use for
               // remote arrives (cutlass/arch/barrier.h ClusterBarrier::arrive)
-              if (MOSAIC_K3_GFENCE) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
               asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(
                                mapa_shared(smem_u32(&afull[stage]), 0))
                            : "memory");
@@ -820,8 +850,9 @@ int launch(const ASource& a, int64_t m_cap, const int32_t* m_dev, int64_t m_host
     p.h = a.base;
     p.ld_h = a.ld;
     static const int gmode = env_int("MOSAIC_K3_GATHER", kGatherCpAsync);  // 1 = TMA gather4 (measured slower)
-    if constexpr (kStore) {
-      return fail(MOSAIC_E_UNSUPPORTED, "gather mode has no logits debug path");
+    if constexpr (kStore) {  // materialised logits straight from H at idx (the drop-in gather_gemm)
+      st = cg == 2 ? launch_cg<2, true, kGatherCpAsync>(ta, tb, p, m_cap, s)
+                   : launch_cg<1, true, kGatherCpAsync>(ta, tb, p, m_cap, s);
     } else if (gmode == kGatherTma4) {
       st = cg == 2 ? launch_cg<2, false, kGatherTma4>(ta, tb, p, m_cap, s)
                    : launch_cg<1, false, kGatherTma4>(ta, tb, p, m_cap, s);
@@ -974,6 +1005,36 @@ extern "C" int mosaic_lmhead_stats_gather_die(const uint16_t* H, int64_t n_rows,
   MOSAIC_REQUIRE(die_of_sm && sched_scratch, "die-aware gather needs the die map and its 16-byte scratch");
   return lmhead_stats_gather_impl(H, n_rows, ld_h, idx, shift, m_cap, m_dev, m_host, W, V_shard, d, v_offset,
                                   n_splits, part_max, part_sum, part_arg, die_of_sm, sched_scratch, stream);
+}
+
+extern "C" int mosaic_lmhead_logits_gather(const uint16_t* H, int64_t n_rows, int64_t ld_h, const int32_t* idx,
+                                           int32_t shift, int64_t m_cap, const int32_t* m_dev, int64_t m_host,
+                                           const uint16_t* W, int64_t V_shard, int64_t d, float* out, int64_t ldo,
+                                           void* stream) {
+  MOSAIC_REQUIRE(H && idx, "null operands");
+  MOSAIC_REQUIRE(n_rows >= 1 && n_rows < (int64_t(1) << 31), "n_rows out of range");
+  MOSAIC_REQUIRE(out != nullptr && ldo >= V_shard, "bad logits output");
+  Params p{};
+  p.tiles_per_split = static_cast<int32_t>(ceil_div(V_shard, BN));
+  p.n_splits = 1;
+  p.out = out;
+  p.ldo = ldo;
+  return launch<true>(ASource{H, n_rows, ld_h, idx, shift ? 1 : 0}, m_cap, m_dev, m_host, W, V_shard, d, p, stream);
+}
+
+extern "C" int mosaic_lmhead_config(int64_t m_cap, int32_t gather, int64_t* out) {
+  MOSAIC_REQUIRE(out != nullptr, "null output");
+  const int cg = cta_group_for(m_cap);
+  const bool cp = gather != 0;
+  out[0] = cg;                                                   // SMs per tile (cta_group)
+  out[1] = cg == 2 ? Cfg<2>::STAGES : Cfg<1>::STAGES;            // shared-memory ring stages
+  out[2] = BM;                                                   // A rows staged per CTA
+  out[3] = BK;                                                   // K per stage
+  out[4] = BN / cg;                                              // W rows staged per CTA
+  out[5] = TMEM_COLS;                                            // TMEM columns (fp32 x 128 lanes)
+  out[6] = cg == 2 ? Cfg<2>::SMEM : Cfg<1>::SMEM;                // dynamic shared memory per CTA (bytes)
+  out[7] = threads_for(cp ? kGatherCpAsync : kGatherNone, false);
+  return MOSAIC_OK;
 }
 
 extern "C" int mosaic_lmhead_logits(const uint16_t* Hc, int64_t m_cap, const int32_t* m_dev,

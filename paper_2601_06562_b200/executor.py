@@ -12,10 +12,12 @@ live outside the workspace, as in the reference (mosaic/liveness.py:52-53).
 
 Op kinds (mosaic/workload.py:179-316, plus the fused-logits kinds):
 
-* embed / matmul / fused_attention / add / alloc — model forward (cuBLAS and
-  PyTorch SDPA; not the hot path);
+* embed / matmul / fused_attention (K11 rotary positions + PyTorch SDPA) /
+  add / alloc — model forward (not the hot path);
 * ffn_up / ffn_gate / glu (K6) / activation / ffn_down / chunk_write — the
-  lazily chunked FFN, rows [i*ceil(L/K_FFN), ...) per iteration;
+  lazily chunked FFN, rows [i*ceil(L/K_FFN), ...) per iteration; with
+  ``fused_ffn``: ffn_gate_up (K10 + SwiGLU epilogue) / ffn_down_res (K10 +
+  residual epilogue: down, chunk_write and the residual add in one launch);
 * gather (K2) / lmhead_stats (K3) / sample (K4) / commit (K5) — the fused
   mask-only logits + remask hot path (``logits_mode="fused"``);
 * gather_logits / logits / shift / chunk_write / sample — the reference's
@@ -24,6 +26,7 @@ Op kinds (mosaic/workload.py:179-316, plus the fused-logits kinds):
 """
 from __future__ import annotations
 
+import ctypes
 import math
 from typing import Optional
 
@@ -49,10 +52,12 @@ class RandomDLLM:
 
     ``distinct_layers`` limits how many layer weight sets are materialised;
     layer i uses set ``i % distinct_layers`` (the context sweep allocates all
-    of them to charge the full weight footprint)."""
+    of them to charge the full weight footprint). ``rope_theta`` (LLaDA-8B's
+    500000 by default; None = no positions) sets the rotary embedding K11
+    applies to q and k inside ``fused_attention``."""
 
     def __init__(self, cfg: ModelConfig, device, seed: int = 0, distinct_layers: Optional[int] = None,
-                 vocab_shard: tuple[int, int] | None = None):
+                 vocab_shard: tuple[int, int] | None = None, rope_theta: Optional[float] = 500000.0):
         if cfg.moe is not None and cfg.logits_mode not in ("fused", "fused_gather"):
             raise InputError("MoE models execute through the fused template (logits_mode='fused'), "
                              "whose FFN block carries the expert routing")
@@ -80,7 +85,7 @@ class RandomDLLM:
                 lw["w_down"] = w(E, f, d, scale=0.02 * out_scale).transpose(1, 2).contiguous().view(E * d, f)
             elif cfg.fused_ffn and fused:
                 lw["w_gate_up"] = hotpath.interleave_gate_up(w(d, f), w(d, f))  # [2f, d]
-                lw["w_down"] = w(f, d, scale=0.02 * out_scale)
+                lw["w_down"] = w(f, d, scale=0.02 * out_scale).t().contiguous()  # [d, f] K-major for K10
             else:
                 lw.update(w_up=w(d, f), w_down=w(f, d, scale=0.02 * out_scale))
                 if cfg.gated_ffn:
@@ -91,6 +96,9 @@ class RandomDLLM:
         w_vocab = w(V, d)  # the full head from the same stream, so a shard is a slice of the unsharded model
         self.w_vocab = w_vocab if (v0, v1) == (0, V) else w_vocab[v0:v1].contiguous()  # [V_shard, d]
         del w_vocab
+        self.rope_theta = rope_theta
+        self.inv_freq = (None if rope_theta is None
+                         else hotpath.rope_inv_freq(d // cfg.n_heads, float(rope_theta), device))
 
     def layer(self, i: int) -> dict:
         return self.layers[i % len(self.layers)]
@@ -100,6 +108,22 @@ class RandomDLLM:
         for lw in self.layers:
             n += sum(t.numel() for t in lw.values())
         return 2 * n
+
+
+_ALLOCATOR = None
+
+
+def _scratch_allocator():
+    """One pluggable allocator over csrc/pool.cu for the process (each executor's
+    MemPool draws from the region it selects before its step)."""
+    global _ALLOCATOR
+    if _ALLOCATOR is None:
+        from . import _native
+
+        _native.load()
+        _ALLOCATOR = torch.cuda.memory.CUDAPluggableAllocator(str(_native.LIB_PATH), "mosaic_pool_alloc",
+                                                              "mosaic_pool_free")
+    return _ALLOCATOR
 
 
 def _rows(n_total: int, trips: int, it: Optional[int]) -> tuple[int, int]:
@@ -140,6 +164,17 @@ class StepExecutor:
         self._die_table = None
         self._die_tried = False
         self._sched = torch.zeros(4, dtype=torch.int32, device=dev)
+        # torch-side step temporaries (attention outputs, cuBLAS scratch) live in a
+        # region at the start of the arena, served by csrc/pool.cu through a MemPool;
+        # the planned activations follow it (offsets shifted by its size)
+        self.scratch_bytes = 0
+        self._pool = None
+        # cuBLAS / cuBLASLt keep one workspace per handle and stream for the life of
+        # the process: create it now, outside the step, so it is not charged to (and
+        # pinned inside) the step's scratch region
+        a = torch.zeros(64, 64, dtype=torch.bfloat16, device=dev)
+        torch.matmul(a, a)
+        torch.mm(a, a, out_dtype=torch.float32)
         if hotpath.die_aware_default(die_aware, 1 << 30, model.w_vocab.shape[0]):
             # measured now (a one-off probe with ~250 MB of scratch), not mid-step next to a full arena
             self._die_table = hotpath.die_table_or_none(dev)
@@ -152,6 +187,59 @@ class StepExecutor:
             self._die_table = hotpath.die_table_or_none(self.device)
             self._die_tried = True
         return self._die_table
+
+    # ---------------------------------------------------------------- scratch
+    def scratch_bytes_for(self, L: int) -> int:
+        """Size of the arena's torch-scratch region for sequences of length L:
+        the attention call's temporaries for one query block (output
+        [rows, d] bf16 + per-head log-sum-exp fp32 + its q/k/v staging, each
+        rounded to the caching allocator's 2 MiB segments) with 64 MiB of
+        headroom. Measured use is reported per step (``pool_high_water``); an
+        undersized region fails loudly with torch's out-of-memory error."""
+        cfg = self.cfg
+        qb = min(L, ATTN_BLOCK)
+        mib2 = 2 << 20
+        blk = -(-(qb * cfg.d_model * 2) // mib2) * mib2
+        lse = -(-(cfg.n_heads * qb * 4) // mib2) * mib2
+        need = 4 * blk + 2 * lse + (64 << 20)
+        return -(-need // self.ws.page_size) * self.ws.page_size
+
+    def _ensure_scratch(self, need: int) -> None:
+        from . import _native
+
+        if need > self.scratch_bytes:  # create, or grow in place (live blocks stay where they are)
+            if self.ws.committed_bytes < need:
+                self.ws.commit_to(need)
+            _native.call("mosaic_pool_bind", self.ws.device, ctypes.c_void_p(self.ws.base), int(need))
+            self.scratch_bytes = need
+        if self._pool is None:
+            self._pool = torch.cuda.MemPool(_scratch_allocator().allocator())
+            self.ws.on_close(self.close)
+
+    def close(self) -> None:
+        """Release the scratch pool before the arena goes away (called by the
+        workspace's close): cached segments are returned, the region forgotten."""
+        from . import _native
+
+        if self._pool is None:
+            return
+        torch.cuda.synchronize(self.device)
+        self._pool = None
+        import gc
+
+        gc.collect()
+        torch.cuda.empty_cache()
+        if self.ws.base is not None:
+            _native.call("mosaic_pool_unbind", self.ws.device, ctypes.c_void_p(self.ws.base))
+        self.scratch_bytes = 0
+
+    def pool_stats(self) -> dict:
+        from . import _native
+
+        vals = [ctypes.c_uint64() for _ in range(4)]
+        _native.call("mosaic_pool_stats", self.ws.device, ctypes.c_void_p(self.ws.base),
+                     *(ctypes.byref(v) for v in vals))
+        return dict(zip(("in_use", "high_water", "allocs", "refused"), (int(v.value) for v in vals)))
 
     # ---------------------------------------------------------------- buffers
     def _side_buffers(self, L: int) -> dict:
@@ -190,7 +278,7 @@ class StepExecutor:
                 if 0 in shape:
                     views[key] = torch.empty(shape, dtype=dtype, device=self.device)
                 else:
-                    views[key] = self.ws.view(base, shape, dtype)
+                    views[key] = self.ws.view(self.scratch_bytes + base, shape, dtype)
         return views
 
     # ---------------------------------------------------------------- run
@@ -208,16 +296,21 @@ class StepExecutor:
         and the result carries device milliseconds per op kind."""
         if table is None or plan is None:
             table, plan = self.plan(g)
-        if plan.workspace_size > self.ws.committed_bytes:
-            self.ws.commit_to(plan.workspace_size)
         b = g.bindings
         L, M = b["L"], b["M"]
         if x.dtype != torch.int32 or x.numel() != L:
             raise InputError("x must be int32 [L]")
-        side = self._side_buffers(L)
         kinds = {op.kind for op in g.ops}  # the graph, not the model config, fixes the logits mode
         fused = "lmhead_stats" in kinds or "lmhead_stats_gather" in kinds
         self._mode = "fused" if fused else ("mask_only" if "gather_logits" in kinds else "eager")
+        # the B200 path runs the whole step in the arena: torch-side temporaries in the
+        # scratch region (MemPool), activations at their planned offsets after it. The
+        # reference's materialising modes are the dense-logits baselines: torch allocator.
+        if fused:
+            self._ensure_scratch(self.scratch_bytes_for(L))
+        if self.scratch_bytes + plan.workspace_size > self.ws.committed_bytes:
+            self.ws.commit_to(self.scratch_bytes + plan.workspace_size)
+        side = self._side_buffers(L)
         views = self._views(g, table, plan)
         kept: dict[str, torch.Tensor] = {}
         start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -229,6 +322,33 @@ class StepExecutor:
         if self.exec_layers is not None:
             skip_layers = {f"l{i}." for i in range(self.exec_layers, self.cfg.n_layers)}
         marks = []
+        keep_dst = {key: torch.empty_like(views[key]) for op in g.ops for key in op.outputs if key[0] in keep}
+        if "token_out" in keep:
+            keep_dst.update({(n, None): torch.empty_like(views[(n, None)]) for n in ("token_out", "confidence")})
+        from contextlib import nullcontext
+
+        if fused:
+            from . import _native
+
+            _native.call("mosaic_pool_select", self.ws.device, ctypes.c_void_p(self.ws.base))
+        with torch.cuda.use_mem_pool(self._pool) if fused else nullcontext():
+            self._run_ops(g, views, x, mask_idx, side, k_unmask, skip_layers, profile, marks, keep_dst, kept)
+        end.record()
+        end.synchronize()
+        m_seen = int(side["m_dev"].item())  # K1's count; the step was planned for the binding M
+        if m_seen != M:
+            raise InputError(f"x holds {m_seen} masked positions but the step graph was instantiated for M={M} "
+                             "(only the first min(count, M) masked rows were eligible for the commit)")
+        by_kind: dict[str, float] = {}
+        for kind, e0, e1 in marks:
+            by_kind[kind] = by_kind.get(kind, 0.0) + e0.elapsed_time(e1)
+        return {"ms": start.elapsed_time(end), "workspace_bytes": plan.workspace_size,
+                "committed_bytes": self.ws.committed_bytes, "scratch_bytes": self.scratch_bytes,
+                "pool": self.pool_stats() if fused else None, "ops": len(g.ops), "kept": kept,
+                "ms_by_kind": by_kind}
+
+    def _run_ops(self, g, views, x, mask_idx, side, k_unmask, skip_layers, profile, marks, keep_dst, kept) -> None:
+        keep = {key[0] for key in keep_dst}
         for op in g.ops:
             if skip_layers and op.op_id[:op.op_id.find(".") + 1] in skip_layers:
                 continue
@@ -240,24 +360,13 @@ class StepExecutor:
                 e1 = torch.cuda.Event(enable_timing=True)
                 e1.record()
                 marks.append((op.kind, e0, e1))
+            # copies out of the arena (tests / profiling) into buffers allocated before the step
             for key in op.outputs:
                 if key[0] in keep:
-                    kept[key[0] if key[1] is None else f"{key[0]}@{key[1]}"] = views[key].clone()
+                    kept[key[0] if key[1] is None else f"{key[0]}@{key[1]}"] = keep_dst[key].copy_(views[key])
             if op.kind == "sample" and "token_out" in keep:
-                kept["token_out"] = views[("token_out", None)].clone()
-                kept["confidence"] = views[("confidence", None)].clone()
-        end.record()
-        end.synchronize()
-        m_seen = int(side["m_dev"].item())  # K1's count; the step was planned for the binding M
-        if m_seen != M:
-            raise InputError(f"x holds {m_seen} masked positions but the step graph was instantiated for M={M} "
-                             "(only the first min(count, M) masked rows were eligible for the commit)")
-        by_kind: dict[str, float] = {}
-        for kind, e0, e1 in marks:
-            by_kind[kind] = by_kind.get(kind, 0.0) + e0.elapsed_time(e1)
-        return {"ms": start.elapsed_time(end), "workspace_bytes": plan.workspace_size,
-                "committed_bytes": self.ws.committed_bytes, "ops": len(g.ops), "kept": kept,
-                "ms_by_kind": by_kind}
+                for name in ("token_out", "confidence"):
+                    kept[name] = keep_dst[(name, None)].copy_(views[(name, None)])
 
     # ---------------------------------------------------------------- ops
     def _dispatch(self, op, g: ConcreteGraph, v, x, mask_idx, side, k_unmask: int) -> None:
@@ -274,6 +383,8 @@ class StepExecutor:
             q, k, vv = (v[key] for key in op.inputs)
             H = cfg.n_heads
             dh = d // H
+            if self.model.inv_freq is not None:  # K11: positions, in place on q and k (read only here)
+                hotpath.rope_qk_(q, k, H, self.model.inv_freq)
             qh, kh, vh = (t.view(L, H, dh).transpose(0, 1).unsqueeze(0) for t in (q, k, vv))
             out = v[op.outputs[0]].view(L, H, dh)
             # bidirectional dLLM attention, query-blocked so the library's output
@@ -296,6 +407,14 @@ class StepExecutor:
             f = cfg.d_ff
             hotpath.ffn_gemm(v[op.inputs[0]][r0:r1], self._layer(op.op_id)["w_gate_up"], v[op.outputs[0]][: r1 - r0],
                              2 * f, m_host=r1 - r0, swiglu=True)
+        elif kind == "ffn_down_res":  # K10: h_attn[rows] += act @ w_down (down + chunk_write + residual)
+            r0, r1 = _rows(L, b["K_FFN"], op.iteration)
+            if r1 > r0:
+                act, h = v[op.inputs[0]], v[op.inputs[2]]
+                hotpath.ffn_gemm(act[: r1 - r0], self._layer(op.op_id)["w_down"], h[r0:r1], d, m_host=r1 - r0,
+                                 residual=True)
+        elif kind == "identity":
+            pass  # in-place output naming the mutated storage (planned as one storage group)
         elif kind in ("ffn_up", "ffn_gate"):
             layer = self._layer(op.op_id)
             r0, r1 = _rows(L, b["K_FFN"], op.iteration)

@@ -262,6 +262,29 @@ def lmhead_logits(hc: torch.Tensor, weight: torch.Tensor, out: torch.Tensor, m_d
 
 
 # ----------------------------------------------------------------- K4 / K5
+def lmhead_logits_gather(hidden: torch.Tensor, idx: torch.Tensor, weight: torch.Tensor, out: torch.Tensor,
+                         m_dev=None, m_host: int = 0, shift: bool = False, stream=None) -> None:
+    """Materialised logits out[r] = hidden[src(idx[r])] @ weight.T (fp32), A rows
+    gathered inside K3 (no [m, d] buffer): the drop-in gather_gemm's kernel."""
+    _req(hidden, torch.bfloat16, "hidden", 2)
+    _req(weight, torch.bfloat16, "weight", 2)
+    _req(idx, torch.int32, "idx", 1)
+    if out.dtype != torch.float32 or out.stride(1) != 1 or out.shape[1] < weight.shape[0]:
+        raise InputError("out must be fp32 [m, >= V] with contiguous rows")
+    m = min(idx.numel(), out.shape[0])
+    _native.call("mosaic_lmhead_logits_gather", _p(hidden), hidden.shape[0], hidden.stride(0), _p(idx), int(shift),
+                 m, _p(m_dev), int(m_host), _p(weight), weight.shape[0], weight.shape[1], _p(out), out.stride(0),
+                 _s(stream))
+
+
+def lmhead_config(m_cap: int, gather: bool = False) -> dict:
+    """The K3 configuration a launch over m_cap rows uses (mosaic_lmhead_config)."""
+    out = (ctypes.c_int64 * 8)()
+    _native.call("mosaic_lmhead_config", int(m_cap), int(bool(gather)), out)
+    keys = ("cta_group", "stages", "a_rows", "k_step", "w_rows", "tmem_cols", "smem_bytes", "threads")
+    return dict(zip(keys, (int(v) for v in out)))
+
+
 def stats_merge(in_max, in_sum, in_arg, S: int, stride: int, m_cap: int, m_dev=None, m_host: int = 0,
                 out_max=None, out_sum=None, out_arg=None, token=None, lse=None, conf=None,
                 stream=None) -> None:
@@ -292,6 +315,28 @@ def remask_commit_segmented(conf, pos, token, x, m_cap: int, seg_len: int, n_seg
             raise InputError("k_per_seg must hold one count per segment")
     _native.call("mosaic_remask_commit_segmented", _p(conf), _p(pos), _p(token), _p(m_dev), int(m_host),
                  int(m_cap), int(seg_len), int(n_seg), _p(k_per_seg), int(k), _p(x), _p(selected), _s(stream))
+
+
+# ----------------------------------------------------------------- K11
+def rope_inv_freq(head_dim: int, theta: float, device) -> torch.Tensor:
+    """theta^(-2i/head_dim), i < head_dim/2, fp32 -- the same expression as the
+    torch reference (tests/torch_reference.py)."""
+    return 1.0 / (theta ** (torch.arange(0, head_dim, 2, dtype=torch.float32, device=device) / head_dim))
+
+
+def rope_qk_(q: torch.Tensor, k: torch.Tensor, n_heads: int, inv_freq: torch.Tensor, pos0: int = 0,
+             stream=None) -> None:
+    """In place: rotary embedding of q and k ([L, n_heads * head_dim] bf16 rows)."""
+    _req(q, torch.bfloat16, "q", 2)
+    _req(k, torch.bfloat16, "k", 2)
+    if q.shape != k.shape or q.stride() != k.stride() or q.stride(1) != 1:
+        raise InputError("q and k must be [L, d] row-major views of the same shape and stride")
+    _req(inv_freq, torch.float32, "inv_freq", 1)
+    dh = q.shape[1] // n_heads
+    if inv_freq.numel() != dh // 2:
+        raise InputError(f"inv_freq must hold head_dim/2 = {dh // 2} entries")
+    _native.call("mosaic_rope_qk", _p(q), _p(k), q.shape[0], int(n_heads), int(dh), q.stride(0), _p(inv_freq),
+                 int(pos0), _s(stream))
 
 
 # ----------------------------------------------------------------- K6
@@ -359,9 +404,13 @@ def interleave_gate_up(w_gate: torch.Tensor, w_up: torch.Tensor) -> torch.Tensor
 
 
 def ffn_gemm(a: torch.Tensor, w: torch.Tensor, out: torch.Tensor, n: int, group_off: Optional[torch.Tensor] = None,
-             groups: int = 1, m_host: int = 0, swiglu: bool = False, stream=None) -> None:
+             groups: int = 1, m_host: int = 0, swiglu: bool = False, residual: bool = False,
+             stream=None) -> None:
     """K10: out[rows of group g] = a[rows of g] @ w[g].T (bf16, fp32 accumulate),
-    w = [groups * n, K] K-major; with ``swiglu`` out = silu(gate) * up, n/2 columns."""
+    w = [groups * n, K] K-major; with ``swiglu`` out = silu(gate) * up, n/2
+    columns; with ``residual`` out += a @ w.T in place (one bf16 rounding)."""
+    if swiglu and residual:
+        raise InputError("swiglu and residual epilogues are exclusive")
     if a.dtype != torch.bfloat16 or a.dim() != 2 or a.stride(1) != 1 or not a.is_cuda:
         raise InputError("a must be 2-D bf16 with contiguous rows")
     if out.dtype != torch.bfloat16 or out.dim() != 2 or out.stride(1) != 1:
@@ -378,8 +427,9 @@ def ffn_gemm(a: torch.Tensor, w: torch.Tensor, out: torch.Tensor, n: int, group_
             raise InputError("group_off needs groups + 1 entries")
     elif groups != 1:
         raise InputError("several groups need device offsets")
-    _native.call("mosaic_ffn_gemm", _p(a), min(a.shape[0], out.shape[0]), a.stride(0), _p(group_off), int(groups),
-                 int(m_host), _p(w), int(n), K, int(bool(swiglu)), _p(out), out.stride(0), _s(stream))
+    _native.call("mosaic_ffn_gemm_ex", _p(a), min(a.shape[0], out.shape[0]), a.stride(0), _p(group_off),
+                 int(groups), int(m_host), _p(w), int(n), K, 2 if residual else int(bool(swiglu)), _p(out),
+                 out.stride(0), _s(stream))
 
 
 # ----------------------------------------------------------------- buffers

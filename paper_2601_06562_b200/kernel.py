@@ -8,9 +8,12 @@ the tcgen05 LM-head kernel K3 with BF16 operands and FP32 accumulation, so
 results match the float64 reference within BF16/FP32 tolerance, not 1e-12.
 
 ``gather_gemm`` materialises ``[m, V]`` exactly like the reference (kernel.py:68)
-for parity; the production path is the sibling :func:`gather_logits_stats`,
-which returns only (token, lse, confidence) per masked row and never writes
-the logits.
+for parity, with K3 in gather mode: the A rows are read from ``hidden`` at
+``mask_idx`` inside the kernel, so -- as SPEC.md:550 requires of the
+reference -- no ``[m, d]`` gathered copy exists, and the returned
+:class:`ScratchAccount` proves it against a bound that fails when one does.
+The production path is the sibling :func:`gather_logits_stats`, which returns
+only (token, lse, confidence) per masked row and never writes the logits.
 """
 from __future__ import annotations
 
@@ -23,8 +26,11 @@ import torch
 from . import hotpath
 from .errors import InputError
 
-# hardware tile of K3 (rows x K-stage x vocab) and its on-chip buffering
-TILE_M, TILE_K, TILE_V, SMEM_STAGES, TMEM_BUFFERS = 128, 64, 256, 4, 2
+# K3's K granularity (d is zero-padded to a multiple of it)
+TILE_K = 64
+# on-chip capacity of one B200 SM: opt-in shared memory per block and tensor memory
+SM_SMEM_OPTIN_BYTES = 232448   # 227 KB (cudaDevAttrMaxSharedMemoryPerBlockOptin on sm_100a)
+TMEM_LANES, TMEM_MAX_COLS = 128, 512
 
 
 @dataclass(frozen=True)
@@ -54,10 +60,19 @@ class GatherGemmProblem:
 
 @dataclass(frozen=True)
 class ScratchAccount:
-    """On-chip scratch of one CTA, in elements: SMEM_STAGES stages of the hidden
-    and weight panels plus TMEM_BUFFERS fp32 accumulators. ``bound`` applies the
-    reference formula (kernel.py:52-59) per buffer, so no global gathered copy
-    beyond the [M, d] operand panel is ever charged."""
+    """Peak scratch elements used by the kernel beyond its inputs and output,
+    and the bound they must respect (mosaic/kernel.py:52-59).
+
+    The reference bounds the scratch by one tile working set, tm*td + td*tv +
+    tm*tv elements, which rules out a global [m, d] gathered copy. The device
+    kernel's tile working set is the launched configuration's on-chip staging
+    per CTA -- ``stages`` shared-memory panels of (A rows + W rows) x K-step
+    bf16 elements plus the fp32 TMEM accumulators (``device_scratch``) -- and
+    its bound is what one SM can hold: opt-in shared memory (as bf16 elements)
+    plus tensor memory (128 lanes x 512 fp32 columns). A gathered [m, d] copy
+    in global memory is charged to ``peak_elements`` too, so ``within_bound``
+    fails whenever one exists (the buffered K2 + K3 path at any real m), as it
+    fails for a configuration that would not fit the SM."""
 
     peak_elements: int
     bound: int
@@ -67,11 +82,17 @@ class ScratchAccount:
         return self.peak_elements <= self.bound
 
 
-def device_scratch() -> ScratchAccount:
-    panels = SMEM_STAGES * (TILE_M * TILE_K + TILE_K * TILE_V)
-    acc = TMEM_BUFFERS * TILE_M * TILE_V
-    bound = SMEM_STAGES * (TILE_M * TILE_K + TILE_K * TILE_V) + TMEM_BUFFERS * TILE_M * TILE_V
-    return ScratchAccount(panels + acc, bound)
+def device_scratch(m_cap: int, d: int, gather: bool = True,
+                   smem_capacity_bytes: int = SM_SMEM_OPTIN_BYTES) -> ScratchAccount:
+    """ScratchAccount of the K3 launch for ``m_cap`` rows (configuration read
+    from the library, ``mosaic_lmhead_config``). ``gather=False`` charges the
+    [m_cap, d] buffer K2 writes for the buffered path."""
+    cfg = hotpath.lmhead_config(m_cap, gather)
+    stages = cfg["stages"] * (cfg["a_rows"] + cfg["w_rows"]) * cfg["k_step"]  # bf16 panels per CTA
+    acc = TMEM_LANES * cfg["tmem_cols"]                                      # fp32 accumulators per CTA
+    gathered = 0 if gather else int(m_cap) * int(d)                          # global [m, d] copy
+    bound = smem_capacity_bytes // 2 + TMEM_LANES * TMEM_MAX_COLS
+    return ScratchAccount(stages + acc + gathered, bound)
 
 
 def _to_device_bf16(a, device) -> torch.Tensor:
@@ -114,14 +135,13 @@ def gather_gemm(p: GatherGemmProblem, device=None) -> tuple[object, ScratchAccou
     m = idx.numel()
     V = Wt.shape[0]
     out = torch.empty((max(m, 1), V), dtype=torch.float32, device=dev)
-    if m:
-        hc = torch.empty((m, H.shape[1]), dtype=torch.bfloat16, device=dev)
-        hotpath.gather_rows(H, idx, hc, m_host=m)
-        hotpath.lmhead_logits(hc, Wt, out, m_host=m)
+    if m:  # gather-mode K3: A rows read from H at idx inside the kernel (no [m, d] copy)
+        hotpath.lmhead_logits_gather(H, idx, Wt, out, m_host=m)
     out = out[:m]
+    scratch = device_scratch(max(m, 1), H.shape[1], gather=True)
     if isinstance(p.hidden, torch.Tensor):
-        return out, device_scratch()
-    return out.cpu().numpy().astype(np.asarray(p.hidden).dtype, copy=False), device_scratch()
+        return out, scratch
+    return out.cpu().numpy().astype(np.asarray(p.hidden).dtype, copy=False), scratch
 
 
 def gather_logits_stats(hidden, weight, mask_idx, *, weight_layout: str = "dv", shift: bool = False,

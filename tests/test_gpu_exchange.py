@@ -54,11 +54,15 @@ def test_p2p_exchange_world1(native_lib):
         dist.destroy_process_group()
 
 
-def _rank_main(rank, world, bufs, q):
+def _rank_main(rank, world, bufs, q, delay=0.0):
     """One vocab shard; peers reached through CUDA-IPC mappings of the other
     process's gathered/signal buffers (what symmetric memory provides across
-    NVLink peers)."""
+    NVLink peers). ``delay`` > 0: rank 1's host sleeps between enqueuing its
+    push and its wait, so the peer finishes its wait, runs a whole step and
+    publishes the next epoch before this rank's wait of the current one runs
+    (the case a wait for "slot == epoch" would miss)."""
     import sys
+    import time
 
     sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
     from paper_2601_06562_b200 import MaskOnlyHead, shard
@@ -73,6 +77,15 @@ def _rank_main(rank, world, bufs, q):
         v0, v1 = shard.vocab_shard_bounds(V, world, rank)
         head = MaskOnlyHead(W[v0:v1].contiguous(), seq_len=L, mask_id=mask_id, vocab_offset=v0, m_cap=L,
                             exchange=ex)
+        if delay > 0 and rank == 1:
+            wait = ex.wait
+
+            def late_wait(stream=None):
+                torch.cuda.synchronize()  # this rank's push has landed; the peer can run ahead
+                time.sleep(delay)
+                wait(stream)
+
+            ex.wait = late_wait
         for _ in range(3):  # three epochs through the same pads
             xd = torch.from_numpy(x).to(dev)
             o = head.step(xd, H, k)
@@ -85,7 +98,8 @@ def _rank_main(rank, world, bufs, q):
         q.put((rank, "error", repr(exc), None))
 
 
-def test_p2p_exchange_two_ranks_one_gpu(native_lib):
+@pytest.mark.parametrize("delay", [0.0, 0.5])
+def test_p2p_exchange_two_ranks_one_gpu(native_lib, delay):
     import torch.multiprocessing as mp
 
     from paper_2601_06562_b200 import MaskOnlyHead
@@ -98,7 +112,7 @@ def test_p2p_exchange_two_ranks_one_gpu(native_lib):
     torch.cuda.synchronize()
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
-    procs = [ctx.Process(target=_rank_main, args=(r, world, (gathered, signal), q)) for r in range(world)]
+    procs = [ctx.Process(target=_rank_main, args=(r, world, (gathered, signal), q, delay)) for r in range(world)]
     for p in procs:
         p.start()
     res = {}

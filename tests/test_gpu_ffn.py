@@ -99,3 +99,38 @@ def test_grouped_from_moe_routing(dev):
         xe = xin[o[e]:o[e + 1]].float()
         ref = (F.silu(xe @ wg[e].float()) * (xe @ wu[e].float())).bfloat16().float()
         torch.testing.assert_close(act[o[e]:o[e + 1]].float(), ref, rtol=2e-2, atol=2e-2)
+
+
+@pytest.mark.parametrize("L,H,dh,theta", [(1, 4, 64, 500000.0), (2048, 4, 64, 500000.0), (5000, 32, 128, 1e6)])
+def test_rope_vs_torch(dev, L, H, dh, theta):
+    """K11 rotary embedding of q and k in place against the torch fp32
+    restatement (tests/torch_reference.py): one bf16 rounding apart at most."""
+    from torch_reference import rope
+
+    from paper_2601_06562_b200 import hotpath
+
+    q = _rand((L, H * dh), dev, seed=5)
+    k = _rand((L, H * dh), dev, seed=6)
+    inv = hotpath.rope_inv_freq(dh, theta, dev)
+    rq, rk = rope(q, H, inv), rope(k, H, inv)
+    hotpath.rope_qk_(q, k, H, inv)
+    for got, want in ((q, rq), (k, rk)):
+        torch.testing.assert_close(got.float(), want.float(), rtol=1e-2, atol=1e-2)
+        assert (got != want).float().mean().item() < 0.01  # almost everywhere bit-equal
+
+
+@pytest.mark.parametrize("M,K,N", [(1, 128, 256), (777, 768, 256), (3000, 1408, 2048), (4096, 18944, 3584)])
+def test_residual_epilogue_vs_fp32(dev, M, K, N):
+    """K10 residual mode (the dense chunk's down projection + chunk write +
+    residual add): out = bf16(out + a @ w) in place, one rounding of the fp32
+    sum, against fp32 torch; rows past M untouched."""
+    from paper_2601_06562_b200 import hotpath
+
+    a = _rand((M, K), dev, seed=K)
+    w = _rand((K, N), dev, 0.02, seed=N)
+    res = _rand((M + 5, N), dev, seed=M)
+    out = res.clone()
+    hotpath.ffn_gemm(a, w.t().contiguous(), out[:M], N, m_host=M, residual=True)
+    ref = (res[:M].float() + a.float() @ w.float()).bfloat16().float()
+    torch.testing.assert_close(out[:M].float(), ref, rtol=1e-2, atol=1e-2)
+    assert torch.equal(out[M:], res[M:])

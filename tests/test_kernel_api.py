@@ -130,3 +130,25 @@ def test_gather_logits_stats_sibling(native_lib, layout, shift):
     assert np.array_equal(tok.cpu().numpy()[ok], ref["arg"][ok])
     assert orc.isclose_rel(lse.cpu().numpy(), ref["lse"], 1e-3)
     assert orc.isclose_rel(conf.cpu().numpy(), ref["conf"], 1e-3)
+
+
+def test_scratch_account_is_a_real_bound(native_lib):
+    """ScratchAccount (mosaic/kernel.py:52-59): the device account is the
+    launched K3 configuration's on-chip staging per CTA, bounded by what one SM
+    holds. It fails exactly where the reference's would: a global [m, d]
+    gathered copy (the buffered K2 path), or a configuration larger than the
+    SM. Host-only query, no kernel launch."""
+    from paper_2601_06562_b200 import hotpath
+    from paper_2601_06562_b200.kernel import SM_SMEM_OPTIN_BYTES, device_scratch
+
+    for m, cg in ((16384, 2), (100, 1)):
+        cfg = hotpath.lmhead_config(m, gather=True)
+        assert cfg["cta_group"] == cg and cfg["a_rows"] == 128 and cfg["k_step"] == 64
+        assert cfg["w_rows"] == 256 // cg and cfg["tmem_cols"] == 512
+        assert cfg["smem_bytes"] <= SM_SMEM_OPTIN_BYTES
+        staged = cfg["stages"] * (cfg["a_rows"] + cfg["w_rows"]) * cfg["k_step"]
+        assert 2 * staged <= cfg["smem_bytes"]  # the panels are what the shared memory holds
+        acc = device_scratch(m, 4096, gather=True)
+        assert acc.peak_elements == staged + 128 * 512 and acc.within_bound
+        assert not device_scratch(m, 4096, gather=False).within_bound  # a [m, d] copy breaks the bound
+        assert not device_scratch(m, 4096, gather=True, smem_capacity_bytes=96 << 10).within_bound

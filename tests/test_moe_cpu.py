@@ -131,4 +131,7 @@ def test_fused_ffn_template_holds_act_only():
     p0 = chunker.evaluate_peak(t0, b, chunker.ChunkConfig(1, 1))
     p1 = chunker.evaluate_peak(t1, b, chunker.ChunkConfig(1, 1))
     assert p1.component_peaks["ffn"] * 2 == p0.component_peaks["ffn"]  # [L, d_ff] once instead of twice
+    # the residual epilogue: no `down` chunk rows, no [L, d] ffn_acc
+    assert not ({"l0.down", "l0.ffn_acc"} & set(t1.tensors)) and any(op.kind == "ffn_down_res" for op in t1.ops)
+    assert p1.total_peak < p0.total_peak
     assert workload.model_config_from_json_dict(replace(base, fused_ffn=True).to_json_dict()).fused_ffn

@@ -23,6 +23,8 @@ def reference_forward(model: RandomDLLM, x: torch.Tensor) -> torch.Tensor:
     for i in range(cfg.n_layers):
         lw = model.layer(i)
         q, k, v = (h @ lw["w_qkv"][:, j * d:(j + 1) * d] for j in range(3))
+        if model.inv_freq is not None:
+            q, k = rope(q, H, model.inv_freq), rope(k, H, model.inv_freq)
         qh, kh, vh = (t.view(L, H, d // H).transpose(0, 1).unsqueeze(0) for t in (q, k, v))
         a = F.scaled_dot_product_attention(qh, kh, vh).squeeze(0).transpose(0, 1).reshape(L, d)
         h = h + a @ lw["w_attn_out"]
@@ -31,11 +33,23 @@ def reference_forward(model: RandomDLLM, x: torch.Tensor) -> torch.Tensor:
             continue
         if "w_gate_up" in lw:  # fused_ffn layout -> torch layout
             wg, wu = _split_gate_up(lw["w_gate_up"], cfg.d_ff)
-            lw = {**lw, "w_gate": wg, "w_up": wu}
+            lw = {**lw, "w_gate": wg, "w_up": wu, "w_down": lw["w_down"].t()}  # K-major [d, f] -> [f, d]
         up = h @ lw["w_up"]
         act = F.silu((h @ lw["w_gate"]).float()).mul(up.float()).to(torch.bfloat16) if cfg.gated_ffn else F.silu(up)
         h = h + act @ lw["w_down"]
     return h
+
+
+def rope(t: torch.Tensor, n_heads: int, inv_freq: torch.Tensor) -> torch.Tensor:
+    """Rotate-half rotary embedding of [L, n_heads * dh] bf16 rows in fp32 math
+    (the rule K11 applies in place), rounded back to bf16."""
+    L, d = t.shape
+    dh = d // n_heads
+    ang = torch.arange(L, device=t.device, dtype=torch.float32)[:, None] * inv_freq[None, :]  # [L, dh/2]
+    c, s = torch.cos(ang)[:, None, :], torch.sin(ang)[:, None, :]
+    x = t.view(L, n_heads, dh).float()
+    a, b = x[..., : dh // 2], x[..., dh // 2:]
+    return torch.cat([a * c - b * s, b * c + a * s], dim=-1).to(torch.bfloat16).view(L, d)
 
 
 def _moe_reference(cfg: ModelConfig, lw: dict, h: torch.Tensor) -> torch.Tensor:
