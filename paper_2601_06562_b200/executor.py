@@ -169,6 +169,7 @@ class StepExecutor:
         # the planned activations follow it (offsets shifted by its size)
         self.scratch_bytes = 0
         self._pool = None
+        self._fitted_L = None
         # cuBLAS / cuBLASLt keep one workspace per handle and stream for the life of
         # the process: create it now, outside the step, so it is not charged to (and
         # pinned inside) the step's scratch region
@@ -190,12 +191,13 @@ class StepExecutor:
 
     # ---------------------------------------------------------------- scratch
     def scratch_bytes_for(self, L: int) -> int:
-        """Size of the arena's torch-scratch region for sequences of length L:
-        the attention call's temporaries for one query block (output
-        [rows, d] bf16 + per-head log-sum-exp fp32 + its q/k/v staging, each
-        rounded to the caching allocator's 2 MiB segments) with 64 MiB of
-        headroom. Measured use is reported per step (``pool_high_water``); an
-        undersized region fails loudly with torch's out-of-memory error."""
+        """Size of the arena's torch-scratch region for a first step at length
+        L: an upper bound on the attention call's temporaries for one query
+        block (output [rows, d] bf16 + per-head log-sum-exp fp32 + room for
+        q/k/v staging, each rounded to the caching allocator's 2 MiB segments)
+        with 64 MiB of headroom. After the step the region is cut to its
+        measured high-water mark (``_fit_scratch``); an undersized region fails
+        loudly with torch's out-of-memory error."""
         cfg = self.cfg
         qb = min(L, ATTN_BLOCK)
         mib2 = 2 << 20
@@ -216,6 +218,18 @@ class StepExecutor:
             self._pool = torch.cuda.MemPool(_scratch_allocator().allocator())
             self.ws.on_close(self.close)
 
+    def _fit_scratch(self) -> None:
+        """Shrink the scratch region to what the step actually used (the
+        caching allocator keeps those segments and reuses them every step)
+        plus 8 MiB, so the arena's commitment is plan + measured scratch."""
+        from . import _native
+
+        used = self.pool_stats()["high_water"]
+        want = -(-(used + (8 << 20)) // self.ws.page_size) * self.ws.page_size
+        if used and want < self.scratch_bytes:
+            _native.call("mosaic_pool_bind", self.ws.device, ctypes.c_void_p(self.ws.base), int(want))
+            self.scratch_bytes = want
+
     def close(self) -> None:
         """Release the scratch pool before the arena goes away (called by the
         workspace's close): cached segments are returned, the region forgotten."""
@@ -230,8 +244,14 @@ class StepExecutor:
         gc.collect()
         torch.cuda.empty_cache()
         if self.ws.base is not None:
+            live = self.pool_stats()["in_use"]
+            if live:  # a library kept a block of the step's scratch past the step: it dangles once unmapped
+                import warnings
+
+                warnings.warn(f"{live} bytes of the arena's torch-scratch region are still held at close")
             _native.call("mosaic_pool_unbind", self.ws.device, ctypes.c_void_p(self.ws.base))
         self.scratch_bytes = 0
+        self._fitted_L = None
 
     def pool_stats(self) -> dict:
         from . import _native
@@ -306,7 +326,7 @@ class StepExecutor:
         # the B200 path runs the whole step in the arena: torch-side temporaries in the
         # scratch region (MemPool), activations at their planned offsets after it. The
         # reference's materialising modes are the dense-logits baselines: torch allocator.
-        if fused:
+        if fused and not (self._pool is not None and self._fitted_L == L):
             self._ensure_scratch(self.scratch_bytes_for(L))
         if self.scratch_bytes + plan.workspace_size > self.ws.committed_bytes:
             self.ws.commit_to(self.scratch_bytes + plan.workspace_size)
@@ -335,6 +355,11 @@ class StepExecutor:
             self._run_ops(g, views, x, mask_idx, side, k_unmask, skip_layers, profile, marks, keep_dst, kept)
         end.record()
         end.synchronize()
+        peak_committed = self.ws.committed_bytes  # what this step ran with
+        if fused and self._fitted_L != L:  # first step at this length: cut the scratch region to
+            self._fit_scratch()             # its measured use and give the arena's tail back
+            self._fitted_L = L
+            self.ws.commit_to(self.scratch_bytes + plan.workspace_size)
         m_seen = int(side["m_dev"].item())  # K1's count; the step was planned for the binding M
         if m_seen != M:
             raise InputError(f"x holds {m_seen} masked positions but the step graph was instantiated for M={M} "
@@ -343,7 +368,8 @@ class StepExecutor:
         for kind, e0, e1 in marks:
             by_kind[kind] = by_kind.get(kind, 0.0) + e0.elapsed_time(e1)
         return {"ms": start.elapsed_time(end), "workspace_bytes": plan.workspace_size,
-                "committed_bytes": self.ws.committed_bytes, "scratch_bytes": self.scratch_bytes,
+                "committed_bytes": self.ws.committed_bytes, "step_committed_bytes": peak_committed,
+                "scratch_bytes": self.scratch_bytes,
                 "pool": self.pool_stats() if fused else None, "ops": len(g.ops), "kept": kept,
                 "ms_by_kind": by_kind}
 

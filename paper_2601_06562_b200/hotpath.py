@@ -517,8 +517,8 @@ class MaskOnlyHead:
         self._wplans: dict = {}
         self.die_table = (die_table_or_none(weight_shard.device)
                           if die_aware_default(die_aware, self.m_cap, self.v_shard) else None)
-        if not (exchange in ("nccl", "p2p") or hasattr(exchange, "push")):
-            raise InputError(f"exchange must be 'nccl', 'p2p' or a P2PExchange, got {exchange!r}")
+        if not (exchange in ("nccl", "p2p", "p2p_ipc") or hasattr(exchange, "push")):
+            raise InputError(f"exchange must be 'nccl', 'p2p', 'p2p_ipc' or a P2PExchange, got {exchange!r}")
         self.exchange = exchange
         self.world = 1
         if group is not None:
@@ -553,10 +553,13 @@ class MaskOnlyHead:
         if hasattr(exchange, "push"):  # a prepared P2PExchange (peer buffers set up by the caller)
             self.p2p = exchange
             self.world = exchange.world
-        elif group is not None and exchange == "p2p":
+        elif group is not None and exchange in ("p2p", "p2p_ipc"):
             from .shard import P2PExchange
 
-            self.p2p = P2PExchange(self.m_cap, group, weight_shard.device)
+            if exchange == "p2p":  # peers through torch symmetric memory (one GPU per rank)
+                self.p2p = P2PExchange(self.m_cap, group, weight_shard.device)
+            else:  # peers through CUDA IPC handles (ranks sharing a GPU)
+                self.p2p = P2PExchange.ipc(self.m_cap, group, weight_shard.device)
         if block is None:
             block = torch.empty(lay.size, dtype=torch.uint8, device=weight_shard.device)
         self.block = block

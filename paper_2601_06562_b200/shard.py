@@ -65,6 +65,33 @@ class P2PExchange:
         dist.barrier(group)  # every rank's pads are zero before anyone signals
 
     @classmethod
+    def ipc(cls, m_cap: int, group, device) -> "P2PExchange":
+        """The same exchange with the peer buffers mapped through CUDA IPC
+        handles traded over the process group (torch.multiprocessing's tensor
+        reductions) instead of symmetric memory -- for ranks that share one GPU
+        (symmetric memory refuses overlapping devices), e.g. the multi-rank
+        bench test on a one-GPU box. The data path (csrc/exchange.cu) is the
+        same peer-pointer stores and signal pads."""
+        from torch.multiprocessing.reductions import reduce_tensor
+
+        world, rank = dist.get_world_size(group), dist.get_rank(group)
+        gathered = torch.zeros((2, world, 3, int(m_cap)), dtype=torch.float32, device=device)
+        signal = torch.zeros((world,), dtype=torch.int32, device=device)
+        torch.cuda.synchronize(device)
+        handles = [None] * world
+        dist.all_gather_object(handles, (reduce_tensor(gathered), reduce_tensor(signal)), group=group)
+        keep, pg, ps = [], [], []
+        for r, (hg, hs) in enumerate(handles):
+            g, sg = (gathered, signal) if r == rank else (hg[0](*hg[1]), hs[0](*hs[1]))
+            keep += [g, sg]
+            pg.append(g.data_ptr())
+            ps.append(sg.data_ptr())
+        self = cls.from_buffers(gathered, signal, pg, ps, rank, world)
+        self._mapped = keep  # the peers' mappings live as long as the exchange
+        dist.barrier(group)
+        return self
+
+    @classmethod
     def from_buffers(cls, gathered: torch.Tensor, signal: torch.Tensor, peer_gathered: list, peer_signal: list,
                      rank: int, world: int) -> "P2PExchange":
         """Peers given as raw device pointers (e.g. CUDA-IPC mappings of the
