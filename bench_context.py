@@ -152,25 +152,29 @@ def main():
     cfg = llada_cfg(wbytes)
     free, _ = torch.cuda.mem_get_info()
     act_budget = free - RESERVE
+    ws = vmm.reserve(act_budget + (1 << 30), backend="cuda")
+    ex = StepExecutor(model, ws, MASK_ID, exec_layers=args.exec_layers)
+    # the arena holds the plan AND the torch-scratch region (attention temporaries): the
+    # planner's budget is what is left after the region a step at L >= 32k starts with
+    scratch = ex.scratch_bytes_for(1 << 22)
+    plan_budget = act_budget - scratch
     result = {"device_total_bytes": total, "weights_bytes": wbytes, "free_after_weights": free,
-              "reserve_bytes": RESERVE, "activation_budget": act_budget, "exec_layers": args.exec_layers,
-              "model": cfg.to_json_dict(), "code_hash": code_hash}
+              "reserve_bytes": RESERVE, "activation_budget": act_budget, "scratch_region_first_step": scratch,
+              "exec_layers": args.exec_layers, "model": cfg.to_json_dict(), "code_hash": code_hash}
     t0 = time.time()
     result["planned_lmax"] = {
-        "fused_chunking": workload.find_lmax(cfg, 0.5, act_budget + wbytes, logits_mode="fused",
+        "fused_chunking": workload.find_lmax(cfg, 0.5, plan_budget + wbytes, logits_mode="fused",
                                              peaks_monotone=False),
-        "fused_no_chunking": workload.find_lmax(cfg, 0.5, act_budget + wbytes, ("global_plan", "mask_only"),
+        "fused_no_chunking": workload.find_lmax(cfg, 0.5, plan_budget + wbytes, ("global_plan", "mask_only"),
                                                 logits_mode="fused", peaks_monotone=False),
-        "mask_only_chunking": workload.find_lmax(cfg, 0.5, act_budget + wbytes, logits_mode="mask_only",
+        "mask_only_chunking": workload.find_lmax(cfg, 0.5, plan_budget + wbytes, logits_mode="mask_only",
                                                  peaks_monotone=False),
-        "eager_global_plan": workload.find_lmax(cfg, 0.5, act_budget + wbytes, ("global_plan",),
+        "eager_global_plan": workload.find_lmax(cfg, 0.5, plan_budget + wbytes, ("global_plan",),
                                                 peaks_monotone=False),
         "seconds": time.time() - t0,
     }
     print(json.dumps(result["planned_lmax"]), flush=True)
 
-    ws = vmm.reserve(act_budget + (1 << 30), backend="cuda")
-    ex = StepExecutor(model, ws, MASK_ID, exec_layers=args.exec_layers)
     lengths = [int(s) for s in args.lengths.split(",") if s]
     lmax = result["planned_lmax"]["fused_chunking"]
     if not args.no_lmax_run:
@@ -183,8 +187,7 @@ def main():
     over = pipeline_probe(ex, cfg, int(lmax * 1.02) + 1, act_budget)  # just past the plan's limit
     result["pipeline"] = runs
     result["pipeline_past_lmax"] = over
-    ws.commit_to(0)
-    ws.close()
+    ws.close()  # the executor's scratch pool lets go of the arena first (Workspace.on_close)
     torch.cuda.empty_cache()
 
     # baseline: bisection on OOM

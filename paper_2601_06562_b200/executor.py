@@ -193,9 +193,9 @@ class StepExecutor:
     def scratch_bytes_for(self, L: int) -> int:
         """Size of the arena's torch-scratch region for a first step at length
         L: an upper bound on the attention call's temporaries for one query
-        block (output [rows, d] bf16 + per-head log-sum-exp fp32 + room for
-        q/k/v staging, each rounded to the caching allocator's 2 MiB segments)
-        with 64 MiB of headroom. After the step the region is cut to its
+        block (output [rows, d] bf16 + per-head log-sum-exp fp32, each rounded
+        to the caching allocator's 2 MiB segments, doubled for staging) with
+        32 MiB of headroom (measured use: one output block + 2 MiB). After the step the region is cut to its
         measured high-water mark (``_fit_scratch``); an undersized region fails
         loudly with torch's out-of-memory error."""
         cfg = self.cfg
@@ -203,7 +203,7 @@ class StepExecutor:
         mib2 = 2 << 20
         blk = -(-(qb * cfg.d_model * 2) // mib2) * mib2
         lse = -(-(cfg.n_heads * qb * 4) // mib2) * mib2
-        need = 4 * blk + 2 * lse + (64 << 20)
+        need = 2 * blk + 2 * lse + (32 << 20)
         return -(-need // self.ws.page_size) * self.ws.page_size
 
     def _ensure_scratch(self, need: int) -> None:
@@ -417,8 +417,9 @@ class StepExecutor:
             # temporary stays bounded ([ATTN_BLOCK, d]) at million-token contexts
             for q0 in range(0, L, ATTN_BLOCK):
                 q1 = min(q0 + ATTN_BLOCK, L)
-                o = F.scaled_dot_product_attention(qh[:, :, q0:q1], kh, vh, is_causal=False)
-                out[q0:q1].copy_(o.squeeze(0).transpose(0, 1))
+                # one expression: the block's output temporary is freed before the next block's
+                out[q0:q1].copy_(F.scaled_dot_product_attention(qh[:, :, q0:q1], kh, vh, is_causal=False)
+                                 .squeeze(0).transpose(0, 1))
         elif kind == "add":
             a, c = (v[key] for key in op.inputs)
             torch.add(a, c, out=v[op.outputs[0]])

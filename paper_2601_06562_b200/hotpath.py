@@ -155,8 +155,7 @@ def die_map(device=None) -> tuple[torch.Tensor, dict]:
             _native.call("mosaic_die_map", host, n_sm, _p(scratch), ctypes.byref(n0), ctypes.byref(amb), _s(None))
         table = torch.tensor(list(host), dtype=torch.uint8, device=dev)
         _DIE_MAPS[dev.index] = (table, {"n_sm": n_sm, "die0_sms": n0.value, "ambiguous": amb.value})
-        del scratch  # ~2x L2 of probe scratch: hand it back to the driver, not to torch's cache
-        torch.cuda.empty_cache()
+        del scratch  # ~2x L2 of probe scratch: back to torch's caching allocator for reuse
     return _DIE_MAPS[dev.index]
 
 
