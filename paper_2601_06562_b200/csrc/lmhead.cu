@@ -39,17 +39,11 @@ constexpr int kThreads = 192;    // warp0 TMA, warp1 MMA+TMEM, warps 2..5 epilog
 #ifndef MOSAIC_K3_AWARPS
 #define MOSAIC_K3_AWARPS 4  // measured: 4 >= 8 once the per-stage sync is CTA-scope
 #endif
-#ifndef MOSAIC_K3_GTMA_ROWS
-#define MOSAIC_K3_GTMA_ROWS 0  // gather mode: rows per CTA-stage fetched by TMA gather4 (rest by cp.async)
-#endif
 constexpr int kAWarps = MOSAIC_K3_AWARPS;  // cp.async gather path: A loader warps (warp 0 + warps 6..)
-// Optionally the first kTmaRows rows of each CTA's 128 go through TMA gather4
-// ops issued beside the B box, the rest through the loader warps' cp.async.
-// Measured slower for every split (0/16/32/48 rows: 13.8/15.1/17.7/21.3 ms,
-// profiles/r01_k3_gather_modes.txt), so 0 by default.
-constexpr int kTmaRows = MOSAIC_K3_GTMA_ROWS;
-constexpr int kRowsPerAWarp = (BM - kTmaRows) / kAWarps;  // 32
-static_assert(kTmaRows % 4 == 0 && kTmaRows + kRowsPerAWarp * kAWarps == BM, "gather rows must tile the block");
+// (A hybrid that fetched part of each block by TMA gather4 was measured slower
+// for every split, profiles/r01_k3_gather_modes.txt, and is gone.)
+constexpr int kRowsPerAWarp = BM / kAWarps;  // 32
+static_assert(kRowsPerAWarp * kAWarps == BM, "gather rows must tile the block");
 static_assert(kRowsPerAWarp % 4 == 0 && kRowsPerAWarp <= 32, "loader warp covers 4-row groups");
 constexpr int kThreadsCpAsync = kThreads + (kAWarps - 1) * 32;
 constexpr int kEpiWarps = 4;
@@ -376,13 +370,26 @@ __global__ void __launch_bounds__(threads_for(kGather, kSample), 1)
         __syncwarp();
       }
       if constexpr (kGather == kGatherCpAsync) {
-        // kAWarps loader warps, kRowsPerAWarp rows each after the first kTmaRows
-        // (warp 0 lane 0 also issues the B box and the gather4 ops of those
-        // rows). Lane copies 16-byte chunk (lane & 7) of rows (lane >> 3) + 4 i;
-        // the row sources are resolved once per unit and kept in registers.
+        // A rows of a pair tile whose 256 source rows are consecutive rows of H
+        // (a contiguous masked run: the reference schedule's step-0 suffix,
+        // semi-autoregressive blocks) come in one TMA box per CTA-stage, exactly
+        // the dense path's load; any other tile is gathered by the kAWarps
+        // loader warps with 16-byte cp.async (kRowsPerAWarp rows each, lane
+        // copies chunk (lane & 7) of rows (lane >> 3) + 4 i, swizzled in software
+        // to the 128-byte TMA layout). The choice is per unit and the same in
+        // both CTAs of the pair (it depends on the pair tile's rows only); idx
+        // ascends strictly, so first/last 255 apart means consecutive.
+        const int64_t pr0 = static_cast<int64_t>(mb) * C::ROWS;
+        bool contig = false;
+        int a_src = 0;
+        if (pr0 + C::ROWS <= M) {
+          const int p0 = __ldg(p.idx + pr0), p1 = __ldg(p.idx + pr0 + C::ROWS - 1);
+          contig = (p1 - p0 == C::ROWS - 1) && !(p.shift && p0 == 0);
+          a_src = p0 + static_cast<int>(rank) * BM - (p.shift ? 1 : 0);  // this CTA's first source row
+        }
         const int slot = warp == 0 ? 0 : warp - 5;
         const int chunk = lane & 7;
-        const int row0 = kTmaRows + slot * kRowsPerAWarp;  // this warp's first row in the CTA's block
+        const int row0 = slot * kRowsPerAWarp;  // this warp's first row in the CTA's block
         const int my_row = a_row + row0 + (lane % kRowsPerAWarp);
         int src = my_row < M ? __ldg(p.idx + my_row) : 0;  // rows past M read row 0, never stored
         if (p.shift) src = max(src - 1, 0);
@@ -390,20 +397,6 @@ __global__ void __launch_bounds__(threads_for(kGather, kSample), 1)
 #pragma unroll
         for (int i = 0; i < kRowsPerAWarp / 4; ++i)
           off[i] = static_cast<int64_t>(__shfl_sync(0xffffffffu, src, 4 * i + (lane >> 3))) * p.ld_h + chunk * 8;
-        int4 trow[kTmaRows / 4 > 0 ? kTmaRows / 4 : 1];
-        if (warp == 0 && lane == 0) {
-#pragma unroll
-          for (int i = 0; i < kTmaRows / 4; ++i) {
-            int v[4];
-#pragma unroll
-            for (int j = 0; j < 4; ++j) {
-              const int r = a_row + 4 * i + j;
-              v[j] = r < M ? __ldg(p.idx + r) : 0;
-              if (p.shift) v[j] = max(v[j] - 1, 0);
-            }
-            trow[i] = make_int4(v[0], v[1], v[2], v[3]);
-          }
-        }
         for (int t = t0; t < t1; ++t) {
           const int b_row_off = rank * C::B_ROWS;
           for (int kb = 0; kb < k_blocks; ++kb) {
@@ -411,22 +404,23 @@ __global__ void __launch_bounds__(threads_for(kGather, kSample), 1)
             int bc, br;
             w_box(p, t, kb, k_blocks, b_row_off, bc, br);
             if (warp == 0 && lane == 0) {
-              if (rank == 0) mbar_arrive_expect_tx(&full[stage], (C::B_BYTES + kTmaRows * BK * 2) * CG);
-              if constexpr (CG == 1)
+              if (rank == 0) mbar_arrive_expect_tx(&full[stage], (C::B_BYTES + (contig ? C::A_BYTES : 0)) * CG);
+              if constexpr (CG == 1) {
                 tma_load_2d(sB + stage * C::B_BYTES, &tmap_b, &full[stage], bc, br, pol_b);
-              else
+                if (contig) tma_load_2d(sA + stage * C::A_BYTES, &tmap_a, &full[stage], kb * BK, a_src, pol_a);
+              } else {
                 tma_load_2d_cg2(sB + stage * C::B_BYTES, &tmap_b, &full[stage], bc, br, pol_b);
-#pragma unroll
-              for (int i = 0; i < kTmaRows / 4; ++i)
-                tma_gather4<CG>(sA + stage * C::A_BYTES + i * 4 * (BK * 2), &tmap_a, &full[stage], kb * BK,
-                                trow[i], pol_a);
+                if (contig) tma_load_2d_cg2(sA + stage * C::A_BYTES, &tmap_a, &full[stage], kb * BK, a_src, pol_a);
+              }
             }
-            const uint32_t dst0 = smem_u32(sA + stage * C::A_BYTES);
-            const uint16_t* hk = p.h + static_cast<int64_t>(kb) * BK;
+            if (!contig) {
+              const uint32_t dst0 = smem_u32(sA + stage * C::A_BYTES);
+              const uint16_t* hk = p.h + static_cast<int64_t>(kb) * BK;
 #pragma unroll
-            for (int i = 0; i < kRowsPerAWarp / 4; ++i) {
-              const int r = row0 + 4 * i + (lane >> 3);  // row within the CTA's 128-row block
-              cp_async16(dst0 + r * (BK * 2) + ((chunk ^ (r & 7)) << 4), hk + off[i], pol_a);
+              for (int i = 0; i < kRowsPerAWarp / 4; ++i) {
+                const int r = row0 + 4 * i + (lane >> 3);  // row within the CTA's 128-row block
+                cp_async16(dst0 + r * (BK * 2) + ((chunk ^ (r & 7)) << 4), hk + off[i], pol_a);
+              }
             }
             // writer-side release of the slot issued kALag stages ago: this
             // thread's copies of it have landed (wait_group), its generic-proxy
@@ -819,7 +813,10 @@ int launch(const ASource& a, int64_t m_cap, const int32_t* m_dev, int64_t m_host
   const int cg = cta_group_for(m_cap);  // gather mode included: pairs measured faster since the
                                         // per-stage sync is CTA-scope only (r01_k3_gather_modes.txt)
   CUtensorMap ta, tb;
-  int st = gather ? encode_tma_bf16(&ta, a.base, a.rows, d, a.ld, 1, BK) : encode_tma_bf16(&ta, a.base, m_cap, d, a.ld, BM, BK);
+  static const int gmode = env_int("MOSAIC_K3_GATHER", kGatherCpAsync);  // 1 = TMA gather4 (measured slower)
+  // gather4 reads single rows of H; the cp.async path's contiguous-run tiles read 128-row boxes of H
+  int st = gather ? encode_tma_bf16(&ta, a.base, a.rows, d, a.ld, (gmode == kGatherTma4 && !kStore) ? 1 : BM, BK)
+                  : encode_tma_bf16(&ta, a.base, m_cap, d, a.ld, BM, BK);
   if (st) return st;
   // experiment: W handed over pre-tiled as [n_tiles][d/64][256][64] (each TMA box one contiguous 32 KB block)
   static const int w_blocked = env_int("MOSAIC_K3_WBLOCKED", 0);
@@ -849,7 +846,6 @@ int launch(const ASource& a, int64_t m_cap, const int32_t* m_dev, int64_t m_host
   if (gather) {
     p.h = a.base;
     p.ld_h = a.ld;
-    static const int gmode = env_int("MOSAIC_K3_GATHER", kGatherCpAsync);  // 1 = TMA gather4 (measured slower)
     if constexpr (kStore) {  // materialised logits straight from H at idx (the drop-in gather_gemm)
       st = cg == 2 ? launch_cg<2, true, kGatherCpAsync>(ta, tb, p, m_cap, s)
                    : launch_cg<1, true, kGatherCpAsync>(ta, tb, p, m_cap, s);

@@ -354,18 +354,37 @@ def test_nccl_exchange_path_world1(dev):
                                                   (4096, 256, 8192, 2000, "scattered", True),
                                                   (300, 512, 1000, 100, "suffix", False),      # M <= 128 -> cg1
                                                   (9000, 4096, 126464 // 8 + 5, 4500, "scattered", False),
-                                                  (20000, 3584, 19008, 10000, "suffix", True)])
+                                                  (20000, 3584, 19008, 10000, "suffix", True),
+                                                  (6000, 1024, 9000, 3000, "runs", False),
+                                                  (6000, 1024, 9000, 3000, "runs", True),
+                                                  (700, 256, 4096, 600, "prefix", True)])
 def test_lmhead_gather_mode_equals_gathered_buffer(dev, L, d, V, m, layout, shift):
-    """K3 with the A operand gathered from H (cp.async loader warps) must be
-    bit-identical to K2 (gather into Hc) followed by the dense-A K3: same
-    operands, same MMA order, same epilogue -- also under the die-aware
-    schedule."""
+    """K3 with the A operand gathered from H must be bit-identical to K2
+    (gather into Hc) followed by the dense-A K3: same operands, same MMA
+    order, same epilogue -- also under the die-aware schedule. Layouts cover
+    both A paths: pair tiles whose rows are one contiguous run of H (one TMA
+    box; "suffix", long "runs") and gathered tiles (cp.async; "scattered", run
+    boundaries, the shifted run starting at position 0 in "prefix", and the
+    ragged last tile)."""
     from paper_2601_06562_b200 import hotpath
 
     rng = np.random.default_rng(L + m)
     H = bf16_tensor(rng.standard_normal((L, d)), dev)
     W = bf16_tensor(rng.standard_normal((V, d)) * 0.03, dev)
-    pos = np.arange(L - m, L) if layout == "suffix" else np.sort(rng.choice(L, m, replace=False))
+    if layout == "suffix":
+        pos = np.arange(L - m, L)
+    elif layout == "prefix":
+        pos = np.arange(m)
+    elif layout == "runs":  # runs of 200-700 masked positions separated by gaps
+        runs, p0 = [], 0
+        while sum(len(r) for r in runs) < m:
+            p0 += int(rng.integers(1, 50))
+            n = int(rng.integers(200, 700))
+            runs.append(np.arange(p0, min(p0 + n, L)))
+            p0 += n
+        pos = np.concatenate(runs)[:m]
+    else:
+        pos = np.sort(rng.choice(L, m, replace=False))
     idx = torch.from_numpy(pos.astype(np.int32)).to(dev)
     cap = m + 37  # capacity larger than M: rows past M never stored
     idx_cap = torch.zeros(cap, dtype=torch.int32, device=dev)
