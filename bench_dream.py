@@ -8,7 +8,8 @@ rank shard.
 Model: Dream-7B shape (28 layers, d 3584, d_ff 18944, 28 heads, V 152064;
 BASELINE's vocab), random-init bf16 weights, ``shift_mode="in_place"`` (the
 masked position p reads hidden row max(p-1, 0)), ``fused_ffn=True`` (K10
-gate/up GEMM with the SwiGLU epilogue; down projection on cuBLAS). One denoising step at
+gate/up GEMM with the SwiGLU epilogue; K10 down GEMM with the residual
+epilogue, which also does the chunk write and the residual add). One denoising step at
 L = seq, r_p = 0.5 (M = L/2), k = M/64, run twice through the executor:
 
 * ``unchunked``: K = (1, 1);
@@ -57,7 +58,7 @@ def run(ex, tmpl, L, M, K, profile=True):
     assert int((xx == MASK_ID).sum()) == M - k
     hot = sum(r["ms_by_kind"].get(kd, 0.0) for kd in ("gather", "lmhead_stats", "sample", "commit"))
     ffn = sum(r["ms_by_kind"].get(kd, 0.0) for kd in ("ffn_gate_up", "ffn_up", "ffn_gate", "glu", "ffn_down",
-                                                       "chunk_write"))
+                                                       "ffn_down_res", "chunk_write", "identity"))
     return {"K": list(K), "step_ms": r["ms"], "workspace_bytes": plan.workspace_size,
             "committed_bytes": r["committed_bytes"], "hot_path_ms": hot, "ffn_ms": ffn,
             "ms_by_kind": {kk: round(v, 3) for kk, v in r["ms_by_kind"].items()}}

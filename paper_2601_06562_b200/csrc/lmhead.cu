@@ -209,27 +209,39 @@ __device__ __forceinline__ void cp_async16(uint32_t dst, const void* src, uint64
                : "memory");
 }
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
-__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
 
-// cp.async A path: a slot is released LAG stages after it is issued, so up to
-// LAG + 1 stages of each loader thread's copies stay in flight. LAG < STAGES
-// leaves the producer a free slot to issue into (no deadlock): 4 of 6 stages
-// on pairs, 2 of 4 on single CTAs.
+// cp.async A path: a gathered slot is released LAG stages after it is issued,
+// so up to LAG + 1 stages of each loader thread's copies stay in flight. LAG <
+// STAGES leaves the producer a free slot to issue into (no deadlock): 4 of 6
+// stages on pairs, 2 of 4 on single CTAs. Slots of contiguous-run tiles (TMA
+// A) carry no copies and are released as soon as they are issued, after the
+// pending gathered ones (each barrier sees its arrivals in stage order).
 template <int STAGES>
 constexpr int a_lag() { return STAGES - 2 < 4 ? STAGES - 2 : 4; }
 
-// Release the slot issued LAG stages before `stage`: wait until at most LAG of
-// this thread's copy groups are pending (so that slot's group has landed),
-// fence its generic-proxy writes to the async proxy, then arrive (release).
+// Release the oldest of `pend` pending slots (the one issued pend - 1 stages
+// before `stage`): wait until at most LAG of this thread's copy groups are in
+// flight -- that slot's group has landed --, fence its generic-proxy writes to
+// the async proxy (the writer-side fence of the PTX memory model), arrive
+// (release); the MMA issuer acquires the barrier before tcgen05.mma reads.
 template <int STAGES>
-__device__ __forceinline__ void a_release(uint64_t* afull, uint32_t stage) {
+__device__ __forceinline__ void a_release_oldest(uint64_t* afull, uint32_t stage, int pend) {
   constexpr int LAG = a_lag<STAGES>();
   static_assert(LAG >= 1 && LAG < STAGES, "bad lag");
   asm volatile("cp.async.wait_group %0;" ::"n"(LAG) : "memory");
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-  mbar_arrive(&afull[(stage + STAGES - LAG) % STAGES]);
+  mbar_arrive(&afull[(stage + STAGES - (pend - 1)) % STAGES]);
 }
 
+// Release every pending slot (oldest first); `next` is the next stage to issue.
+template <int STAGES>
+__device__ __forceinline__ void a_release_all(uint64_t* afull, uint32_t next, int& pend) {
+  if (pend == 0) return;
+  asm volatile("cp.async.wait_group 0;" ::: "memory");
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  for (int i = pend; i >= 1; --i) mbar_arrive(&afull[(next + STAGES - i) % STAGES]);
+  pend = 0;
+}
 
 template <int CG, bool kStoreLogits, int kGather = kGatherNone, bool kSample = false>
 __global__ void __launch_bounds__(threads_for(kGather, kSample), 1)
@@ -350,7 +362,7 @@ __global__ void __launch_bounds__(threads_for(kGather, kSample), 1)
     const uint64_t pol_a = (p.policy == 1 || p.policy == 3) ? policy_evict_last() : policy_evict_normal();
     const uint64_t pol_b = (p.policy == 2 || p.policy == 3) ? policy_evict_first() : policy_evict_normal();
     uint32_t stage = 0, phase = 0;
-    int64_t a_issued = 0;  // cp.async A path: stages issued by this thread
+    int a_pend = 0;  // cp.async A path: slots issued by this thread and not yet released
     for (int64_t u = u_first; u < units_here; u += u_stride) {
       int mb, s;
       unit_coords(p, m_blocks, u, mb, s);
@@ -397,6 +409,7 @@ __global__ void __launch_bounds__(threads_for(kGather, kSample), 1)
 #pragma unroll
         for (int i = 0; i < kRowsPerAWarp / 4; ++i)
           off[i] = static_cast<int64_t>(__shfl_sync(0xffffffffu, src, 4 * i + (lane >> 3))) * p.ld_h + chunk * 8;
+        if (contig) a_release_all<C::STAGES>(afull, stage, a_pend);  // gathered slots of earlier units first
         for (int t = t0; t < t1; ++t) {
           const int b_row_off = rank * C::B_ROWS;
           for (int kb = 0; kb < k_blocks; ++kb) {
@@ -428,8 +441,12 @@ __global__ void __launch_bounds__(threads_for(kGather, kSample), 1)
             // reads (fence.proxy.async by the writing thread), then a release
             // arrive that the MMA issuer acquires (PTX memory model: proxy
             // fence after the writes, before the synchronising release)
-            cp_async_commit();
-            if (++a_issued > a_lag<C::STAGES>()) a_release<C::STAGES>(afull, stage);
+            if (contig) {
+              mbar_arrive(&afull[stage]);  // nothing gathered into this slot
+            } else {
+              cp_async_commit();
+              if (++a_pend > a_lag<C::STAGES>()) a_release_oldest<C::STAGES>(afull, stage, a_pend--);
+            }
             if (++stage == C::STAGES) {
               stage = 0;
               phase ^= 1;
@@ -474,14 +491,7 @@ __global__ void __launch_bounds__(threads_for(kGather, kSample), 1)
       __syncwarp();
     }
     if constexpr (kGather == kGatherCpAsync) {
-      // drain: release the last min(issued, kALag) slots, oldest first
-      cp_async_wait_all();
-      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-      const int64_t pend = a_issued < a_lag<C::STAGES>() ? a_issued : a_lag<C::STAGES>();
-      for (int64_t i = pend; i >= 1; --i) {
-        const uint32_t st = static_cast<uint32_t>((stage + C::STAGES - i) % C::STAGES);
-        mbar_arrive(&afull[st]);
-      }
+      a_release_all<C::STAGES>(afull, stage, a_pend);  // drain: the last pending slots, oldest first
     }
   } else if (warp == 1) {
     // ------------------------------------------------------------ MMA issuer (pair leader)
