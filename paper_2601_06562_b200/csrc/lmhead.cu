@@ -224,6 +224,8 @@ constexpr int a_lag() { return STAGES - 2 < 4 ? STAGES - 2 : 4; }
 // flight -- that slot's group has landed --, fence its generic-proxy writes to
 // the async proxy (the writer-side fence of the PTX memory model), arrive
 // (release); the MMA issuer acquires the barrier before tcgen05.mma reads.
+// (One arrival per thread: electing one lane per warp after a __syncwarp was
+// measured slower, 17 vs 14 ms at LLaDA 32k scattered.)
 template <int STAGES>
 __device__ __forceinline__ void a_release_oldest(uint64_t* afull, uint32_t stage, int pend) {
   constexpr int LAG = a_lag<STAGES>();
@@ -241,6 +243,22 @@ __device__ __forceinline__ void a_release_all(uint64_t* afull, uint32_t next, in
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   for (int i = pend; i >= 1; --i) mbar_arrive(&afull[(next + STAGES - i) % STAGES]);
   pend = 0;
+}
+
+// Gather mode: the pair tile of row block `mb` (ROWS rows) reads one
+// contiguous run of H -- its source rows are consecutive (idx ascends
+// strictly, so first and last ROWS - 1 apart means consecutive; with the
+// shift, src = p - 1 stays consecutive unless the run starts at position 0) --
+// so its A operand is a plain TMA box. Evaluated identically by the producer,
+// the MMA issuer and the peer relay: every role agrees which slots carry
+// gathered rows (and so take part in the afull protocol).
+template <int ROWS>
+__device__ __forceinline__ bool contiguous_tile(const int32_t* idx, int shift, int64_t M, int mb, int* p0_out) {
+  const int64_t r0 = static_cast<int64_t>(mb) * ROWS;
+  if (r0 + ROWS > M) return false;
+  const int p0 = __ldg(idx + r0), p1 = __ldg(idx + r0 + ROWS - 1);
+  *p0_out = p0;
+  return p1 - p0 == ROWS - 1 && !(shift && p0 == 0);
 }
 
 template <int CG, bool kStoreLogits, int kGather = kGatherNone, bool kSample = false>
@@ -277,7 +295,7 @@ __global__ void __launch_bounds__(threads_for(kGather, kSample), 1)
     for (int i = 0; i < C::STAGES; ++i) {
       mbar_init(&full[i], 1);
       mbar_init(&empty[i], 1);
-      mbar_init(&afull[i], kAWarps * 32 + (CG == 2 && rank == 0 ? 1 : 0));
+      mbar_init(&afull[i], kAWarps * 32 + (CG == 2 && rank == 0 ? 1 : 0));  // one arrival per loader thread
     }
     for (int i = 0; i < NUM_ACC; ++i) {
       mbar_init(&tfull[i], 1);
@@ -391,13 +409,42 @@ __global__ void __launch_bounds__(threads_for(kGather, kSample), 1)
         // to the 128-byte TMA layout). The choice is per unit and the same in
         // both CTAs of the pair (it depends on the pair tile's rows only); idx
         // ascends strictly, so first/last 255 apart means consecutive.
-        const int64_t pr0 = static_cast<int64_t>(mb) * C::ROWS;
-        bool contig = false;
-        int a_src = 0;
-        if (pr0 + C::ROWS <= M) {
-          const int p0 = __ldg(p.idx + pr0), p1 = __ldg(p.idx + pr0 + C::ROWS - 1);
-          contig = (p1 - p0 == C::ROWS - 1) && !(p.shift && p0 == 0);
-          a_src = p0 + static_cast<int>(rank) * BM - (p.shift ? 1 : 0);  // this CTA's first source row
+        int p0 = 0;
+        const bool contig = contiguous_tile<C::ROWS>(p.idx, p.shift, M, mb, &p0);
+        const int a_src = p0 + static_cast<int>(rank) * BM - (p.shift ? 1 : 0);  // this CTA's first source row
+        if (contig) {
+          // the unit runs exactly like the dense path: warp 0 lane 0 issues A and
+          // B boxes, no afull traffic; the other loader warps skip its slots
+          // (the MMA issuer and the peer relay skip them in the afull protocol)
+          a_release_all<C::STAGES>(afull, stage, a_pend);  // gathered slots of earlier units first
+          const int n_st = (t1 - t0) * k_blocks;
+          if (warp == 0 && lane == 0) {
+            for (int t = t0; t < t1; ++t)
+              for (int kb = 0; kb < k_blocks; ++kb) {
+                mbar_wait(&empty[(stage + (t - t0) * k_blocks + kb) % C::STAGES],
+                          (phase ^ (((stage + (t - t0) * k_blocks + kb) / C::STAGES) & 1)) ^ 1);
+                const uint32_t st = (stage + (t - t0) * k_blocks + kb) % C::STAGES;
+                int bc, br;
+                w_box(p, t, kb, k_blocks, rank * C::B_ROWS, bc, br);
+                if (rank == 0) mbar_arrive_expect_tx(&full[st], C::STAGE_BYTES * CG);
+                if constexpr (CG == 1) {
+                  tma_load_2d(sB + st * C::B_BYTES, &tmap_b, &full[st], bc, br, pol_b);
+                  tma_load_2d(sA + st * C::A_BYTES, &tmap_a, &full[st], kb * BK, a_src, pol_a);
+                } else {
+                  tma_load_2d_cg2(sB + st * C::B_BYTES, &tmap_b, &full[st], bc, br, pol_b);
+                  tma_load_2d_cg2(sA + st * C::A_BYTES, &tmap_a, &full[st], kb * BK, a_src, pol_a);
+                }
+              }
+          }
+          // the other loader warps wait here (a hardware barrier, no polling) until
+          // warp 0 has issued the whole unit, i.e. waited on every slot's
+          // free-barrier in ring order: skipping ahead without it would let them
+          // poll a slot's barrier several phases early, where its 1-bit parity
+          // aliases
+          asm volatile("bar.sync 1, %0;" ::"n"(kAWarps * 32) : "memory");
+          phase ^= ((stage + n_st) / C::STAGES) & 1;
+          stage = (stage + n_st) % C::STAGES;
+          continue;
         }
         const int slot = warp == 0 ? 0 : warp - 5;
         const int chunk = lane & 7;
@@ -409,44 +456,29 @@ __global__ void __launch_bounds__(threads_for(kGather, kSample), 1)
 #pragma unroll
         for (int i = 0; i < kRowsPerAWarp / 4; ++i)
           off[i] = static_cast<int64_t>(__shfl_sync(0xffffffffu, src, 4 * i + (lane >> 3))) * p.ld_h + chunk * 8;
-        if (contig) a_release_all<C::STAGES>(afull, stage, a_pend);  // gathered slots of earlier units first
         for (int t = t0; t < t1; ++t) {
           const int b_row_off = rank * C::B_ROWS;
           for (int kb = 0; kb < k_blocks; ++kb) {
-            mbar_wait_sleep(&empty[stage], phase ^ 1, MOSAIC_K3_PROD_SLEEP_NS);
+            mbar_wait(&empty[stage], phase ^ 1);
             int bc, br;
             w_box(p, t, kb, k_blocks, b_row_off, bc, br);
             if (warp == 0 && lane == 0) {
-              if (rank == 0) mbar_arrive_expect_tx(&full[stage], (C::B_BYTES + (contig ? C::A_BYTES : 0)) * CG);
-              if constexpr (CG == 1) {
+              if (rank == 0) mbar_arrive_expect_tx(&full[stage], C::B_BYTES * CG);
+              if constexpr (CG == 1)
                 tma_load_2d(sB + stage * C::B_BYTES, &tmap_b, &full[stage], bc, br, pol_b);
-                if (contig) tma_load_2d(sA + stage * C::A_BYTES, &tmap_a, &full[stage], kb * BK, a_src, pol_a);
-              } else {
+              else
                 tma_load_2d_cg2(sB + stage * C::B_BYTES, &tmap_b, &full[stage], bc, br, pol_b);
-                if (contig) tma_load_2d_cg2(sA + stage * C::A_BYTES, &tmap_a, &full[stage], kb * BK, a_src, pol_a);
-              }
             }
-            if (!contig) {
-              const uint32_t dst0 = smem_u32(sA + stage * C::A_BYTES);
-              const uint16_t* hk = p.h + static_cast<int64_t>(kb) * BK;
+            const uint32_t dst0 = smem_u32(sA + stage * C::A_BYTES);
+            const uint16_t* hk = p.h + static_cast<int64_t>(kb) * BK;
 #pragma unroll
-              for (int i = 0; i < kRowsPerAWarp / 4; ++i) {
-                const int r = row0 + 4 * i + (lane >> 3);  // row within the CTA's 128-row block
-                cp_async16(dst0 + r * (BK * 2) + ((chunk ^ (r & 7)) << 4), hk + off[i], pol_a);
-              }
+            for (int i = 0; i < kRowsPerAWarp / 4; ++i) {
+              const int r = row0 + 4 * i + (lane >> 3);  // row within the CTA's 128-row block
+              cp_async16(dst0 + r * (BK * 2) + ((chunk ^ (r & 7)) << 4), hk + off[i], pol_a);
             }
-            // writer-side release of the slot issued kALag stages ago: this
-            // thread's copies of it have landed (wait_group), its generic-proxy
-            // smem writes are ordered before the tensor core's async-proxy
-            // reads (fence.proxy.async by the writing thread), then a release
-            // arrive that the MMA issuer acquires (PTX memory model: proxy
-            // fence after the writes, before the synchronising release)
-            if (contig) {
-              mbar_arrive(&afull[stage]);  // nothing gathered into this slot
-            } else {
-              cp_async_commit();
-              if (++a_pend > a_lag<C::STAGES>()) a_release_oldest<C::STAGES>(afull, stage, a_pend--);
-            }
+            // writer-side release of the slot issued LAG stages ago (a_release_oldest)
+            cp_async_commit();
+            if (++a_pend > a_lag<C::STAGES>()) a_release_oldest<C::STAGES>(afull, stage, a_pend--);
             if (++stage == C::STAGES) {
               stage = 0;
               phase ^= 1;
@@ -497,11 +529,14 @@ __global__ void __launch_bounds__(threads_for(kGather, kSample), 1)
     // ------------------------------------------------------------ MMA issuer (pair leader)
     if (lane == 0 && rank == 0) {
       uint32_t stage = 0, phase = 0, acc = 0, acc_phase = 0;
+      uint32_t abits = 0;  // gather mode: expected afull parity per slot (only gathered uses flip it)
       for (int64_t u = u_first; u < units_here; u += u_stride) {
         int mb, s;
         unit_coords(p, m_blocks, u, mb, s);
         const int t0 = s * p.tiles_per_split;
         const int t1 = min(t0 + p.tiles_per_split, p.n_tiles);
+        int p0_unused;
+        const bool gathered = kGather == kGatherCpAsync && !contiguous_tile<C::ROWS>(p.idx, p.shift, M, mb, &p0_unused);
         for (int t = t0; t < t1; ++t) {
           if constexpr (CG == 2) mbar_wait_cluster(&tempty[acc], acc_phase ^ 1);
           else mbar_wait(&tempty[acc], acc_phase ^ 1);
@@ -509,15 +544,15 @@ __global__ void __launch_bounds__(threads_for(kGather, kSample), 1)
           const uint32_t d_tmem = tmem_base + acc * BN;
           for (int kb = 0; kb < k_blocks; ++kb) {
             mbar_wait(&full[stage], phase);
-            if constexpr (kGather == kGatherCpAsync) {
-              // this CTA's rows landed (and, on a pair, the peer's: relayed below);
-              // the proxy fence orders this CTA's generic-proxy cp.async writes
-              // before the tensor core's async-proxy reads. Only CTA-scope
-              // operations on the per-stage path: cluster-scope fences and
-              // release.cluster arrives compile to MEMBAR.ALL.GPU, which
-              // serialised the pair ring at ~0.9 us per stage
-              // (profiles/r01_k3_gather_modes.txt).
-              mbar_wait(&afull[stage], phase);
+            if (gathered) {
+              // the gathered rows of this slot landed and were fenced to the
+              // async proxy by their writers (and, on a pair, the peer's rows:
+              // relayed below). Only CTA-scope operations on the per-stage path:
+              // cluster-scope fences and release.cluster arrives compile to
+              // MEMBAR.ALL.GPU, which serialised the pair ring at ~0.9 us per
+              // stage (profiles/r01_k3_gather_modes.txt).
+              mbar_wait(&afull[stage], (abits >> stage) & 1u);
+              abits ^= 1u << stage;
             }
             tc_fence_after();
             const uint32_t a0 = smem_u32(sA + stage * C::A_BYTES);
@@ -543,15 +578,23 @@ __global__ void __launch_bounds__(threads_for(kGather, kSample), 1)
     if constexpr (kGather == kGatherCpAsync && CG == 2) {
       // peer CTA of the pair: relay "A slot landed" to the leader's barrier
       if (lane == 0 && rank == 1) {
-        uint32_t stage = 0, phase = 0;
+        uint32_t stage = 0, phase = 0, abits = 0;
         for (int64_t u = u_first; u < units_here; u += u_stride) {
           int mb, s;
           unit_coords(p, m_blocks, u, mb, s);
           const int t0 = s * p.tiles_per_split;
           const int t1 = min(t0 + p.tiles_per_split, p.n_tiles);
+          int p0_unused;
+          if (contiguous_tile<C::ROWS>(p.idx, p.shift, M, mb, &p0_unused)) {  // no gathered slots to relay
+            const int n_st = (t1 - t0) * k_blocks;
+            phase ^= ((stage + n_st) / C::STAGES) & 1;
+            stage = (stage + n_st) % C::STAGES;
+            continue;
+          }
           for (int t = t0; t < t1; ++t)
             for (int kb = 0; kb < k_blocks; ++kb) {
-              mbar_wait(&afull[stage], phase);
+              mbar_wait(&afull[stage], (abits >> stage) & 1u);
+              abits ^= 1u << stage;
               // the peer's writers fenced their rows to the async proxy before
               // arriving; forward with a default-semantics remote arrive on the
               // leader's barrier: the form CUTLASS's cluster pipelines use for
