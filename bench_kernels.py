@@ -114,10 +114,14 @@ def main():
         ms_sep = timeit(lambda: (hotpath.gather_rows(H, idx, hc, m_host=M),
                                  hotpath.lmhead_stats(hc, W, S, pm, ps, pa, m_host=M, die_of_sm=die, sched=sched)),
                         iters=5)
+        ms_runs = timeit(lambda: (hotpath.gather_rows_scattered(H, idx, hc, M, m_host=M),
+                                  hotpath.lmhead_stats_runs(H, idx, hc, W, S, pm, ps, pa, M, m_host=M, die_of_sm=die,
+                                                            sched=sched)), iters=5)
         flops = 2.0 * M * d * V
         out[f"k3_gather_{name}"] = {"M": M, "d": d, "V": V, "splits": S, "ms": ms, "TFLOPs": flops / ms / 1e9,
                                     "frac_bf16_peak": flops / ms / 1e9 / tf, "k2_plus_k3_ms": ms_sep,
-                                    "schedule": "die-aware (both)", "hc_bytes_saved": M * d * 2}
+                                    "runs_k2_plus_k3_ms": ms_runs,
+                                    "schedule": "die-aware (all)", "hc_bytes_saved": M * d * 2}
         del H, W, hc
 
     # whole step: eager launches vs one captured CUDA graph (launch-bound at small sizes)

@@ -95,6 +95,16 @@ MOSAIC_API int mosaic_gather_rows(const uint16_t* H, int64_t n_rows, int64_t ld_
                        const int32_t* idx, const int32_t* m_dev, int64_t m_host,
                        int64_t m_cap, int32_t shift, uint16_t* Hc, void* stream);
 
+/* Runs mode of K2: as mosaic_gather_rows, but the rows of every full K3 tile
+ * (tile_rows consecutive compacted rows: 256 with cta_group::2, 128 with
+ * cta_group::1 -- mosaic_lmhead_config out[0] * out[2]) whose source rows are
+ * one contiguous run of H are skipped: mosaic_lmhead_stats_runs reads those
+ * tiles straight from H. Same indirect fetch it replaces (kernel.py:77).     */
+MOSAIC_API int mosaic_gather_rows_scattered(const uint16_t* H, int64_t n_rows, int64_t ld_h, int64_t d,
+                                 const int32_t* idx, const int32_t* m_dev, int64_t m_host,
+                                 int64_t m_cap, int32_t shift, int32_t tile_rows, uint16_t* Hc,
+                                 void* stream);
+
 /* ---------------------------------------------------------------- K3 ------
  * Mask-only LM head with the fused softmax-statistics epilogue.
  * For every row r < M of Hc [m_cap, d] and every vocab split s of the shard
@@ -152,6 +162,22 @@ MOSAIC_API int mosaic_lmhead_stats_gather_die(const uint16_t* H, int64_t n_rows,
                                    const uint16_t* W, int64_t V_shard, int64_t d, int64_t v_offset,
                                    int32_t n_splits, float* part_max, float* part_sum, int32_t* part_arg,
                                    const uint8_t* die_of_sm, uint32_t* sched_scratch, void* stream);
+
+/* Runs mode of K3 (the product default): per 256-row pair tile (128 with
+ * cta_group::1) the A operand is one TMA box of H itself when the tile's
+ * source rows src(idx[r]) are consecutive -- the reference schedule's step-0
+ * suffix, semi-autoregressive blocks -- and otherwise one TMA box of Hc, where
+ * mosaic_gather_rows_scattered compacted that tile's rows. Both A sources
+ * feed the dense TMA pipeline, so every tile runs at the dense rate and the
+ * gathered copy shrinks to the scattered tiles. Replaces gather_gemm
+ * (kernel.py:62-86) like mosaic_lmhead_stats, with identical outputs;
+ * die_of_sm / sched_scratch optional (null = default schedule).             */
+MOSAIC_API int mosaic_lmhead_stats_runs(const uint16_t* H, int64_t n_rows, int64_t ld_h, const int32_t* idx,
+                             int32_t shift, int64_t m_cap, const int32_t* m_dev, int64_t m_host,
+                             const uint16_t* Hc, const uint16_t* W, int64_t V_shard, int64_t d,
+                             int64_t v_offset, int32_t n_splits, float* part_max, float* part_sum,
+                             int32_t* part_arg, const uint8_t* die_of_sm, uint32_t* sched_scratch,
+                             void* stream);
 
 /* Sampling variant of K3 (temperature > 0; the reference's `sample` op is
  * memory-only, this follows LLaDA's generate): per masked row r the token is

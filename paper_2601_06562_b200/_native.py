@@ -31,6 +31,11 @@ SIGNATURES: dict[str, tuple[object, list[object]]] = {
         c_int,
         [c_void_p, c_int64, c_int64, c_int64, c_void_p, c_void_p, c_int64, c_int64, c_int32, c_void_p, c_void_p],
     ),
+    "mosaic_gather_rows_scattered": (
+        c_int,
+        [c_void_p, c_int64, c_int64, c_int64, c_void_p, c_void_p, c_int64, c_int64, c_int32, c_int32, c_void_p,
+         c_void_p],
+    ),
     "mosaic_lmhead_plan": (c_int, [c_int64, c_int64, c_int64, _i32p, _i32p]),
     "mosaic_lmhead_stats": (
         c_int,
@@ -53,6 +58,11 @@ SIGNATURES: dict[str, tuple[object, list[object]]] = {
         c_int,
         [c_void_p, c_int64, c_int64, c_void_p, c_int32, c_int64, c_void_p, c_int64, c_void_p, c_int64, c_int64,
          c_int64, c_int32, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p],
+    ),
+    "mosaic_lmhead_stats_runs": (
+        c_int,
+        [c_void_p, c_int64, c_int64, c_void_p, c_int32, c_int64, c_void_p, c_int64, c_void_p, c_void_p, c_int64,
+         c_int64, c_int64, c_int32, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p],
     ),
     "mosaic_remask_commit_segmented": (
         c_int,

@@ -122,7 +122,7 @@ __global__ void __launch_bounds__(256) k2_gather(const int4* __restrict__ H, int
                                                  int64_t ld_vec, int64_t d_vec,
                                                  const int32_t* __restrict__ idx,
                                                  const int32_t* __restrict__ m_dev, int64_t m_host,
-                                                 int64_t m_cap, int32_t shift,
+                                                 int64_t m_cap, int32_t shift, int32_t tile_rows,
                                                  int4* __restrict__ Hc) {
   pdl_wait();
   pdl_trigger();
@@ -131,8 +131,18 @@ __global__ void __launch_bounds__(256) k2_gather(const int4* __restrict__ H, int
   const int64_t warps = static_cast<int64_t>(gridDim.x) * (blockDim.x >> 5);
   for (int64_t r = static_cast<int64_t>(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5);
        r < M; r += warps) {
+    if (tile_rows > 0) {
+      // runs mode: rows of a full K3 tile whose source rows are one contiguous
+      // run of H are read by K3 straight from H (lmhead.cu contiguous_tile):
+      // only the other tiles' rows are compacted
+      const int64_t t0 = r - r % tile_rows;
+      if (t0 + tile_rows <= M) {
+        const int q0 = __ldg(idx + t0), q1 = __ldg(idx + t0 + tile_rows - 1);
+        if (q1 - q0 == tile_rows - 1 && !((shift & 1) && q0 == 0) && !(shift & 2)) continue;
+      }
+    }
     int64_t p = __ldg(idx + r);
-    if (shift) p = p > 0 ? p - 1 : 0;
+    if (shift & 1) p = p > 0 ? p - 1 : 0;
     if (p >= n_rows) p = n_rows - 1;  // validated on the host; clamp keeps the read in bounds
     const int4* src = H + p * ld_vec;
     int4* dst = Hc + r * d_vec;
@@ -207,9 +217,10 @@ extern "C" int mosaic_mask_compact(const int32_t* x, int64_t L, int32_t mask_id,
   return check_launch("mosaic_mask_compact");
 }
 
-extern "C" int mosaic_gather_rows(const uint16_t* H, int64_t n_rows, int64_t ld_h, int64_t d,
-                                  const int32_t* idx, const int32_t* m_dev, int64_t m_host,
-                                  int64_t m_cap, int32_t shift, uint16_t* Hc, void* stream) {
+namespace {
+int gather_rows_impl(const uint16_t* H, int64_t n_rows, int64_t ld_h, int64_t d, const int32_t* idx,
+                     const int32_t* m_dev, int64_t m_host, int64_t m_cap, int32_t shift, int32_t tile_rows,
+                     uint16_t* Hc, void* stream) {
   MOSAIC_REQUIRE(d > 0 && d % 8 == 0, "d=%lld must be a positive multiple of 8", (long long)d);
   MOSAIC_REQUIRE(ld_h >= d && ld_h % 8 == 0, "ld_h=%lld must be >= d and a multiple of 8",
                  (long long)ld_h);
@@ -224,6 +235,21 @@ extern "C" int mosaic_gather_rows(const uint16_t* H, int64_t n_rows, int64_t ld_
   const int grid = static_cast<int>(want < num_sms() * 16 ? want : num_sms() * 16);
   MOSAIC_CUDA(launch_pdl(k2_gather<4>, dim3(grid), dim3(256), 0, as_stream(stream),
                          reinterpret_cast<const int4*>(H), n_rows, ld_h / 8, d / 8, idx, m_dev, m_host, m_cap,
-                         shift, reinterpret_cast<int4*>(Hc)));
+                         shift, tile_rows, reinterpret_cast<int4*>(Hc)));
   return check_launch("mosaic_gather_rows");
+}
+}  // namespace
+
+extern "C" int mosaic_gather_rows(const uint16_t* H, int64_t n_rows, int64_t ld_h, int64_t d,
+                                  const int32_t* idx, const int32_t* m_dev, int64_t m_host,
+                                  int64_t m_cap, int32_t shift, uint16_t* Hc, void* stream) {
+  return gather_rows_impl(H, n_rows, ld_h, d, idx, m_dev, m_host, m_cap, shift, 0, Hc, stream);
+}
+
+extern "C" int mosaic_gather_rows_scattered(const uint16_t* H, int64_t n_rows, int64_t ld_h, int64_t d,
+                                            const int32_t* idx, const int32_t* m_dev, int64_t m_host,
+                                            int64_t m_cap, int32_t shift, int32_t tile_rows, uint16_t* Hc,
+                                            void* stream) {
+  MOSAIC_REQUIRE(tile_rows >= 1, "tile_rows=%d must be positive", tile_rows);
+  return gather_rows_impl(H, n_rows, ld_h, d, idx, m_dev, m_host, m_cap, shift, tile_rows, Hc, stream);
 }

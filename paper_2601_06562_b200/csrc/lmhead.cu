@@ -111,7 +111,8 @@ struct Params {
   const int32_t* idx;  // gather mode: masked positions, A rows are H[src(idx[r])]
   const uint16_t* h;   // gather mode: H base (cp.async path)
   int64_t ld_h;        // gather mode: H row stride (elements)
-  int32_t shift;       // gather mode: src(p) = max(p - 1, 0) (Dream token shift)
+  int32_t shift;       // gather/runs modes: bit 0 src(p) = max(p - 1, 0) (Dream token shift); bit 1 idx may
+                       // repeat rows (not strictly ascending): no tile is treated as a contiguous run
   int32_t w_blocked;   // W pre-tiled as [n_tiles][K/64][256][64] (each TMA box contiguous)
   // sampling variant (temperature > 0): token = argmax_v (x_v + T * g(pos, v)),
   // g Gumbel noise from a counter-based hash of (seed, position, vocab id)
@@ -202,7 +203,10 @@ __device__ __forceinline__ void tma_gather4(void* smem_dst, const void* tmap, ui
 // kGather selects the A path: 0 = dense TMA box of Hc, 1 = TMA gather4 from
 // H, 2 = cp.async 16-byte row segments from H issued by the whole producer
 // warp (swizzled in software to the 128-byte TMA layout).
-constexpr int kGatherNone = 0, kGatherTma4 = 1, kGatherCpAsync = 2;
+// 3 = runs: a pair tile whose source rows are one contiguous run of H loads A
+// as a TMA box of H (no copy); any other tile loads its box from Hc, where K2
+// (mosaic_gather_rows_scattered) compacted only the rows of such tiles.
+constexpr int kGatherNone = 0, kGatherTma4 = 1, kGatherCpAsync = 2, kGatherRuns = 3;
 
 __device__ __forceinline__ void cp_async16(uint32_t dst, const void* src, uint64_t policy) {
   asm volatile("cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %2;" ::"r"(dst), "l"(src), "l"(policy)
@@ -256,15 +260,16 @@ template <int ROWS>
 __device__ __forceinline__ bool contiguous_tile(const int32_t* idx, int shift, int64_t M, int mb, int* p0_out) {
   const int64_t r0 = static_cast<int64_t>(mb) * ROWS;
   if (r0 + ROWS > M) return false;
+  if (shift & 2) return false;  // caller's idx may repeat rows (batched windows with the shift)
   const int p0 = __ldg(idx + r0), p1 = __ldg(idx + r0 + ROWS - 1);
   *p0_out = p0;
-  return p1 - p0 == ROWS - 1 && !(shift && p0 == 0);
+  return p1 - p0 == ROWS - 1 && !((shift & 1) && p0 == 0);
 }
 
 template <int CG, bool kStoreLogits, int kGather = kGatherNone, bool kSample = false>
 __global__ void __launch_bounds__(threads_for(kGather, kSample), 1)
     k3_lmhead(const __grid_constant__ CUtensorMap tmap_a, const __grid_constant__ CUtensorMap tmap_b,
-              const Params p) {
+              const __grid_constant__ CUtensorMap tmap_h, const Params p) {
   using C = Cfg<CG>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
@@ -292,6 +297,7 @@ __global__ void __launch_bounds__(threads_for(kGather, kSample), 1)
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&tmap_a);
     tma_prefetch_desc(&tmap_b);
+    if constexpr (kGather == kGatherRuns) tma_prefetch_desc(&tmap_h);
     for (int i = 0; i < C::STAGES; ++i) {
       mbar_init(&full[i], 1);
       mbar_init(&empty[i], 1);
@@ -394,7 +400,7 @@ __global__ void __launch_bounds__(threads_for(kGather, kSample), 1)
         for (int j = 0; j < BM / 32; ++j) {
           const int r = a_row + j * 32 + lane;
           int v = r < M ? __ldg(p.idx + r) : 0;
-          if (p.shift) v = max(v - 1, 0);
+          if (p.shift & 1) v = max(v - 1, 0);
           sidx[j * 32 + lane] = v;
         }
         __syncwarp();
@@ -411,7 +417,7 @@ __global__ void __launch_bounds__(threads_for(kGather, kSample), 1)
         // ascends strictly, so first/last 255 apart means consecutive.
         int p0 = 0;
         const bool contig = contiguous_tile<C::ROWS>(p.idx, p.shift, M, mb, &p0);
-        const int a_src = p0 + static_cast<int>(rank) * BM - (p.shift ? 1 : 0);  // this CTA's first source row
+        const int a_src = p0 + static_cast<int>(rank) * BM - (p.shift & 1);  // this CTA's first source row
         if (contig) {
           // the unit runs exactly like the dense path: warp 0 lane 0 issues A and
           // B boxes, no afull traffic; the other loader warps skip its slots
@@ -451,7 +457,7 @@ __global__ void __launch_bounds__(threads_for(kGather, kSample), 1)
         const int row0 = slot * kRowsPerAWarp;  // this warp's first row in the CTA's block
         const int my_row = a_row + row0 + (lane % kRowsPerAWarp);
         int src = my_row < M ? __ldg(p.idx + my_row) : 0;  // rows past M read row 0, never stored
-        if (p.shift) src = max(src - 1, 0);
+        if (p.shift & 1) src = max(src - 1, 0);
         int64_t off[kRowsPerAWarp / 4];
 #pragma unroll
         for (int i = 0; i < kRowsPerAWarp / 4; ++i)
@@ -486,6 +492,16 @@ __global__ void __launch_bounds__(threads_for(kGather, kSample), 1)
           }
         }
       } else if (lane == 0) {
+        // runs mode: this unit's A box comes from H (contiguous run) or from Hc
+        const CUtensorMap* amap = &tmap_a;
+        int a_box_row = a_row;
+        if constexpr (kGather == kGatherRuns) {
+          int p0 = 0;
+          if (contiguous_tile<C::ROWS>(p.idx, p.shift, M, mb, &p0)) {
+            amap = &tmap_h;
+            a_box_row = p0 + static_cast<int>(rank) * BM - (p.shift & 1);
+          }
+        }
         for (int t = t0; t < t1; ++t) {
           const int b_row_off = rank * C::B_ROWS;
           for (int kb = 0; kb < k_blocks; ++kb) {
@@ -509,9 +525,9 @@ __global__ void __launch_bounds__(threads_for(kGather, kSample), 1)
                                 r4, pol_a);
               }
             } else if constexpr (CG == 1) {
-              tma_load_2d(sA + stage * C::A_BYTES, &tmap_a, &full[stage], kb * BK, a_row, pol_a);
+              tma_load_2d(sA + stage * C::A_BYTES, amap, &full[stage], kb * BK, a_box_row, pol_a);
             } else {
-              tma_load_2d_cg2(sA + stage * C::A_BYTES, &tmap_a, &full[stage], kb * BK, a_row, pol_a);
+              tma_load_2d_cg2(sA + stage * C::A_BYTES, amap, &full[stage], kb * BK, a_box_row, pol_a);
             }
             if (++stage == C::STAGES) {
               stage = 0;
@@ -809,8 +825,8 @@ void plan_splits(int64_t m_cap, int64_t V, int32_t* n_splits, int32_t* tps) {
 }
 
 template <int CG, bool kStore, int kGather, bool kSample = false>
-int launch_cg(const CUtensorMap& ta, const CUtensorMap& tb, const Params& p, int64_t m_cap,
-              cudaStream_t stream) {
+int launch_cg(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& th, const Params& p,
+              int64_t m_cap, cudaStream_t stream) {
   using C = Cfg<CG>;
   auto kern = k3_lmhead<CG, kStore, kGather, kSample>;
   static bool attr_set = false;  // per instantiation
@@ -836,7 +852,7 @@ int launch_cg(const CUtensorMap& ta, const CUtensorMap& tb, const Params& p, int
   attr[1].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
   cfg.attrs = attr;
   cfg.numAttrs = 2;
-  MOSAIC_CUDA(cudaLaunchKernelEx(&cfg, kern, ta, tb, p));
+  MOSAIC_CUDA(cudaLaunchKernelEx(&cfg, kern, ta, tb, th, p));
   return MOSAIC_OK;
 }
 
@@ -848,6 +864,7 @@ struct ASource {
   int64_t ld;
   const int32_t* idx;  // non-null = gather mode
   int32_t shift;
+  const uint16_t* hc = nullptr;  // runs mode: the [m_cap, d] buffer of the scattered tiles' rows (base = H)
 };
 
 template <bool kStore>
@@ -862,15 +879,25 @@ int launch(const ASource& a, int64_t m_cap, const int32_t* m_dev, int64_t m_host
                  "A rows and W must be 16-byte aligned");
   MOSAIC_REQUIRE(a.ld >= d && a.ld % 8 == 0, "row stride %lld must be >= d and a multiple of 8", (long long)a.ld);
   if (m_cap == 0) return MOSAIC_OK;
-  const bool gather = a.idx != nullptr;
+  const bool runs = a.hc != nullptr;
+  const bool gather = a.idx != nullptr && !runs;
+  MOSAIC_REQUIRE(!runs || (a.idx != nullptr && !kStore && p.part_y == nullptr), "runs mode: stats path only");
+  MOSAIC_REQUIRE(!runs || (reinterpret_cast<uintptr_t>(a.hc) & 15) == 0, "Hc must be 16-byte aligned");
   const int cg = cta_group_for(m_cap);  // gather mode included: pairs measured faster since the
                                         // per-stage sync is CTA-scope only (r01_k3_gather_modes.txt)
-  CUtensorMap ta, tb;
+  CUtensorMap ta, tb, th;
   static const int gmode = env_int("MOSAIC_K3_GATHER", kGatherCpAsync);  // 1 = TMA gather4 (measured slower)
   // gather4 reads single rows of H; the cp.async path's contiguous-run tiles read 128-row boxes of H
   int st = gather ? encode_tma_bf16(&ta, a.base, a.rows, d, a.ld, (gmode == kGatherTma4 && !kStore) ? 1 : BM, BK)
+           : runs ? encode_tma_bf16(&ta, a.hc, m_cap, d, d, BM, BK)
                   : encode_tma_bf16(&ta, a.base, m_cap, d, a.ld, BM, BK);
   if (st) return st;
+  if (runs) {
+    st = encode_tma_bf16(&th, a.base, a.rows, d, a.ld, BM, BK);  // H: contiguous-run tiles' boxes
+    if (st) return st;
+  } else {
+    th = ta;  // unused
+  }
   // experiment: W handed over pre-tiled as [n_tiles][d/64][256][64] (each TMA box one contiguous 32 KB block)
   static const int w_blocked = env_int("MOSAIC_K3_WBLOCKED", 0);
   p.w_blocked = w_blocked;
@@ -896,26 +923,29 @@ int launch(const ASource& a, int64_t m_cap, const int32_t* m_dev, int64_t m_host
     p.n_sm = num_sms();  // the die table holds one entry per SM (hotpath.die_map)
     MOSAIC_CUDA(cudaMemsetAsync(p.sched, 0, 16, s));
   }
-  if (gather) {
+  if (runs) {
+    st = cg == 2 ? launch_cg<2, false, kGatherRuns>(ta, tb, th, p, m_cap, s)
+                 : launch_cg<1, false, kGatherRuns>(ta, tb, th, p, m_cap, s);
+  } else if (gather) {
     p.h = a.base;
     p.ld_h = a.ld;
     if constexpr (kStore) {  // materialised logits straight from H at idx (the drop-in gather_gemm)
-      st = cg == 2 ? launch_cg<2, true, kGatherCpAsync>(ta, tb, p, m_cap, s)
-                   : launch_cg<1, true, kGatherCpAsync>(ta, tb, p, m_cap, s);
+      st = cg == 2 ? launch_cg<2, true, kGatherCpAsync>(ta, tb, th, p, m_cap, s)
+                   : launch_cg<1, true, kGatherCpAsync>(ta, tb, th, p, m_cap, s);
     } else if (gmode == kGatherTma4) {
-      st = cg == 2 ? launch_cg<2, false, kGatherTma4>(ta, tb, p, m_cap, s)
-                   : launch_cg<1, false, kGatherTma4>(ta, tb, p, m_cap, s);
+      st = cg == 2 ? launch_cg<2, false, kGatherTma4>(ta, tb, th, p, m_cap, s)
+                   : launch_cg<1, false, kGatherTma4>(ta, tb, th, p, m_cap, s);
     } else {
-      st = cg == 2 ? launch_cg<2, false, kGatherCpAsync>(ta, tb, p, m_cap, s)
-                   : launch_cg<1, false, kGatherCpAsync>(ta, tb, p, m_cap, s);
+      st = cg == 2 ? launch_cg<2, false, kGatherCpAsync>(ta, tb, th, p, m_cap, s)
+                   : launch_cg<1, false, kGatherCpAsync>(ta, tb, th, p, m_cap, s);
     }
   } else {
     if (p.part_y != nullptr) {  // sampling variant (buffered A only)
-      st = cg == 2 ? launch_cg<2, false, kGatherNone, true>(ta, tb, p, m_cap, s)
-                   : launch_cg<1, false, kGatherNone, true>(ta, tb, p, m_cap, s);
+      st = cg == 2 ? launch_cg<2, false, kGatherNone, true>(ta, tb, th, p, m_cap, s)
+                   : launch_cg<1, false, kGatherNone, true>(ta, tb, th, p, m_cap, s);
     } else {
-      st = cg == 2 ? launch_cg<2, kStore, kGatherNone>(ta, tb, p, m_cap, s)
-                   : launch_cg<1, kStore, kGatherNone>(ta, tb, p, m_cap, s);
+      st = cg == 2 ? launch_cg<2, kStore, kGatherNone>(ta, tb, th, p, m_cap, s)
+                   : launch_cg<1, kStore, kGatherNone>(ta, tb, th, p, m_cap, s);
     }
   }
   if (st) return st;
@@ -1031,7 +1061,7 @@ int lmhead_stats_gather_impl(const uint16_t* H, int64_t n_rows, int64_t ld_h, co
   p.part_arg = part_arg;
   p.die_of_sm = die_of_sm;
   p.sched = sched;
-  return launch<false>(ASource{H, n_rows, ld_h, idx, shift ? 1 : 0}, m_cap, m_dev, m_host, W, V_shard, d, p,
+  return launch<false>(ASource{H, n_rows, ld_h, idx, shift & 3}, m_cap, m_dev, m_host, W, V_shard, d, p,
                        stream);
 }
 }  // namespace
@@ -1056,6 +1086,34 @@ extern "C" int mosaic_lmhead_stats_gather_die(const uint16_t* H, int64_t n_rows,
                                   n_splits, part_max, part_sum, part_arg, die_of_sm, sched_scratch, stream);
 }
 
+extern "C" int mosaic_lmhead_stats_runs(const uint16_t* H, int64_t n_rows, int64_t ld_h, const int32_t* idx,
+                                        int32_t shift, int64_t m_cap, const int32_t* m_dev, int64_t m_host,
+                                        const uint16_t* Hc, const uint16_t* W, int64_t V_shard, int64_t d,
+                                        int64_t v_offset, int32_t n_splits, float* part_max, float* part_sum,
+                                        int32_t* part_arg, const uint8_t* die_of_sm, uint32_t* sched_scratch,
+                                        void* stream) {
+  MOSAIC_REQUIRE(H && idx && Hc && part_max && part_sum && part_arg, "null operands");
+  MOSAIC_REQUIRE(n_rows >= 1 && n_rows < (int64_t(1) << 31), "n_rows out of range");
+  MOSAIC_REQUIRE(die_of_sm == nullptr || sched_scratch != nullptr, "die-aware schedule needs its 16-byte scratch");
+  const int64_t n_tiles = ceil_div(V_shard, BN);
+  MOSAIC_REQUIRE(n_splits >= 1 && n_splits <= n_tiles, "n_splits=%d not in [1, %lld]", n_splits,
+                 (long long)n_tiles);
+  Params p{};
+  p.tiles_per_split = static_cast<int32_t>(ceil_div(n_tiles, n_splits));
+  p.n_splits = static_cast<int32_t>(ceil_div(n_tiles, p.tiles_per_split));
+  MOSAIC_REQUIRE(p.n_splits == n_splits, "n_splits=%d does not tile %lld vocab tiles evenly; use mosaic_lmhead_plan",
+                 n_splits, (long long)n_tiles);
+  p.v_offset = v_offset;
+  p.part_max = part_max;
+  p.part_sum = part_sum;
+  p.part_arg = part_arg;
+  p.die_of_sm = die_of_sm;
+  p.sched = sched_scratch;
+  ASource a{H, n_rows, ld_h, idx, shift & 3};
+  a.hc = Hc;
+  return launch<false>(a, m_cap, m_dev, m_host, W, V_shard, d, p, stream);
+}
+
 extern "C" int mosaic_lmhead_logits_gather(const uint16_t* H, int64_t n_rows, int64_t ld_h, const int32_t* idx,
                                            int32_t shift, int64_t m_cap, const int32_t* m_dev, int64_t m_host,
                                            const uint16_t* W, int64_t V_shard, int64_t d, float* out, int64_t ldo,
@@ -1068,7 +1126,7 @@ extern "C" int mosaic_lmhead_logits_gather(const uint16_t* H, int64_t n_rows, in
   p.n_splits = 1;
   p.out = out;
   p.ldo = ldo;
-  return launch<true>(ASource{H, n_rows, ld_h, idx, shift ? 1 : 0}, m_cap, m_dev, m_host, W, V_shard, d, p, stream);
+  return launch<true>(ASource{H, n_rows, ld_h, idx, shift & 3}, m_cap, m_dev, m_host, W, V_shard, d, p, stream);
 }
 
 extern "C" int mosaic_lmhead_config(int64_t m_cap, int32_t gather, int64_t* out) {

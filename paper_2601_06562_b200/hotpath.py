@@ -217,11 +217,13 @@ def lmhead_stats(hc: torch.Tensor, weight: torch.Tensor, n_splits: int, part_max
 def lmhead_stats_gather(hidden: torch.Tensor, idx: torch.Tensor, weight: torch.Tensor, n_splits: int,
                         part_max: torch.Tensor, part_sum: torch.Tensor, part_arg: torch.Tensor, m_cap: int,
                         m_dev=None, m_host: int = 0, shift: bool = False, v_offset: int = 0, stream=None,
-                        die_of_sm: Optional[torch.Tensor] = None, sched: Optional[torch.Tensor] = None) -> None:
+                        die_of_sm: Optional[torch.Tensor] = None, sched: Optional[torch.Tensor] = None,
+                        repeats: bool = False) -> None:
     """K3 in gather mode: the A rows come straight from ``hidden`` [n, d] at
     the masked positions ``idx`` (cp.async loader warps), no compacted
     buffer; ``die_of_sm``/``sched`` select the die-aware schedule as in
-    :func:`lmhead_stats`."""
+    :func:`lmhead_stats`. ``repeats``: ``idx`` may repeat a row (not strictly
+    ascending), so no tile may be taken for a contiguous run."""
     if hidden.dtype != torch.bfloat16 or hidden.dim() != 2 or hidden.stride(1) != 1 or not hidden.is_cuda:
         raise InputError("hidden must be a 2-D bf16 CUDA tensor with contiguous rows")
     _req(idx, torch.int32, "idx", 1)
@@ -240,13 +242,74 @@ def lmhead_stats_gather(hidden: torch.Tensor, idx: torch.Tensor, weight: torch.T
         if sched is None or sched.numel() * sched.element_size() < 16:
             raise InputError("the die-aware schedule needs a 16-byte sched scratch")
         _native.call("mosaic_lmhead_stats_gather_die", _p(hidden), hidden.shape[0], hidden.stride(0), _p(idx),
-                     int(bool(shift)), int(m_cap), _p(m_dev), int(m_host), _p(weight), weight.shape[0], d,
+                     _shift_flags(shift, repeats), int(m_cap), _p(m_dev), int(m_host), _p(weight), weight.shape[0], d,
                      int(v_offset), int(n_splits), _p(part_max), _p(part_sum), _p(part_arg), _p(die_of_sm),
                      _p(sched), _s(stream))
         return
     _native.call("mosaic_lmhead_stats_gather", _p(hidden), hidden.shape[0], hidden.stride(0), _p(idx),
-                 int(bool(shift)), int(m_cap), _p(m_dev), int(m_host), _p(weight), weight.shape[0], d,
+                 _shift_flags(shift, repeats), int(m_cap), _p(m_dev), int(m_host), _p(weight), weight.shape[0], d,
                  int(v_offset), int(n_splits), _p(part_max), _p(part_sum), _p(part_arg), _s(stream))
+
+
+def _shift_flags(shift: bool, repeats: bool) -> int:
+    """The gather/runs entry points' shift word: bit 0 Dream's token shift,
+    bit 1 ``idx`` may repeat rows (no contiguous-run tiles)."""
+    return int(bool(shift)) | (2 if repeats else 0)
+
+
+def lmhead_tile_rows(m_cap: int) -> int:
+    """Rows of one K3 tile at this capacity (256 on a CTA pair, 128 on one CTA):
+    the unit runs mode classifies as contiguous or scattered."""
+    c = lmhead_config(m_cap)
+    return int(c["cta_group"]) * int(c["a_rows"])
+
+
+def gather_rows_scattered(hidden: torch.Tensor, idx: torch.Tensor, hc: torch.Tensor, m_cap: int, m_dev=None,
+                          m_host: int = 0, shift: bool = False, repeats: bool = False, stream=None) -> None:
+    """K2 in runs mode: compact into ``hc`` only the rows of K3 tiles (of
+    :func:`lmhead_tile_rows` rows at this ``m_cap``) whose source rows are not
+    one contiguous run of ``hidden``."""
+    if hidden.dtype != torch.bfloat16 or hidden.dim() != 2 or hidden.stride(1) != 1 or not hidden.is_cuda:
+        raise InputError("hidden must be a 2-D bf16 CUDA tensor with contiguous rows")
+    _req(idx, torch.int32, "idx", 1)
+    _req(hc, torch.bfloat16, "hc", 2)
+    if hc.shape[1] != hidden.shape[1] or hc.shape[0] < m_cap:
+        raise InputError(f"hc {tuple(hc.shape)} does not hold {m_cap} rows of width {hidden.shape[1]}")
+    _native.call("mosaic_gather_rows_scattered", _p(hidden), hidden.shape[0], hidden.stride(0), hidden.shape[1],
+                 _p(idx), _p(m_dev), int(m_host), int(m_cap), _shift_flags(shift, repeats), lmhead_tile_rows(m_cap),
+                 _p(hc), _s(stream))
+
+
+def lmhead_stats_runs(hidden: torch.Tensor, idx: torch.Tensor, hc: torch.Tensor, weight: torch.Tensor,
+                      n_splits: int, part_max: torch.Tensor, part_sum: torch.Tensor, part_arg: torch.Tensor,
+                      m_cap: int, m_dev=None, m_host: int = 0, shift: bool = False, v_offset: int = 0, stream=None,
+                      die_of_sm: Optional[torch.Tensor] = None, sched: Optional[torch.Tensor] = None,
+                      repeats: bool = False) -> None:
+    """K3 in runs mode (the product default): each tile's A box comes by TMA
+    from ``hidden`` (its source rows are one contiguous run) or from ``hc``,
+    where :func:`gather_rows_scattered` compacted the other tiles' rows (call
+    it first). Outputs identical to gather_rows + lmhead_stats."""
+    if hidden.dtype != torch.bfloat16 or hidden.dim() != 2 or hidden.stride(1) != 1 or not hidden.is_cuda:
+        raise InputError("hidden must be a 2-D bf16 CUDA tensor with contiguous rows")
+    _req(idx, torch.int32, "idx", 1)
+    _req(hc, torch.bfloat16, "hc", 2)
+    _req(weight, torch.bfloat16, "weight", 2)
+    d = hidden.shape[1]
+    if weight.shape[1] != d or hc.shape[1] != d or hc.shape[0] < m_cap:
+        raise InputError(f"weight {tuple(weight.shape)} / hc {tuple(hc.shape)} do not match [*, {d}] x {m_cap}")
+    if idx.numel() < (m_cap if m_dev is not None else min(int(m_host), m_cap)):
+        raise InputError("idx must cover the masked rows (m_cap entries with a device count)")
+    for t, dt, n in ((part_max, torch.float32, "part_max"), (part_sum, torch.float32, "part_sum"),
+                     (part_arg, torch.int32, "part_arg")):
+        _req(t, dt, n)
+        if t.numel() < n_splits * m_cap:
+            raise InputError(f"{n} must hold n_splits*m_cap entries")
+    if die_of_sm is not None and (sched is None or sched.numel() * sched.element_size() < 16):
+        raise InputError("the die-aware schedule needs a 16-byte sched scratch")
+    _native.call("mosaic_lmhead_stats_runs", _p(hidden), hidden.shape[0], hidden.stride(0), _p(idx),
+                 _shift_flags(shift, repeats), int(m_cap), _p(m_dev), int(m_host), _p(hc), _p(weight), weight.shape[0], d,
+                 int(v_offset), int(n_splits), _p(part_max), _p(part_sum), _p(part_arg), _p(die_of_sm), _p(sched),
+                 _s(stream))
 
 
 def lmhead_logits(hc: torch.Tensor, weight: torch.Tensor, out: torch.Tensor, m_dev=None,
@@ -503,6 +566,9 @@ class MaskOnlyHead:
         self.shift = bool(shift)
         self.group = group
         self.fused_gather = bool(fused_gather)  # K3 reads rows of `hidden` directly: no K2, no hc buffer
+        # otherwise runs mode: K3 reads contiguous-run tiles from `hidden`, K2 compacts only the other
+        # tiles' rows into hc (MOSAIC_A_RUNS=0: every row through K2, the round-1 buffered path)
+        self.a_runs = not self.fused_gather and temperature == 0 and os.environ.get("MOSAIC_A_RUNS", "1") != "0"
         # temperature > 0: Gumbel-max sampling in K3's epilogue (LLaDA generate's sampler), one fresh
         # noise draw per step from (seed, step counter); single-process, buffered A path
         self.temperature = float(temperature)
@@ -609,7 +675,9 @@ class MaskOnlyHead:
                 rows = self._rows[:m]
                 _native.call("mosaic_window_rows", _p(q), _p(b["m_dev"]), 0, m, Wn, Ls, lo, int(self.shift),
                              _p(rows), _s(stream))
-            self._stats(hidden.view(B * Ls, self.d), rows, False, m, S, die, stream, keys=q)
+            # with the shift and lo = 0, src(0) = src(1): the rows repeat, so no tile is a contiguous run
+            self._stats(hidden.view(B * Ls, self.d), rows, False, m, S, die, stream, keys=q,
+                        repeats=self.shift and lo == 0)
             kt = k if isinstance(k, torch.Tensor) else None
             remask_commit_segmented(b["conf"], q, b["token"], xs.view(-1), m, Wn, B,
                                     k=0 if kt is not None else int(k), k_per_seg=kt, m_dev=b["m_dev"],
@@ -665,7 +733,7 @@ class MaskOnlyHead:
         return self._wplans[m_w]
 
     def _stats(self, hidden: torch.Tensor, rows: torch.Tensor, shift: bool, m: int, S: int, die, stream,
-               keys: Optional[torch.Tensor] = None) -> None:
+               keys: Optional[torch.Tensor] = None, repeats: bool = False) -> None:
         """K2 + K3 (or gather-mode K3) over the hidden rows ``rows[r]`` (src(p)
         = p - 1 with ``shift``) of the M compacted rows, then K4 -- through the
         vocab-shard exchange when the head is sharded -- into token/lse/conf.
@@ -680,7 +748,8 @@ class MaskOnlyHead:
         m_dev = b["m_dev"]
         if self.fused_gather:
             lmhead_stats_gather(hidden, rows, self.weight, S, pmax, psum, parg, m, m_dev=m_dev, shift=shift,
-                                v_offset=self.vocab_offset, stream=stream, die_of_sm=die, sched=b["sched"])
+                                v_offset=self.vocab_offset, stream=stream, die_of_sm=die, sched=b["sched"],
+                                repeats=repeats)
         elif self.temperature > 0:  # Gumbel-max sampling in K3's epilogue, noise keyed by keys[r]
             hc = b["hc"][:m]
             gather_rows(hidden, rows, hc, m_dev=m_dev, shift=shift, stream=stream)
@@ -695,6 +764,12 @@ class MaskOnlyHead:
             sample_merge(pm2, ps2, pa2, py, px, S2, m, m, b["token"], b["conf"], lse=b["lse"], m_dev=m_dev,
                          stream=stream)
             return
+        elif self.a_runs:
+            gather_rows_scattered(hidden, rows, b["hc"][:m], m, m_dev=m_dev, shift=shift, repeats=repeats,
+                                  stream=stream)
+            lmhead_stats_runs(hidden, rows, b["hc"][:m], self.weight, S, pmax, psum, parg, m, m_dev=m_dev,
+                              shift=shift, v_offset=self.vocab_offset, stream=stream, die_of_sm=die,
+                              sched=b["sched"], repeats=repeats)
         else:
             hc = b["hc"][:m]
             gather_rows(hidden, rows, hc, m_dev=m_dev, shift=shift, stream=stream)

@@ -393,7 +393,7 @@ def test_lmhead_gather_mode_equals_gathered_buffer(dev, L, d, V, m, layout, shif
     S, _ = hotpath.lmhead_plan(cap, V, d)
     outs = []
     table, _ = hotpath.die_map(dev)
-    for mode in ("buffer", "gather", "gather_die"):
+    for mode in ("buffer", "gather", "gather_die", "runs", "runs_die"):
         pm = torch.full((S, cap), 7.0, device=dev)
         ps = torch.full((S, cap), 7.0, device=dev)
         pa = torch.full((S, cap), -5, dtype=torch.int32, device=dev)
@@ -403,6 +403,23 @@ def test_lmhead_gather_mode_equals_gathered_buffer(dev, L, d, V, m, layout, shif
             hotpath.lmhead_stats(hc, W, S, pm, ps, pa, m_dev=m_dev, v_offset=11)
         elif mode == "gather":
             hotpath.lmhead_stats_gather(H, idx_cap, W, S, pm, ps, pa, cap, m_dev=m_dev, shift=shift, v_offset=11)
+        elif mode.startswith("runs"):  # K2 compacts only scattered tiles; run tiles read H by TMA
+            hc = torch.full((cap, d), float("nan"), dtype=torch.bfloat16, device=dev)
+            die = dict(die_of_sm=table, sched=torch.zeros(4, dtype=torch.int32, device=dev)) if mode == "runs_die" else {}
+            hotpath.gather_rows_scattered(H, idx_cap, hc, cap, m_dev=m_dev, shift=shift)
+            hotpath.lmhead_stats_runs(H, idx_cap, hc, W, S, pm, ps, pa, cap, m_dev=m_dev, shift=shift, v_offset=11,
+                                      **die)
+            # the buffer holds exactly the scattered tiles' rows (NaN elsewhere: never read by K3)
+            T = hotpath.lmhead_tile_rows(cap)
+            src = np.maximum(pos - 1, 0) if shift else pos
+            for t0 in range(0, m, T):
+                p = pos[t0:t0 + T]
+                run = p.size == T and p[-1] - p[0] == T - 1 and not (shift and p[0] == 0)
+                got = hc[t0:t0 + p.size]
+                if run:
+                    assert torch.isnan(got.float()).all()
+                else:
+                    assert torch.equal(got, H[torch.from_numpy(src[t0:t0 + T]).to(dev).long()])
         else:
             sched = torch.zeros(4, dtype=torch.int32, device=dev)
             hotpath.lmhead_stats_gather(H, idx_cap, W, S, pm, ps, pa, cap, m_dev=m_dev, shift=shift, v_offset=11,
@@ -440,17 +457,21 @@ def test_mask_only_head_fused_gather_equals_buffered(dev, shift):
     x[rng.random(L) < 0.6] = mask_id
     H = bf16_tensor(rng.standard_normal((L, d)), dev)
     W = bf16_tensor(rng.standard_normal((V, d)) * 0.04, dev)
+    x[1000:1700] = mask_id  # a long run: contiguous-run tiles in the runs-mode head
     outs = []
-    for fg in (False, True):
-        head = MaskOnlyHead(W, seq_len=L, mask_id=mask_id, shift=shift, fused_gather=fg)
+    for mode in ("buffered", "runs", "gather"):
+        head = MaskOnlyHead(W, seq_len=L, mask_id=mask_id, shift=shift, fused_gather=mode == "gather")
+        assert head.a_runs == (mode != "gather")  # runs mode is the default A path
+        head.a_runs = mode == "runs"  # buffered: every row through K2 (MOSAIC_A_RUNS=0)
         xd = torch.from_numpy(x).to(dev)
         o = head.step(xd, H, k)
         torch.cuda.synchronize()
         M = int(o.m_dev.item())
         outs.append((xd.cpu(), o.token[:M].cpu(), o.lse[:M].cpu(), o.conf[:M].cpu(), head.workspace_bytes))
-    for a, b in zip(outs[0][:4], outs[1][:4]):
-        assert torch.equal(a, b)
-    assert outs[1][4] < outs[0][4] - L * d  # the [m_cap, d] buffer is gone
+    for other in outs[1:]:
+        for a, b in zip(outs[0][:4], other[:4]):
+            assert torch.equal(a, b)
+    assert outs[2][4] < outs[0][4] - L * d  # gather mode: the [m_cap, d] buffer is gone
 
 
 # ----------------------------------------------------------------------- full BASELINE sizes
@@ -517,9 +538,11 @@ def test_full_size_k3_variants_bit_identical(dev, name, L, d, V, shift, k):
     x0 = torch.randint(0, V - 1, (L,), generator=g, device=dev, dtype=torch.int32)
     x0[torch.randperm(L, generator=g, device=dev)[: L // 2]] = mask_id
     outs = []
-    for gather in (False, True):
+    for gather in (False, True, "buffered"):
         for die in (False, True):
-            head = MaskOnlyHead(W, seq_len=L, mask_id=mask_id, shift=shift, fused_gather=gather, die_aware=die)
+            head = MaskOnlyHead(W, seq_len=L, mask_id=mask_id, shift=shift, fused_gather=gather is True,
+                                die_aware=die)
+            head.a_runs = gather is False  # runs mode (default), gather mode, every row through K2
             x = x0.clone()
             o = head.step(x, H, k)
             torch.cuda.synchronize()
@@ -769,6 +792,42 @@ def test_step_batch_vs_oracle(dev, B, Ls, d, V, window, shift, gather, per_seq_k
         assert np.array_equal(sel[rows], orc.remask_select(conf[rows], p, int(ks[bi])))
         assert int(sel[rows].sum()) == min(int(ks[bi]), p.size)
         assert np.array_equal(xo[bi, p[sel[rows]]], tok[rows][sel[rows]])
+
+
+@pytest.mark.parametrize("mode", ["runs", "gather"])
+def test_step_batch_shift_repeated_rows(dev, mode):
+    """step_batch with the shift and lo = 0 maps positions 0 and 1 to the same
+    hidden row, so the row list is not strictly ascending: a tile of rows
+    0,0,1,...,253,255 spans 255 like a contiguous run but is not one. The
+    run-detecting A paths must treat it as scattered -- bit-identical to the
+    buffered head."""
+    from paper_2601_06562_b200 import MaskOnlyHead
+
+    rng = np.random.default_rng(77)
+    B, Ls, d, V = 3, 1024, 512, 8192
+    mask_id = V - 1
+    x = rng.integers(0, V - 1, size=(B, Ls)).astype(np.int32)
+    x[:, :255] = mask_id  # positions 0..254 masked, 255 not, 256.. masked: src = 0,0,1,..,253,255,...
+    x[:, 256:700] = mask_id
+    H = bf16_tensor(rng.standard_normal((B * Ls, d)), dev).view(B, Ls, d)
+    W = bf16_tensor(rng.standard_normal((V, d)) * 0.03, dev)
+    outs = []
+    for m in ("buffered", mode):
+        head = MaskOnlyHead(W, seq_len=B * Ls, mask_id=mask_id, shift=True, fused_gather=m == "gather")
+        head.a_runs = m == "runs"
+        xd = torch.from_numpy(x).to(dev)
+        o = head.step_batch(xd, H, 40)
+        torch.cuda.synchronize()
+        M = int(o.m_dev.item())
+        outs.append((xd.cpu(), o.token[:M].cpu(), o.lse[:M].cpu(), o.conf[:M].cpu()))
+    for a, b in zip(*outs):
+        assert torch.equal(a, b)
+    # and the first sequence's rows against the oracle
+    Hn = H.float().cpu().numpy().astype(np.float64)
+    p = np.flatnonzero(x[0] == mask_id)
+    ref = orc.softmax_stats(orc.logits_f64(Hn[0, np.maximum(p - 1, 0)], W.float().cpu().numpy().astype(np.float64)))
+    ok = ref["margin"] > MARGIN
+    assert np.array_equal(outs[1][1][:p.size].numpy()[ok], ref["arg"][ok])
 
 
 def test_step_batch_graph_capture(dev):
