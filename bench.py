@@ -445,7 +445,7 @@ def gpu_main(args):
                    "parallelism": (f"vocab-sharded x{world} ({args.exchange} exchange, {args.backend} group)"
                                    if world > 1 else "single GPU"),
                    "vocab_shard": v1 - v0, "n_splits": head.n_splits,
-                   "k3_schedule": "die-aware" if head.die_table is not None else "default",
+                   "k3_schedule": k3_schedule_taken(head),
                    "k3_a_path": ("runs: contiguous-run tiles read H by TMA, K2 compacts only the other tiles' rows"
                                  if head.a_runs else "buffered: K2 compacts every masked row into Hc"),
                    "l2": "inputs larger than L2 (W 1.04 GB, H 268 MB > 126 MB)"},
@@ -482,6 +482,20 @@ def gpu_main(args):
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
+
+
+def k3_schedule_taken(head) -> str:
+    """The unit schedule the last K3 launch actually ran: the die-aware launch
+    agrees on a decision word (sched[3]: 1 = die-aware split, 2 = every pair was
+    not resident within ~100 us, default split) -- plus the die map's counts."""
+    if head.die_table is None:
+        return "default"
+    from paper_2601_06562_b200 import hotpath
+
+    word = int(head.buf["sched"][3].item())
+    _, info = hotpath.die_map(head.weight.device)
+    taken = {1: "die-aware", 2: "default (die-aware fallback)"}.get(word, f"unknown ({word})")
+    return f"{taken}; die map {info['die0_sms']}/{info['n_sm']} SMs on die 0, {info['ambiguous']} ambiguous"
 
 
 def k3_traffic() -> tuple:

@@ -446,7 +446,9 @@ __global__ void __launch_bounds__(threads_for(kGather, kSample), 1)
           // warp 0 has issued the whole unit, i.e. waited on every slot's
           // free-barrier in ring order: skipping ahead without it would let them
           // poll a slot's barrier several phases early, where its 1-bit parity
-          // aliases
+          // aliases. bar.sync is the .aligned form: warp 0 reconverges first (its
+          // lane 0 issued the boxes), or the barrier sees a divergent warp
+          __syncwarp();
           asm volatile("bar.sync 1, %0;" ::"n"(kAWarps * 32) : "memory");
           phase ^= ((stage + n_st) / C::STAGES) & 1;
           stage = (stage + n_st) % C::STAGES;

@@ -19,7 +19,9 @@ Op kinds (mosaic/workload.py:179-316, plus the fused-logits kinds):
   ``fused_ffn``: ffn_gate_up (K10 + SwiGLU epilogue) / ffn_down_res (K10 +
   residual epilogue: down, chunk_write and the residual add in one launch);
 * gather (K2) / lmhead_stats (K3) / sample (K4) / commit (K5) — the fused
-  mask-only logits + remask hot path (``logits_mode="fused"``);
+  mask-only logits + remask hot path (``logits_mode="fused"``); in runs mode
+  (default) the gather compacts only the rows of K3 tiles that are not one
+  contiguous run of h, and K3 reads the run tiles from h by TMA;
 * gather_logits / logits / shift / chunk_write / sample — the reference's
   materialising modes (``mask_only`` / ``eager``), executed with cuBLAS and
   fp32 softmax as the dense-logits baseline.
@@ -28,6 +30,7 @@ from __future__ import annotations
 
 import ctypes
 import math
+import os
 from typing import Optional
 
 import torch
@@ -164,6 +167,10 @@ class StepExecutor:
         self._die_table = None
         self._die_tried = False
         self._sched = torch.zeros(4, dtype=torch.int32, device=dev)
+        # fused logits: runs-mode A path (K3 reads contiguous-run tiles of h by TMA, the gather op
+        # compacts only the other tiles' rows); MOSAIC_A_RUNS=0 gathers every row
+        self.a_runs = os.environ.get("MOSAIC_A_RUNS", "1") != "0"
+        self._runs_src = None
         # torch-side step temporaries (attention outputs, cuBLAS scratch) live in a
         # region at the start of the arena, served by csrc/pool.cu through a MemPool;
         # the planned activations follow it (offsets shifted by its size)
@@ -469,7 +476,12 @@ class StepExecutor:
             v[dst][r0:r1].copy_(v[src][: r1 - r0])
         elif kind == "gather":  # K2, fused mode
             r0, r1 = _rows(M, b["K_logits"], op.iteration)
-            if r1 > r0:
+            if r1 > r0 and self.a_runs:
+                hc = v[op.outputs[0]]
+                hotpath.gather_rows_scattered(v[op.inputs[0]], mask_idx[r0:r1], hc, hc.shape[0], m_host=r1 - r0,
+                                              shift=self.shift)
+                self._runs_src = (v[op.inputs[0]], mask_idx[r0:r1])  # h stays live across the loop (barrier)
+            elif r1 > r0:
                 hotpath.gather_rows(v[op.inputs[0]], mask_idx[r0:r1], v[op.outputs[0]], m_host=r1 - r0,
                                     shift=self.shift)
         elif kind == "lmhead_stats":  # K3
@@ -482,7 +494,13 @@ class StepExecutor:
             flat = buf.view(-1)
             pm, ps = flat[: S * cap].view(S, cap), flat[S * cap: 2 * S * cap].view(S, cap)
             pa = flat[2 * S * cap: 3 * S * cap].view(torch.int32).view(S, cap)
-            if r1 > r0:
+            if r1 > r0 and self._runs_src is not None:
+                h, idx = self._runs_src
+                self._runs_src = None
+                hotpath.lmhead_stats_runs(h, idx, hc, self.model.w_vocab, S, pm, ps, pa, cap, m_host=r1 - r0,
+                                          shift=self.shift, v_offset=self.model.vocab_offset,
+                                          die_of_sm=self._die(cap), sched=self._sched)
+            elif r1 > r0:
                 hotpath.lmhead_stats(hc, self.model.w_vocab, S, pm, ps, pa, m_host=r1 - r0,
                                      v_offset=self.model.vocab_offset, die_of_sm=self._die(cap),
                                      sched=self._sched)

@@ -16,6 +16,10 @@ for fg in (False, True):
     for da in (False, True):  # default and die-aware unit schedules (registration + decision prologue)
         head = MaskOnlyHead(W, seq_len=L, mask_id=mid, shift=True, fused_gather=fg, die_aware=da)
         head.step(torch.from_numpy(x).to(dev), H, 50)
+# runs mode with contiguous-run tiles (A boxes from H) beside scattered ones (A from the partial Hc)
+xr = x.copy(); xr[500:1600] = mid
+for da in (False, True):
+    MaskOnlyHead(W, seq_len=L, mask_id=mid, shift=True, die_aware=da).step(torch.from_numpy(xr).to(dev), H, 50)
 # windowed step and batched step (segmented K5), shift on
 head = MaskOnlyHead(W, seq_len=L, mask_id=mid, shift=True)
 head.step(torch.from_numpy(x).to(dev), H, 5, window=(1000, 1040))
@@ -23,6 +27,8 @@ Bx = torch.from_numpy(np.stack([x[:1000], x[1000:2000], x[2000:3000]])).to(dev)
 bh = MaskOnlyHead(W, seq_len=3 * 100, mask_id=mid, shift=True)
 bh.step_batch(Bx, H[:3000].reshape(3, 1000, d).contiguous(), torch.tensor([3, 0, 7], dtype=torch.int32, device=dev),
               window=(400, 500))
+MaskOnlyHead(W, seq_len=3000, mask_id=mid, shift=True).step_batch(  # shift at lo = 0: rows repeat, no run tiles
+    Bx, H[:3000].reshape(3, 1000, d).contiguous(), 4)
 MaskOnlyHead(W, seq_len=L, mask_id=mid, temperature=0.7, seed=3).step(torch.from_numpy(x).to(dev), H, 9)
 head = MaskOnlyHead(W, seq_len=L, mask_id=mid, m_cap=100)  # M <= 128 -> cta_group::1
 xs = x.copy(); xs[:] = 1; xs[:90] = mid
