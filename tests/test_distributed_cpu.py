@@ -68,12 +68,12 @@ def _worker(rank, world, port, V, m, seed, q):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("V,m", [(1000, 64), (126464 // 64, 33)])
-def test_vocab_sharded_merge_world2(V, m):
+@pytest.mark.parametrize("V,m,world", [(1000, 64, 2), (126464 // 64, 33, 2), (1001, 40, 4)])
+def test_vocab_sharded_merge_world2(V, m, world):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, 2, port, V, m, 7, q)) for r in range(2)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, V, m, 7, q)) for r in range(world)]
     for p in procs:
         p.start()
     res = {}
@@ -84,7 +84,7 @@ def test_vocab_sharded_merge_world2(V, m):
         p.join(timeout=60)
         assert p.exitcode == 0
     # every rank reached the same tokens, confidences and selection ...
-    assert res[0] == res[1]
+    assert all(res[r] == res[0] for r in range(world))
     # ... equal to the unsharded statistics
     z = np.random.default_rng(7).standard_normal((m, V)) * 2.0
     whole = orc.softmax_stats(z)

@@ -1,5 +1,5 @@
 """bench.py's multi-rank branch end to end (make the first 8-GPU
-run low-risk): torchrun with two ranks, vocab-sharded, both exchanges. Both
+run low-risk): torchrun with 2, 4 and 8 ranks, vocab-sharded, both exchanges. Both
 ranks share GPU 0 (MOSAIC_BENCH_SHARE_GPU=1) under a gloo group -- NCCL refuses
 two ranks on one device -- so the NCCL-path code (all-gather of the triples +
 rank-order merge) runs over gloo's all-gather and the p2p path (K4x peer
@@ -25,11 +25,11 @@ def _port():
         return s.getsockname()[1]
 
 
-@pytest.mark.parametrize("exchange", ["nccl", "p2p"])
-def test_bench_two_ranks(native_lib, exchange):
+@pytest.mark.parametrize("world,exchange", [(2, "nccl"), (2, "p2p"), (4, "nccl"), (4, "p2p"), (8, "p2p")])
+def test_bench_multi_rank(native_lib, world, exchange):
     env = {**os.environ, "MOSAIC_BENCH_SHARE_GPU": "1"}
-    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
-           "--master-addr", "127.0.0.1", "--master-port", str(_port()), str(ROOT / "bench.py"), "--gpus", "2",
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", str(world),
+           "--master-addr", "127.0.0.1", "--master-port", str(_port()), str(ROOT / "bench.py"), "--gpus", str(world),
            "--steps", "2", "--warmup", "3", "--no-cpu-baseline", "--no-e2e", "--no-activation",
            "--backend", "gloo", "--exchange", exchange]
     r = subprocess.run(cmd, cwd=ROOT, env=env, capture_output=True, text=True, timeout=600)
@@ -37,6 +37,6 @@ def test_bench_two_ranks(native_lib, exchange):
     lines = [json.loads(l) for l in r.stdout.splitlines() if l.startswith("{")]
     assert len(lines) == 1, r.stdout[-2000:]  # rank 0 prints the one line
     line = lines[0]
-    assert line["n_gpus"] == 2 and line["value"] > 0 and line["config"]["vocab_shard"] == 126464 // 2
+    assert line["n_gpus"] == world and line["value"] > 0 and line["config"]["vocab_shard"] == 126464 // world
     assert exchange in line["config"]["parallelism"]
     assert line["gpu_launches"] > 0
