@@ -14,7 +14,7 @@
 //   c, s = cos, sin(p * theta^(-2i/dh)),
 // the angle formed in fp32 exactly as the torch reference
 // (tests/torch_reference.py) forms it. Streaming: 8 B of HBM traffic per pair
-// (read + write two bf16), one 16-byte vector of each half per thread.
+// (read + write two bf16), 16-byte vectors of each half.
 #include <cuda_bf16.h>
 
 #include "common.cuh"
@@ -23,41 +23,54 @@ namespace mosaic {
 namespace {
 
 constexpr int kRopeThreads = 256;
+constexpr int kHeadsPerThread = 8;  // heads sharing one thread's angles
 
+// One thread: row `row`, pair vector jv (8 consecutive pairs of every head),
+// a chunk of kHeadsPerThread heads, q and k. The 8 angles depend on (row, jv)
+// only, so they are formed once and applied to 2 x kHeadsPerThread vector
+// pairs (round 1 formed them per head and per tensor: 64x the sincosf work,
+// which made the pass compute-bound at 0.58 of HBM). Consecutive threads take
+// consecutive jv, then head chunks, so each head-iteration of a warp touches
+// whole 128-byte runs of the lo and hi halves.
 __global__ void __launch_bounds__(kRopeThreads)
     k11_rope(uint16_t* __restrict__ q, uint16_t* __restrict__ k, int64_t L, int32_t n_heads, int32_t head_dim,
              int64_t ld, const float* __restrict__ inv_freq, int64_t pos0) {
   const int half = head_dim / 2;
-  const int vec_per_head = half / 8;
-  const int64_t per_row = static_cast<int64_t>(n_heads) * vec_per_head;
-  const int64_t total = 2 * L * per_row;  // q then k
+  const int vec_per_half = half / 8;
+  const int chunks = (n_heads + kHeadsPerThread - 1) / kHeadsPerThread;
+  const int per_row = vec_per_half * chunks;
+  const int64_t total = L * per_row;
   for (int64_t i = blockIdx.x * static_cast<int64_t>(kRopeThreads) + threadIdx.x; i < total;
        i += static_cast<int64_t>(gridDim.x) * kRopeThreads) {
-    const int64_t which = i / (L * per_row);
-    const int64_t rem = i - which * L * per_row;
-    const int64_t row = rem / per_row;
-    const int64_t hv = rem - row * per_row;
-    const int h = static_cast<int>(hv / vec_per_head);
-    const int j0 = static_cast<int>(hv - static_cast<int64_t>(h) * vec_per_head) * 8;  // first pair of the vector
-    uint16_t* base = (which == 0 ? q : k) + row * ld + static_cast<int64_t>(h) * head_dim;
-    uint4* lo_p = reinterpret_cast<uint4*>(base + j0);
-    uint4* hi_p = reinterpret_cast<uint4*>(base + half + j0);
-    uint4 lo = *lo_p, hi = *hi_p;
-    __nv_bfloat162* l2 = reinterpret_cast<__nv_bfloat162*>(&lo);
-    __nv_bfloat162* h2 = reinterpret_cast<__nv_bfloat162*>(&hi);
+    const int64_t row = i / per_row;
+    const int r = static_cast<int>(i - row * per_row);
+    const int chunk = r / vec_per_half;
+    const int j0 = (r - chunk * vec_per_half) * 8;  // first pair of the vector
     const float p = static_cast<float>(row + pos0);
+    float c[8], sn[8];
 #pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      const float2 a = __bfloat1622float2(l2[j]);
-      const float2 b = __bfloat1622float2(h2[j]);
-      float s0, c0, s1, c1;
-      sincosf(p * __ldg(inv_freq + j0 + 2 * j), &s0, &c0);
-      sincosf(p * __ldg(inv_freq + j0 + 2 * j + 1), &s1, &c1);
-      l2[j] = __floats2bfloat162_rn(a.x * c0 - b.x * s0, a.y * c1 - b.y * s1);
-      h2[j] = __floats2bfloat162_rn(b.x * c0 + a.x * s0, b.y * c1 + a.y * s1);
+    for (int j = 0; j < 8; ++j) sincosf(p * __ldg(inv_freq + j0 + j), &sn[j], &c[j]);
+    const int h_end = min(n_heads, (chunk + 1) * kHeadsPerThread);
+    for (int h = chunk * kHeadsPerThread; h < h_end; ++h) {
+#pragma unroll
+      for (int t = 0; t < 2; ++t) {
+        uint16_t* base = (t == 0 ? q : k) + row * ld + static_cast<int64_t>(h) * head_dim;
+        uint4* lo_p = reinterpret_cast<uint4*>(base + j0);
+        uint4* hi_p = reinterpret_cast<uint4*>(base + half + j0);
+        uint4 lo = *lo_p, hi = *hi_p;
+        __nv_bfloat162* l2 = reinterpret_cast<__nv_bfloat162*>(&lo);
+        __nv_bfloat162* h2 = reinterpret_cast<__nv_bfloat162*>(&hi);
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const float2 a = __bfloat1622float2(l2[j]);
+          const float2 b = __bfloat1622float2(h2[j]);
+          l2[j] = __floats2bfloat162_rn(a.x * c[2 * j] - b.x * sn[2 * j], a.y * c[2 * j + 1] - b.y * sn[2 * j + 1]);
+          h2[j] = __floats2bfloat162_rn(b.x * c[2 * j] + a.x * sn[2 * j], b.y * c[2 * j + 1] + a.y * sn[2 * j + 1]);
+        }
+        *lo_p = lo;
+        *hi_p = hi;
+      }
     }
-    *lo_p = lo;
-    *hi_p = hi;
   }
 }
 
@@ -75,9 +88,9 @@ extern "C" int mosaic_rope_qk(uint16_t* q, uint16_t* k, int64_t L, int32_t n_hea
   MOSAIC_REQUIRE(q && k && inv_freq, "null operands");
   MOSAIC_REQUIRE((reinterpret_cast<uintptr_t>(q) & 15) == 0 && (reinterpret_cast<uintptr_t>(k) & 15) == 0,
                  "q/k must be 16-byte aligned");
-  const int64_t total = 2 * L * n_heads * (head_dim / 16);
+  const int64_t total = L * ((n_heads + kHeadsPerThread - 1) / kHeadsPerThread) * (head_dim / 16);
   const int64_t want = ceil_div(total, kRopeThreads);
-  const int64_t cap = static_cast<int64_t>(num_sms()) * 8;
+  const int64_t cap = static_cast<int64_t>(num_sms()) * 16;
   k11_rope<<<static_cast<int>(want < cap ? want : cap), kRopeThreads, 0, as_stream(stream)>>>(
       q, k, L, n_heads, head_dim, ld, inv_freq, pos0);
   return check_launch("mosaic_rope_qk");

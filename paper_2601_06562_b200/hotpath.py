@@ -388,9 +388,11 @@ def rope_inv_freq(head_dim: int, theta: float, device) -> torch.Tensor:
 
 def rope_qk_(q: torch.Tensor, k: torch.Tensor, n_heads: int, inv_freq: torch.Tensor, pos0: int = 0,
              stream=None) -> None:
-    """In place: rotary embedding of q and k ([L, n_heads * head_dim] bf16 rows)."""
-    _req(q, torch.bfloat16, "q", 2)
-    _req(k, torch.bfloat16, "k", 2)
+    """In place: rotary embedding of q and k ([L, n_heads * head_dim] bf16 rows;
+    the rows may be strided, e.g. the q and k column blocks of one fused qkv)."""
+    for t, n in ((q, "q"), (k, "k")):
+        if not t.is_cuda or t.dtype != torch.bfloat16 or t.dim() != 2:
+            raise InputError(f"{n} must be a 2-D bf16 CUDA tensor")
     if q.shape != k.shape or q.stride() != k.stride() or q.stride(1) != 1:
         raise InputError("q and k must be [L, d] row-major views of the same shape and stride")
     _req(inv_freq, torch.float32, "inv_freq", 1)

@@ -58,7 +58,7 @@ def main():
 
         l0 = launches[0]
         t = {"bytes_per_launch": l0["dram_read_bytes"] + l0["dram_write_bytes"],
-             "kernel": l0.get("kernel"), "source": str(out), "duration_ns_under_ncu": l0.get("duration_ns"),
+             "kernel": l0.get("kernel"), "source": f"profiles/{out.name}", "duration_ns_under_ncu": l0.get("duration_ns"),
              "code_hash": _build.source_hash(_build.K3_SOURCES),
              "code_hash_of": "csrc/lmhead.cu + csrc/common.cuh + nvcc flags (paper_2601_06562_b200._build.source_hash)"}
         (out.parent / "k3_traffic.json").write_text(json.dumps(t, indent=1))

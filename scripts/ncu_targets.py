@@ -1,6 +1,9 @@
-"""One launch each of the HBM-bound kernels (K2 gather, K6 SwiGLU, K9 combine)
-and of K10 (FFN GEMM) at the BASELINE shapes, for an ncu --set full capture:
-    ncu --set full -k regex:'k2_|k6_|k9_|k10_' -o prof python scripts/ncu_targets.py"""
+"""One launch each of the HBM-bound kernels (K2 gather, K6 SwiGLU, K9 combine,
+K11 RoPE) and of K10 (FFN GEMM: gate/up + SwiGLU, down + residual) at the
+BASELINE shapes, for an ncu --set full capture:
+    ncu --set full -k regex:'k2_|k6_|k9_|k10_|k11_' -o prof python scripts/ncu_targets.py
+K2 runs on a scattered layout (every tile gathered: runs mode compacts all rows,
+the same launch the buffered path makes)."""
 import os
 import sys
 
@@ -15,10 +18,14 @@ g = torch.Generator(device=dev).manual_seed(0)
 # K2: LLaDA 32k, 16384 masked rows of d 4096
 L, d = 32768, 4096
 H = torch.randn(L, d, generator=g, device=dev).to(torch.bfloat16)
-idx = torch.arange(L // 2, L, device=dev, dtype=torch.int32)
+idx = torch.randperm(L, generator=g, device=dev)[: L // 2].sort().values.to(torch.int32)
 hc = torch.empty(L // 2, d, device=dev, dtype=torch.bfloat16)
-hotpath.gather_rows(H, idx, hc, m_host=L // 2)
-del H, hc
+hotpath.gather_rows_scattered(H, idx, hc, L // 2, m_host=L // 2)
+# K11: rotary positions on q and k of one LLaDA layer at 32k (32 heads of 128)
+q = torch.randn(L, d, generator=g, device=dev).to(torch.bfloat16)
+inv = hotpath.rope_inv_freq(128, 10000.0, dev)
+hotpath.rope_qk_(q, H, 32, inv)
+del H, hc, q
 # K6: LLaDA FFN chunk 32768 x 12288
 gate = torch.randn(32768, 12288, generator=g, device=dev).to(torch.bfloat16)
 up = torch.randn(32768, 12288, generator=g, device=dev).to(torch.bfloat16)
@@ -37,5 +44,8 @@ x = torch.randn(32768, 4096, generator=g, device=dev).to(torch.bfloat16)
 wgu = (torch.randn(2 * 12288, 4096, generator=g, device=dev) * 0.02).to(torch.bfloat16)
 act = torch.empty(32768, 12288, device=dev, dtype=torch.bfloat16)
 hotpath.ffn_gemm(x, wgu, act, 2 * 12288, m_host=32768, swiglu=True)
+# K10: dense down projection with the residual epilogue (h[rows] += act @ W_down)
+wd = (torch.randn(4096, 12288, generator=g, device=dev) * 0.02).to(torch.bfloat16)
+hotpath.ffn_gemm(act, wd, x, 4096, m_host=32768, residual=True)
 torch.cuda.synchronize()
 print("ok")

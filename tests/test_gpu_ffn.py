@@ -101,22 +101,33 @@ def test_grouped_from_moe_routing(dev):
         torch.testing.assert_close(act[o[e]:o[e + 1]].float(), ref, rtol=2e-2, atol=2e-2)
 
 
-@pytest.mark.parametrize("L,H,dh,theta", [(1, 4, 64, 500000.0), (2048, 4, 64, 500000.0), (5000, 32, 128, 1e6)])
-def test_rope_vs_torch(dev, L, H, dh, theta):
+@pytest.mark.parametrize("L,H,dh,theta,fused", [(1, 4, 64, 500000.0, False), (2048, 4, 64, 500000.0, False),
+                                                (5000, 32, 128, 1e6, False), (3001, 28, 128, 1e6, True),
+                                                (77, 3, 32, 1e4, True)])
+def test_rope_vs_torch(dev, L, H, dh, theta, fused):
     """K11 rotary embedding of q and k in place against the torch fp32
-    restatement (tests/torch_reference.py): one bf16 rounding apart at most."""
+    restatement (tests/torch_reference.py): one bf16 rounding apart at most.
+    Head counts that are not a multiple of K11's 8-head chunk (Dream's 28),
+    and q/k as strided views of one fused [L, 3*H*dh] qkv row."""
     from torch_reference import rope
 
     from paper_2601_06562_b200 import hotpath
 
-    q = _rand((L, H * dh), dev, seed=5)
-    k = _rand((L, H * dh), dev, seed=6)
+    if fused:
+        qkv = _rand((L, 3 * H * dh), dev, seed=7)
+        v0 = qkv[:, 2 * H * dh:].clone()
+        q, k = qkv[:, :H * dh], qkv[:, H * dh:2 * H * dh]
+    else:
+        q = _rand((L, H * dh), dev, seed=5)
+        k = _rand((L, H * dh), dev, seed=6)
     inv = hotpath.rope_inv_freq(dh, theta, dev)
     rq, rk = rope(q, H, inv), rope(k, H, inv)
     hotpath.rope_qk_(q, k, H, inv)
     for got, want in ((q, rq), (k, rk)):
         torch.testing.assert_close(got.float(), want.float(), rtol=1e-2, atol=1e-2)
         assert (got != want).float().mean().item() < 0.01  # almost everywhere bit-equal
+    if fused:
+        assert torch.equal(qkv[:, 2 * H * dh:], v0)  # v untouched
 
 
 @pytest.mark.parametrize("M,K,N", [(1, 128, 256), (777, 768, 256), (3000, 1408, 2048), (4096, 18944, 3584)])
