@@ -1,6 +1,6 @@
-"""Soak: many fused steps with every K3 variant (buffered / gather mode x default /
-die-aware schedule) on random inputs, each compared bit for bit with the buffered
-default-schedule step. Catches rare ordering bugs in the pair-gather relay and the
+"""Soak: many fused steps with every K3 variant (buffered / runs / gather mode x
+default / die-aware schedule) on random inputs (scattered and blocked masks), each
+compared bit for bit with the buffered default-schedule step. Catches rare ordering bugs in the pair-gather relay and the
 die-aware registration that a single test run would miss.
 
     python scripts/soak_variants.py [--iters N] [--seconds S]
@@ -37,14 +37,20 @@ while n < args.iters and time.time() - t0 < args.seconds:
     H = torch.randn(L, d, generator=rng, device=dev).to(torch.bfloat16)
     x0 = torch.randint(0, V - 1, (L,), generator=rng, device=dev, dtype=torch.int32)
     frac = float(torch.rand(1, generator=rng, device=dev)) * 0.9 + 0.05
-    x0[torch.rand(L, generator=rng, device=dev) < frac] = mask_id
+    if n % 2:  # scattered positions
+        x0[torch.rand(L, generator=rng, device=dev) < frac] = mask_id
+    else:  # a few masked blocks: contiguous-run tiles for the runs / gather A paths
+        for _ in range(1 + n % 4):
+            a = int(torch.randint(0, L, (1,), generator=rng, device=dev))
+            x0[a:a + int(frac * L / 3) + 1] = mask_id
     outs = []
-    for gather in (False, True):
+    for a_path in ("buffered", "runs", "gather"):
         for die in (False, True):
-            key = (gather, die, shift)
+            key = (a_path, die, shift)
             if key not in hv:
-                hv[key] = MaskOnlyHead(W, seq_len=L, mask_id=mask_id, shift=shift, fused_gather=gather,
+                hv[key] = MaskOnlyHead(W, seq_len=L, mask_id=mask_id, shift=shift, fused_gather=a_path == "gather",
                                        die_aware=die)
+                hv[key].a_runs = a_path == "runs"
             x = x0.clone()
             o = hv[key].step(x, H, 64)
             M = int(o.m_dev.item())
@@ -72,5 +78,5 @@ while n < args.iters and time.time() - t0 < args.seconds:
             print(f"MISMATCH (sampling) iter {n} shape {(L, d, V)}", flush=True)
     n += 1
 torch.cuda.synchronize()
-print(f"soak: {n} iterations x 4 variants in {time.time() - t0:.0f} s, mismatches {mismatches}")
+print(f"soak: {n} iterations x 6 variants in {time.time() - t0:.0f} s, mismatches {mismatches}")
 sys.exit(1 if mismatches else 0)

@@ -1,8 +1,8 @@
 """Seeded fuzz of the whole fused step against the oracle: random sequence
 lengths, widths (multiples of 64), vocabulary sizes (ragged against the
 256-column tile), mask densities and layouts, unmask counts, token shift,
-and every K3 variant (buffered or gather mode, default or die-aware unit
-schedule, single-SM or pair tiles), and temperature sampling in a third of the
+and every K3 variant (runs mode, buffered or gather mode, default or
+die-aware unit schedule, single-SM or pair tiles), and temperature sampling in a third of the
 buffered cases. Tolerances as tests/test_gpu_parity.py:
 indices and selections bit-exact, tokens exact where the fp64 top-1 margin
 exceeds 1e-3, lse / confidence within 1e-3 relative.
@@ -34,17 +34,17 @@ def _case(i: int):
     layout = str(rng.choice(["scattered", "suffix", "blocks"]))
     k = int(rng.integers(0, 300))
     shift = bool(rng.integers(0, 2))
-    gather = bool(rng.integers(0, 2))
+    a_path = str(rng.choice(["runs", "buffered", "gather"]))  # K3's A operand: runs mode (default) / K2 all / H
     die = bool(rng.integers(0, 2))
-    temperature = float(rng.choice([0.0, 0.0, 0.5, 1.5])) if not gather else 0.0  # sampling: buffered A path
-    return rng, L, d, V, density, layout, k, shift, gather, die, temperature
+    temperature = float(rng.choice([0.0, 0.0, 0.5, 1.5])) if a_path != "gather" else 0.0  # sampling: buffered A
+    return rng, L, d, V, density, layout, k, shift, a_path, die, temperature
 
 
 @pytest.mark.parametrize("i", range(N_CASES))
 def test_fused_step_fuzz(dev, i):
     from paper_2601_06562_b200 import MaskOnlyHead
 
-    rng, L, d, V, density, layout, k, shift, gather, die, temperature = _case(i)
+    rng, L, d, V, density, layout, k, shift, a_path, die, temperature = _case(i)
     mask_id = V - 1
     x = rng.integers(0, max(V - 1, 1), size=L).astype(np.int32)
     if layout == "scattered":
@@ -59,8 +59,10 @@ def test_fused_step_fuzz(dev, i):
     W = orc.bf16_round(rng.standard_normal((V, d)) * float(rng.choice([0.02, 0.1])))
     Hd = torch.from_numpy(H.astype(np.float32)).to(dev).bfloat16()
     Wd = torch.from_numpy(W.astype(np.float32)).to(dev).bfloat16()
-    head = MaskOnlyHead(Wd, seq_len=L, mask_id=mask_id, shift=shift, fused_gather=gather, die_aware=die,
-                        temperature=temperature, seed=i)
+    head = MaskOnlyHead(Wd, seq_len=L, mask_id=mask_id, shift=shift, fused_gather=a_path == "gather",
+                        die_aware=die, temperature=temperature, seed=i)
+    if a_path == "buffered":
+        head.a_runs = False
     xd = torch.from_numpy(x).to(dev)
     out = head.step(xd, Hd, k)
     torch.cuda.synchronize()
