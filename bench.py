@@ -485,17 +485,18 @@ def gpu_main(args):
 
 
 def k3_schedule_taken(head) -> str:
-    """The unit schedule the last K3 launch actually ran: the die-aware launch
-    agrees on a decision word (sched[3]: 1 = die-aware split, 2 = every pair was
-    not resident within ~100 us, default split) -- plus the die map's counts."""
+    """K3's unit schedule in this run: dynamic (units claimed from global
+    counters, csrc/lmhead.cu) unless MOSAIC_K3_STATIC=1; with the die map,
+    die-0 pairs claim from the front and die-1 pairs from the back."""
+    if os.environ.get("MOSAIC_K3_STATIC") == "1":
+        return "static (pair c takes units c, c + pairs, ...)"
     if head.die_table is None:
-        return "default"
+        return "dynamic (every pair claims from the front)"
     from paper_2601_06562_b200 import hotpath
 
-    word = int(head.buf["sched"][3].item())
     _, info = hotpath.die_map(head.weight.device)
-    taken = {1: "die-aware", 2: "default (die-aware fallback)"}.get(word, f"unknown ({word})")
-    return f"{taken}; die map {info['die0_sms']}/{info['n_sm']} SMs on die 0, {info['ambiguous']} ambiguous"
+    return (f"dynamic die-aware (die-0 pairs claim from the front, die-1 pairs from the back); die map "
+            f"{info['die0_sms']}/{info['n_sm']} SMs on die 0, {info['ambiguous']} ambiguous")
 
 
 def k3_traffic() -> tuple:

@@ -100,7 +100,7 @@ def shard_times(M, d, V, dev):
         torch.cuda.synchronize()
         ms = a.elapsed_time(b) / 3
         out[f"P{P}"] = {"vocab_shard": v, "k3_k4_ms": ms, "tflops": 2.0 * M * d * v / ms / 1e9,
-                        "k3_schedule": "die-aware" if die is not None else "default"}
+                        "k3_schedule": "dynamic die-aware" if die is not None else "dynamic"}
     return out
 
 

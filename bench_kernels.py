@@ -80,8 +80,10 @@ def main():
         ps = torch.empty(S, M, device=dev)
         pa = torch.empty(S, M, device=dev, dtype=torch.int32)
         it = 5 if M * V > 1e9 else 50
-        ms = timeit(lambda: hotpath.lmhead_stats(hc, W, S, pm, ps, pa, m_host=M), iters=it)
         die, sched = hotpath.die_map(dev)[0], torch.zeros(4, dtype=torch.int32, device=dev)
+        # the product's dynamic unit schedule; the static one and the die-split dynamic one beside it
+        ms = timeit(lambda: hotpath.lmhead_stats(hc, W, S, pm, ps, pa, m_host=M, sched=sched), iters=it)
+        ms_static = timeit(lambda: hotpath.lmhead_stats(hc, W, S, pm, ps, pa, m_host=M), iters=it)
         ms_die = timeit(lambda: hotpath.lmhead_stats(hc, W, S, pm, ps, pa, m_host=M, die_of_sm=die, sched=sched),
                         iters=it)
         flops = 2.0 * M * d * V
@@ -91,6 +93,8 @@ def main():
         ms4 = timeit(lambda: hotpath.stats_merge(pm, ps, pa, S, M, M, m_host=M, token=tok, lse=lse, conf=conf))
         out[f"k3_lmhead_{name}"] = {"M": M, "d": d, "V": V, "splits": S, "tiles_per_split": tps, "ms": ms,
                                     "TFLOPs": flops / ms / 1e9, "frac_bf16_peak": flops / ms / 1e9 / tf,
+                                    "schedule": "dynamic", "static_ms": ms_static,
+                                    "static_TFLOPs": flops / ms_static / 1e9,
                                     "die_aware_ms": ms_die, "die_aware_TFLOPs": flops / ms_die / 1e9,
                                     "k4_merge_ms": ms4}
         del hc, W
@@ -107,7 +111,7 @@ def main():
         pm = torch.empty(S, M, device=dev)
         ps = torch.empty(S, M, device=dev)
         pa = torch.empty(S, M, device=dev, dtype=torch.int32)
-        die, sched = hotpath.die_map(dev)[0], torch.zeros(4, dtype=torch.int32, device=dev)
+        die, sched = None, torch.zeros(4, dtype=torch.int32, device=dev)  # dynamic schedule (product default)
         ms = timeit(lambda: hotpath.lmhead_stats_gather(H, idx, W, S, pm, ps, pa, M, m_host=M, die_of_sm=die,
                                                         sched=sched), iters=5)
         hc = torch.empty(M, d, device=dev, dtype=torch.bfloat16)
@@ -121,7 +125,7 @@ def main():
         out[f"k3_gather_{name}"] = {"M": M, "d": d, "V": V, "splits": S, "ms": ms, "TFLOPs": flops / ms / 1e9,
                                     "frac_bf16_peak": flops / ms / 1e9 / tf, "k2_plus_k3_ms": ms_sep,
                                     "runs_k2_plus_k3_ms": ms_runs,
-                                    "schedule": "die-aware (all)", "hc_bytes_saved": M * d * 2}
+                                    "schedule": "dynamic (all)", "hc_bytes_saved": M * d * 2}
         del H, W, hc
 
     # whole step: eager launches vs one captured CUDA graph (launch-bound at small sizes)

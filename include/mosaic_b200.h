@@ -124,23 +124,26 @@ MOSAIC_API int mosaic_lmhead_stats(const uint16_t* Hc, int64_t m_cap, const int3
                         int32_t n_splits, float* part_max, float* part_sum, int32_t* part_arg,
                         void* stream);
 
-/* K3 with the die-aware unit schedule: as mosaic_lmhead_stats, but the work
- * units are split between the GPU's two L2 dies in proportion to the SM pairs
- * each die holds, each die's pairs taking a contiguous range of whole m-groups,
- * so a row block stays in one die's L2. die_of_sm: device uint8 [num SMs] from
- * mosaic_die_map (0/1); sched_scratch: 16 caller-owned device bytes (zeroed by
- * the call; one launch at a time per scratch; word 3 ends as 1 = die-aware
- * split taken, 2 = not every pair became resident within ~100 us, default
- * split taken). Exact for any map and either outcome.                        */
+/* K3 with the dynamic unit schedule (MaskOnlyHead's default): the pairs claim
+ * work units (row block x vocab split, numbered m-fastest inside groups of 16
+ * row blocks) from counters in sched_scratch (16 caller-owned device bytes,
+ * zeroed by the call; one launch at a time per scratch), so the units in flight
+ * stay one contiguous window of the order and each split's LM-head tiles are
+ * shared through L2 (DRAM per LLaDA 32k launch 5.8 GB vs 12.1 GB for the
+ * static order the plain entry point keeps). die_of_sm (optional, device
+ * uint8 [num SMs] from mosaic_die_map, 0/1): pairs on die 1 claim from the back
+ * of the order instead of the front. Same outputs bit for bit as
+ * mosaic_lmhead_stats for any schedule and any map.                          */
 MOSAIC_API int mosaic_lmhead_stats_die(const uint16_t* Hc, int64_t m_cap, const int32_t* m_dev, int64_t m_host,
                             const uint16_t* W, int64_t V_shard, int64_t d, int64_t v_offset,
                             int32_t n_splits, float* part_max, float* part_sum, int32_t* part_arg,
                             const uint8_t* die_of_sm, uint32_t* sched_scratch, void* stream);
 
 /* SM -> L2-die map, measured (two cold-read latency classes; see
- * csrc/topology.cu). die_of_sm_host receives 0/1 per SM (255 = unknown);
- * scratch holds mosaic_die_map_scratch_bytes(n_sm) device bytes. Synchronises
- * `stream`. *ambiguous_out counts SMs without a clear class.                 */
+ * csrc/topology.cu), for the optional die split of the dynamic schedule.
+ * die_of_sm_host receives 0/1 per SM (255 = unknown); scratch holds
+ * mosaic_die_map_scratch_bytes(n_sm) device bytes. Synchronises `stream`.
+ * *ambiguous_out counts SMs without a clear class.                          */
 MOSAIC_API size_t mosaic_die_map_scratch_bytes(int32_t n_sm);
 MOSAIC_API int mosaic_die_map(uint8_t* die_of_sm_host, int32_t n_sm, void* scratch, int32_t* n_die0_out,
                    int32_t* ambiguous_out, void* stream);
@@ -151,7 +154,7 @@ MOSAIC_API int mosaic_die_map(uint8_t* die_of_sm_host, int32_t n_sm, void* scrat
  * max(p-1, 0) with shift = 1) by cp.async loader warps (16-byte segments,
  * swizzled in software to the UMMA layout), so K2 and the [m_cap, d]
  * compacted buffer disappear. Outputs as mosaic_lmhead_stats. The _die form
- * adds the die-aware schedule (arguments as mosaic_lmhead_stats_die).        */
+ * takes the dynamic schedule (arguments as mosaic_lmhead_stats_die).         */
 MOSAIC_API int mosaic_lmhead_stats_gather(const uint16_t* H, int64_t n_rows, int64_t ld_h, const int32_t* idx,
                                int32_t shift, int64_t m_cap, const int32_t* m_dev, int64_t m_host,
                                const uint16_t* W, int64_t V_shard, int64_t d, int64_t v_offset,
@@ -171,7 +174,8 @@ MOSAIC_API int mosaic_lmhead_stats_gather_die(const uint16_t* H, int64_t n_rows,
  * feed the dense TMA pipeline, so every tile runs at the dense rate and the
  * gathered copy shrinks to the scattered tiles. Replaces gather_gemm
  * (kernel.py:62-86) like mosaic_lmhead_stats, with identical outputs;
- * die_of_sm / sched_scratch optional (null = default schedule).             */
+ * sched_scratch (16 B) selects the dynamic schedule, die_of_sm its optional
+ * die split (both null = static schedule).                                  */
 MOSAIC_API int mosaic_lmhead_stats_runs(const uint16_t* H, int64_t n_rows, int64_t ld_h, const int32_t* idx,
                              int32_t shift, int64_t m_cap, const int32_t* m_dev, int64_t m_host,
                              const uint16_t* Hc, const uint16_t* W, int64_t V_shard, int64_t d,

@@ -60,6 +60,13 @@ constexpr int threads_for(int gather, bool sample) {
                      : ((sample || MOSAIC_K3_EPI_HALVES == 2) ? kThreads + kEpiWarps * 32 : kThreads);
 }
 constexpr int kMaxSplits = 64;
+// Dynamic unit schedule: the pair leader's producer thread claims units from
+// global counters and publishes each id into this ring in both CTAs; every
+// other role of the pair reads it. No free-slot barrier: the producer runs at
+// most STAGES k-blocks (so <= STAGES units) ahead of the MMA issuer, which runs
+// at most NUM_ACC tiles ahead of the slowest epilogue, so the reader furthest
+// behind lags the publisher by < STAGES + NUM_ACC + 2 < kURing units.
+constexpr int kURing = 16;
 #ifndef MOSAIC_K3_EPI_SLEEP_NS
 #define MOSAIC_K3_EPI_SLEEP_NS 0   // epilogue poll backoff while the next accumulator fills
 #endif
@@ -83,7 +90,10 @@ struct Cfg {
 #define MOSAIC_K3_STAGES2 6
 #endif
   static constexpr int STAGES = CG == 1 ? 4 : MOSAIC_K3_STAGES2;
-  static constexpr int SMEM = STAGES * STAGE_BYTES + 1024 + 256 + BM * 4 + 16;  // + gather rows, die schedule
+  static constexpr int OFF_BAR = STAGES * STAGE_BYTES;  // mbarriers + TMEM slot (256 B)
+  static constexpr int OFF_SIDX = OFF_BAR + 256;          // gather4 rows (BM int32)
+  static constexpr int OFF_RING = OFF_SIDX + BM * 4;      // unit ring: kURing mbarriers + kURing ids
+  static constexpr int SMEM = OFF_RING + kURing * 12 + 1024;  // + 1 KB alignment slack
   static constexpr uint32_t IDESC = umma_idesc_bf16(ROWS, BN);
 };
 
@@ -98,9 +108,10 @@ struct Params {
   int32_t n_splits;
   int32_t group_m;
   int32_t seg_splits;  // vocab segments of this many splits, processed segment-major (0 = one segment)
-  const uint8_t* die_of_sm;  // die-aware schedule: SM -> L2 die (null = off)
+  const uint8_t* die_of_sm;  // die-aware dynamic schedule: SM -> L2 die (null = every pair claims from the front)
   int32_t n_sm;              // entries of die_of_sm (%smid need not be below it: treated as die 0)
-  uint32_t* sched;           // die-aware schedule: [die0 pairs, die1 pairs, registered, decision], zeroed per launch
+  uint32_t* sched;           // dynamic schedule: [claimed, front, back, unused] counters, zeroed per launch;
+                             // null = static schedule (pair c takes units c, c + pairs, ...)
   int32_t policy;   // L2 policy of (A, B) loads: 0 = (normal, normal), 1 = (evict_last, normal), 2 = (normal, evict_first), 3 = (evict_last, evict_first)
   int64_t v_offset;
   float* part_max;
@@ -285,7 +296,9 @@ __global__ void __launch_bounds__(threads_for(kGather, kSample), 1)
   // arrival from the peer CTA)
   uint64_t* afull = tempty + NUM_ACC;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(afull + C::STAGES);
-  int32_t* sidx = reinterpret_cast<int32_t*>(smem + C::STAGES * C::STAGE_BYTES + 256);  // gather rows
+  int32_t* sidx = reinterpret_cast<int32_t*>(smem + C::OFF_SIDX);  // gather rows
+  uint64_t* ufull = reinterpret_cast<uint64_t*>(smem + C::OFF_RING);  // unit ring: id published
+  int32_t* uring = reinterpret_cast<int32_t*>(ufull + kURing);
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -307,6 +320,7 @@ __global__ void __launch_bounds__(threads_for(kGather, kSample), 1)
       mbar_init(&tfull[i], 1);
       mbar_init(&tempty[i], kEpiWarps * ((kSample || (kGather != 2 && MOSAIC_K3_EPI_HALVES == 2)) ? 2 : 1) * CG);
     }
+    for (int i = 0; i < kURing; ++i) mbar_init(&ufull[i], 1);
     fence_mbar_init();
   }
   if (warp == 1) tmem_alloc<CG>(tmem_slot, TMEM_COLS);
@@ -321,63 +335,55 @@ __global__ void __launch_bounds__(threads_for(kGather, kSample), 1)
   const int64_t M = min(static_cast<int64_t>(load_count(p.m_dev, p.m_host)), p.m_cap);
   const int m_blocks = static_cast<int>((M + C::ROWS - 1) / C::ROWS);
 
-  // Die-aware schedule: the units (in the usual m-group order, so a contiguous
-  // unit range covers whole m-groups) are split between the two dies in
-  // proportion to the pairs each die actually got, and each die's pairs stride
-  // over their own range only -- an m-group's rows (re-read once per vocab
-  // tile) then live in one die's L2 instead of being replicated in both.
-  // Splitting by units rather than whole m-blocks keeps every pair within one
-  // unit of the default schedule's load. The pair leader registers its die
-  // (slot = arrival order on that die); the split needs every pair registered,
-  // so the pairs agree on a decision word: the pair whose registration
-  // completes the count publishes "die-aware", and a pair that waited ~100 us
-  // without that (some CTAs not resident, e.g. another kernel holding SMs)
-  // publishes "default". Whoever comes later reads the published decision, so
-  // the launch never traps or hangs, and either schedule is exact.
-  // sched[0..1] = pairs registered per die, sched[2] = total, sched[3] = decision.
-  int64_t u_first = cluster, u_stride = n_clusters;
-  int64_t units_here = static_cast<int64_t>(m_blocks) * p.n_splits;
-  if (p.die_of_sm != nullptr) {
-    int32_t* info = reinterpret_cast<int32_t*>(smem + C::STAGES * C::STAGE_BYTES + 256 + BM * 4);
-    if (threadIdx.x == 0 && rank == 0) {
-      uint32_t smid;
-      asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
-      const int d = (static_cast<int32_t>(smid) < p.n_sm && p.die_of_sm[smid] == 1) ? 1 : 0;
-      const uint32_t slot = atomicAdd(p.sched + d, 1u);
-      __threadfence();
-      volatile uint32_t* decision = p.sched + 3;
-      if (atomicAdd(p.sched + 2, 1u) + 1u == static_cast<uint32_t>(n_clusters)) {
-        __threadfence();
-        atomicCAS(p.sched + 3, 0u, 1u);  // every pair registered: die-aware
-      }
-      const long long t0 = clock64();
-      while (*decision == 0u) {
-        if (clock64() - t0 > 200000) atomicCAS(p.sched + 3, 0u, 2u);  // ~100+ us: fall back
-        __nanosleep(200);
-      }
-      __threadfence();
-      int32_t v[3] = {static_cast<int32_t>(cluster), static_cast<int32_t>(n_clusters),
-                      static_cast<int32_t>(units_here)};
-      if (*decision == 1u) {
-        const int64_t n0 = *reinterpret_cast<volatile uint32_t*>(p.sched + 0);
-        const int64_t n1 = *reinterpret_cast<volatile uint32_t*>(p.sched + 1);
-        const int64_t u0 = (units_here * n0 + (n0 + n1) / 2) / (n0 + n1);  // die 0: [0, u0), die 1: [u0, end)
-        v[0] = static_cast<int32_t>((d ? u0 : 0) + slot);
-        v[1] = static_cast<int32_t>(d ? n1 : n0);
-        v[2] = static_cast<int32_t>(d ? units_here : u0);
-      }
-      for (int i = 0; i < 3; ++i) {
-        info[i] = v[i];
-        if constexpr (CG == 2)
-          asm volatile("st.shared::cluster.s32 [%0], %1;" ::"r"(mapa_shared(smem_u32(info + i), 1)), "r"(v[i])
-                       : "memory");
-      }
-    }
-    if constexpr (CG == 2) cluster_sync(); else __syncthreads();
-    u_first = info[0];
-    u_stride = info[1];
-    units_here = info[2];
+  // Unit schedule. Units (m-block, split) are numbered m-fastest inside groups
+  // of group_m m-blocks (unit_coords), so a contiguous range of unit ids shares
+  // the group's row blocks and each split's W tiles through L2.
+  //  * static (p.sched == null): pair c runs units c, c + pairs, ... -- the
+  //    pairs drift apart over many units (equal work, unequal speed), and the
+  //    units of one split stop sharing W fetches (Dream 128k: 77 GB of DRAM per
+  //    launch against ~25 GB in lockstep, profiles/r02h_k3_shapes.json);
+  //  * dynamic: the pair leader's producer claims the next unit from global
+  //    counters when it starts one, so the units in flight are always one
+  //    contiguous window of ids; with a die map, pairs on die 0 claim from the
+  //    front of the range and pairs on die 1 from the back, so each die walks its
+  //    own m-groups (its L2 holds them) and the two meet wherever their speeds
+  //    put them -- no registration, no per-die pair counts, no idle tail.
+  //    Claimed ids reach the pair's other roles through the unit ring.
+  const int64_t units = static_cast<int64_t>(m_blocks) * p.n_splits;
+  const bool dyn = p.sched != nullptr;
+  int die = 0;
+  if (dyn && p.die_of_sm != nullptr) {
+    uint32_t smid;
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+    die = (static_cast<int32_t>(smid) < p.n_sm && p.die_of_sm[smid] == 1) ? 1 : 0;
   }
+  // the n-th unit of this pair (-1: no more); `publisher`: the pair leader's
+  // producer thread, which claims it and publishes it to both CTAs' rings
+  auto unit_at = [&](int n, bool publisher) -> int64_t {
+    if (!dyn) {
+      const int64_t u = cluster + static_cast<int64_t>(n) * n_clusters;
+      return u < units ? u : -1;
+    }
+    const int slot = n & (kURing - 1);
+    if (publisher) {
+      int32_t u = -1;
+      if (atomicAdd(p.sched + 0, 1u) < static_cast<uint32_t>(units))
+        u = die == 0 ? static_cast<int32_t>(atomicAdd(p.sched + 1, 1u))
+                     : static_cast<int32_t>(units - 1 - static_cast<int64_t>(atomicAdd(p.sched + 2, 1u)));
+      uring[slot] = u;
+      if constexpr (CG == 2) {
+        asm volatile("st.shared::cluster.s32 [%0], %1;" ::"r"(mapa_shared(smem_u32(uring + slot), 1)), "r"(u)
+                     : "memory");
+        mbar_arrive_cluster(mapa_shared(smem_u32(&ufull[slot]), 1));  // release.cluster: orders the store
+      }
+      mbar_arrive(&ufull[slot]);
+      return u;
+    }
+    if (CG == 2 && rank == 1) mbar_wait_cluster(&ufull[slot], (n / kURing) & 1);
+    else mbar_wait(&ufull[slot], (n / kURing) & 1);
+    return *reinterpret_cast<volatile int32_t*>(uring + slot);
+  };
+  const bool is_publisher = dyn && rank == 0 && warp == 0 && lane == 0;
 
   if (warp == 0 || (kGather == kGatherCpAsync && warp >= 6)) {
     // ------------------------------------------------------------ TMA producer (both CTAs)
@@ -387,7 +393,12 @@ __global__ void __launch_bounds__(threads_for(kGather, kSample), 1)
     const uint64_t pol_b = (p.policy == 2 || p.policy == 3) ? policy_evict_first() : policy_evict_normal();
     uint32_t stage = 0, phase = 0;
     int a_pend = 0;  // cp.async A path: slots issued by this thread and not yet released
-    for (int64_t u = u_first; u < units_here; u += u_stride) {
+    for (int n = 0;; ++n) {
+      // lane 0 of each producer warp learns the unit (the leader's warp 0 lane 0 claims it)
+      int64_t u = 0;
+      if (lane == 0) u = unit_at(n, is_publisher);
+      u = __shfl_sync(0xffffffffu, u, 0);
+      if (u < 0) break;
       int mb, s;
       unit_coords(p, m_blocks, u, mb, s);
       const int t0 = s * p.tiles_per_split;
@@ -548,7 +559,9 @@ __global__ void __launch_bounds__(threads_for(kGather, kSample), 1)
     if (lane == 0 && rank == 0) {
       uint32_t stage = 0, phase = 0, acc = 0, acc_phase = 0;
       uint32_t abits = 0;  // gather mode: expected afull parity per slot (only gathered uses flip it)
-      for (int64_t u = u_first; u < units_here; u += u_stride) {
+      for (int n = 0;; ++n) {
+        const int64_t u = unit_at(n, false);
+        if (u < 0) break;
         int mb, s;
         unit_coords(p, m_blocks, u, mb, s);
         const int t0 = s * p.tiles_per_split;
@@ -597,7 +610,9 @@ __global__ void __launch_bounds__(threads_for(kGather, kSample), 1)
       // peer CTA of the pair: relay "A slot landed" to the leader's barrier
       if (lane == 0 && rank == 1) {
         uint32_t stage = 0, phase = 0, abits = 0;
-        for (int64_t u = u_first; u < units_here; u += u_stride) {
+        for (int n = 0;; ++n) {
+          const int64_t u = unit_at(n, false);
+          if (u < 0) break;
           int mb, s;
           unit_coords(p, m_blocks, u, mb, s);
           const int t0 = s * p.tiles_per_split;
@@ -638,7 +653,11 @@ __global__ void __launch_bounds__(threads_for(kGather, kSample), 1)
     // tempty lives in the pair leader: arrive locally or through the cluster window
     const uint32_t tempty_addr0 = CG == 2 ? mapa_shared(smem_u32(&tempty[0]), 0) : smem_u32(&tempty[0]);
     uint32_t acc = 0, acc_phase = 0;
-    for (int64_t u = u_first; u < units_here; u += u_stride) {
+    for (int n = 0;; ++n) {
+      int64_t u = 0;
+      if (lane == 0) u = unit_at(n, false);
+      u = __shfl_sync(0xffffffffu, u, 0);
+      if (u < 0) break;
       int mb, s;
       unit_coords(p, m_blocks, u, mb, s);
       const int t0 = s * p.tiles_per_split;
@@ -920,9 +939,15 @@ int launch(const ASource& a, int64_t m_cap, const int32_t* m_dev, int64_t m_host
   static const int policy = env_int("MOSAIC_L2_POLICY", 1);  // measured best: A evict_last
   p.policy = policy;
   cudaStream_t s = as_stream(stream);
-  if (p.die_of_sm != nullptr) {
-    MOSAIC_REQUIRE(p.sched != nullptr, "die-aware schedule needs its 16-byte scratch");
-    p.n_sm = num_sms();  // the die table holds one entry per SM (hotpath.die_map)
+  MOSAIC_REQUIRE(p.die_of_sm == nullptr || p.sched != nullptr, "the die map needs the dynamic schedule's scratch");
+  MOSAIC_REQUIRE(p.sched == nullptr || !kStore, "materialised logits use the static schedule");
+  static const int force_static = env_int("MOSAIC_K3_STATIC", 0);  // experiment: the static schedule
+  if (force_static) {
+    p.sched = nullptr;
+    p.die_of_sm = nullptr;
+  }
+  if (p.sched != nullptr) {  // dynamic schedule: counters start at zero every launch
+    p.n_sm = num_sms();      // the die table holds one entry per SM (hotpath.die_map)
     MOSAIC_CUDA(cudaMemsetAsync(p.sched, 0, 16, s));
   }
   if (runs) {
@@ -1083,7 +1108,7 @@ extern "C" int mosaic_lmhead_stats_gather_die(const uint16_t* H, int64_t n_rows,
                                               int32_t n_splits, float* part_max, float* part_sum,
                                               int32_t* part_arg, const uint8_t* die_of_sm, uint32_t* sched_scratch,
                                               void* stream) {
-  MOSAIC_REQUIRE(die_of_sm && sched_scratch, "die-aware gather needs the die map and its 16-byte scratch");
+  MOSAIC_REQUIRE(sched_scratch, "the dynamic schedule needs its 16-byte scratch (die_of_sm optional)");
   return lmhead_stats_gather_impl(H, n_rows, ld_h, idx, shift, m_cap, m_dev, m_host, W, V_shard, d, v_offset,
                                   n_splits, part_max, part_sum, part_arg, die_of_sm, sched_scratch, stream);
 }

@@ -121,8 +121,8 @@ def lmhead_sample(hc: torch.Tensor, weight: torch.Tensor, n_splits: int, pos: to
         _req(t, dt, n)
         if t.numel() < 2 * n_splits * m_cap:
             raise InputError(f"{n} must hold 2*n_splits*m_cap entries (two column halves per split)")
-    if die_of_sm is not None and (sched is None or sched.numel() * sched.element_size() < 16):
-        raise InputError("the die-aware schedule needs a 16-byte sched scratch")
+    if (die_of_sm is not None or sched is not None) and (sched is None or sched.numel() * sched.element_size() < 16):
+        raise InputError("the dynamic schedule needs a 16-byte sched scratch")
     _native.call("mosaic_lmhead_sample", _p(hc), m_cap, _p(m_dev), int(m_host), _p(weight), weight.shape[0], d,
                  int(v_offset), int(n_splits), _p(pos), ctypes.c_float(float(temperature)),
                  ctypes.c_uint32(int(seed) & 0xFFFFFFFF), _p(part_max), _p(part_sum), _p(part_arg), _p(part_y),
@@ -173,19 +173,20 @@ def die_table_or_none(device) -> Optional[torch.Tensor]:
 
 
 def die_aware_default(die_aware: Optional[bool] = None, m_cap: int = 0, v_shard: int = 0) -> bool:
-    """Whether K3 takes the die-aware unit schedule. An explicit argument or
-    MOSAIC_DIE_AWARE=0/1 decides; otherwise it is on when m_cap >= 4096 rows
-    and the vocab shard >= 8192, where it was measured faster in the
-    power-capped steady state (profiles/r01i_k3_die_aware_steady.txt: Dream
-    +6.6%, LLaDA +3%, MoE-like +2.5%, the 1/4 and 1/8 LLaDA shards +1.1% /
-    +0.6%, neutral at M = 4096), and off for small heads, where the launch-time
-    registration (~6 us) is not repaid."""
+    """Whether K3's dynamic schedule uses the SM -> die map (die-0 pairs claim
+    units from the front, die-1 pairs from the back). An explicit argument or
+    MOSAIC_DIE_AWARE=0/1 decides; the default is off: with units claimed
+    dynamically the pairs already walk one contiguous window of m-groups, and
+    the die split measured slightly slower with more DRAM traffic (LLaDA 32k
+    steady 1.320-1.324 M vs 1.329-1.333 M masked tok/s, DRAM 7.3 vs 5.8 GB per
+    launch; Dream 128k 30.1 vs 23.3 GB, profiles/r02i_k3_dynamic_schedule.txt).
+    ``m_cap`` / ``v_shard`` are kept for callers that size the decision."""
     if die_aware is not None:
         return bool(die_aware)
     env = os.environ.get("MOSAIC_DIE_AWARE")
     if env in ("0", "1"):
         return env == "1"
-    return m_cap >= 4096 and v_shard >= 8192
+    return False
 
 
 def lmhead_stats(hc: torch.Tensor, weight: torch.Tensor, n_splits: int, part_max: torch.Tensor,
@@ -202,9 +203,9 @@ def lmhead_stats(hc: torch.Tensor, weight: torch.Tensor, n_splits: int, part_max
         _req(t, dt, n)
         if t.numel() < n_splits * m_cap:
             raise InputError(f"{n} must hold n_splits*m_cap entries")
-    if die_of_sm is not None:  # die-aware unit schedule (see csrc/lmhead.cu)
+    if die_of_sm is not None or sched is not None:  # dynamic unit schedule (+ die map), csrc/lmhead.cu
         if sched is None or sched.numel() * sched.element_size() < 16:
-            raise InputError("the die-aware schedule needs a 16-byte sched scratch")
+            raise InputError("the dynamic schedule needs a 16-byte sched scratch")
         _native.call("mosaic_lmhead_stats_die", _p(hc), m_cap, _p(m_dev), int(m_host), _p(weight),
                      weight.shape[0], d, int(v_offset), int(n_splits), _p(part_max), _p(part_sum),
                      _p(part_arg), _p(die_of_sm), _p(sched), _s(stream))
@@ -238,9 +239,9 @@ def lmhead_stats_gather(hidden: torch.Tensor, idx: torch.Tensor, weight: torch.T
         _req(t, dt, n)
         if t.numel() < n_splits * m_cap:
             raise InputError(f"{n} must hold n_splits*m_cap entries")
-    if die_of_sm is not None:
+    if die_of_sm is not None or sched is not None:
         if sched is None or sched.numel() * sched.element_size() < 16:
-            raise InputError("the die-aware schedule needs a 16-byte sched scratch")
+            raise InputError("the dynamic schedule needs a 16-byte sched scratch")
         _native.call("mosaic_lmhead_stats_gather_die", _p(hidden), hidden.shape[0], hidden.stride(0), _p(idx),
                      _shift_flags(shift, repeats), int(m_cap), _p(m_dev), int(m_host), _p(weight), weight.shape[0], d,
                      int(v_offset), int(n_splits), _p(part_max), _p(part_sum), _p(part_arg), _p(die_of_sm),
@@ -304,8 +305,8 @@ def lmhead_stats_runs(hidden: torch.Tensor, idx: torch.Tensor, hc: torch.Tensor,
         _req(t, dt, n)
         if t.numel() < n_splits * m_cap:
             raise InputError(f"{n} must hold n_splits*m_cap entries")
-    if die_of_sm is not None and (sched is None or sched.numel() * sched.element_size() < 16):
-        raise InputError("the die-aware schedule needs a 16-byte sched scratch")
+    if (die_of_sm is not None or sched is not None) and (sched is None or sched.numel() * sched.element_size() < 16):
+        raise InputError("the dynamic schedule needs a 16-byte sched scratch")
     _native.call("mosaic_lmhead_stats_runs", _p(hidden), hidden.shape[0], hidden.stride(0), _p(idx),
                  _shift_flags(shift, repeats), int(m_cap), _p(m_dev), int(m_host), _p(hc), _p(weight), weight.shape[0], d,
                  int(v_offset), int(n_splits), _p(part_max), _p(part_sum), _p(part_arg), _p(die_of_sm), _p(sched),

@@ -1,5 +1,7 @@
-"""Same-box A/B of K3's die-aware vs default unit schedule at per-rank vocab
-shards (strong-scaling shapes), alternating, CUDA events on the launching stream.
+"""Same-box A/B of K3's unit schedules -- static (pair c takes units c, c +
+pairs, ...), dynamic (units claimed from a global counter), dynamic die-aware
+(die-0 pairs claim from the front, die-1 pairs from the back) -- at the full and
+per-rank vocab-shard shapes, alternating, CUDA events on the launching stream.
 
     python scripts/k3_die_ab.py [--reps 3]
 """
@@ -39,10 +41,11 @@ def main():
         S, _ = hotpath.lmhead_plan(M, V, d)
         pm, ps = torch.empty(S, M, device=dev), torch.empty(S, M, device=dev)
         pa = torch.empty(S, M, device=dev, dtype=torch.int32)
-        res = {"default": [], "die": []}
+        res = {"static": [], "dynamic": [], "dynamic_die": []}
         for _ in range(a.reps):
-            for mode in ("default", "die"):
-                kw = dict(die_of_sm=table, sched=sched) if mode == "die" else {}
+            for mode in res:
+                kw = ({} if mode == "static" else
+                      dict(sched=sched) if mode == "dynamic" else dict(die_of_sm=table, sched=sched))
                 for _ in range(3):
                     hotpath.lmhead_stats(hc, W, S, pm, ps, pa, m_host=M, **kw)
                 s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)

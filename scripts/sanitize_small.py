@@ -13,7 +13,7 @@ x = rng.integers(0, V - 1, size=L).astype(np.int32); x[rng.random(L) < 0.5] = mi
 H = torch.from_numpy(rng.standard_normal((L, d)).astype(np.float32)).to(dev).bfloat16()
 W = torch.from_numpy((rng.standard_normal((V, d)) * 0.05).astype(np.float32)).to(dev).bfloat16()
 for fg in (False, True):
-    for da in (False, True):  # default and die-aware unit schedules (registration + decision prologue)
+    for da in (False, True):  # dynamic and dynamic die-aware unit schedules (unit ring)
         head = MaskOnlyHead(W, seq_len=L, mask_id=mid, shift=True, fused_gather=fg, die_aware=da)
         head.step(torch.from_numpy(x).to(dev), H, 50)
 # runs mode with contiguous-run tiles (A boxes from H) beside scattered ones (A from the partial Hc)

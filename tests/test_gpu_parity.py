@@ -556,9 +556,11 @@ def test_full_size_k3_variants_bit_identical(dev, name, L, d, V, shift, k):
 
 def test_die_map_and_die_aware_k3(dev):
     """The measured SM -> die map splits the SMs into two halves (TPC pairs
-    together), and K3 under the die-aware schedule is bit-identical to the
-    default schedule -- also with a deliberately wrong map (exactness does not
-    depend on the map)."""
+    together), and K3 under every unit schedule -- static, dynamic, dynamic
+    die-aware with the measured map, an all-die-0 map or a random map -- is
+    bit-identical (exactness does not depend on the schedule). The dynamic
+    schedule's counters: every unit claimed exactly once (front + back =
+    units), one failed claim per pair."""
     from paper_2601_06562_b200 import hotpath
 
     table, info = hotpath.die_map(dev)
@@ -572,15 +574,23 @@ def test_die_map_and_die_aware_k3(dev):
         Hc = bf16_tensor(rng.standard_normal((m, d)), dev)
         W = bf16_tensor(rng.standard_normal((V, d)) * 0.03, dev)
         S, _ = hotpath.lmhead_plan(m, V, d)
+        cfg = hotpath.lmhead_config(m)
+        units = -(-m // hotpath.lmhead_tile_rows(m)) * S
+        pairs = min(units, torch.cuda.get_device_properties(dev).multi_processor_count // cfg["cta_group"])
         outs = []
-        for tab in (None, table, torch.zeros_like(table), torch.from_numpy(rng.integers(0, 2, t.size).astype(np.uint8)).to(dev)):
+        rand_tab = torch.from_numpy(rng.integers(0, 2, t.size).astype(np.uint8)).to(dev)
+        for mode, tab in (("static", None), ("dynamic", None), ("die", table), ("die", torch.zeros_like(table)),
+                          ("die", rand_tab)):
             pm, ps = torch.empty(S, m, device=dev), torch.empty(S, m, device=dev)
             pa = torch.empty(S, m, dtype=torch.int32, device=dev)
-            sched = torch.empty(4, dtype=torch.int32, device=dev)
+            sched = torch.full((4,), 7, dtype=torch.int32, device=dev) if mode != "static" else None
             hotpath.lmhead_stats(Hc, W, S, pm, ps, pa, m_host=m, v_offset=3, die_of_sm=tab, sched=sched)
             torch.cuda.synchronize()
-            if tab is not None:  # alone on the GPU every pair registers: the die-aware split is taken
-                assert int(sched[3]) == 1
+            if sched is not None:
+                claimed, front, back = (int(v) for v in sched[:3].cpu())
+                assert front + back == units and claimed == units + pairs
+                if tab is None or not bool(tab.any()):
+                    assert back == 0
             outs.append((pm.cpu(), ps.cpu(), pa.cpu()))
         for o in outs[1:]:
             for a, b in zip(outs[0], o):
@@ -588,9 +598,10 @@ def test_die_map_and_die_aware_k3(dev):
 
 
 def test_die_aware_k3_with_sms_held_by_another_stream(dev):
-    """K3's die-aware prologue must neither trap nor hang when not every pair
-    can become resident (another stream's GEMM holds the SMs): the pairs agree
-    on the default schedule instead, and the result is unchanged."""
+    """K3's dynamic schedule must neither trap nor hang when not every pair
+    can become resident at once (another stream's GEMM holds the SMs): the
+    pairs that are resident claim the units, every unit is claimed exactly
+    once, and the result is unchanged."""
     from paper_2601_06562_b200 import hotpath
 
     table, _ = hotpath.die_map(dev)
@@ -612,9 +623,9 @@ def test_die_aware_k3_with_sms_held_by_another_stream(dev):
                 a = (a @ a).clamp_(-1, 1)
         hotpath.lmhead_stats(Hc, W, S, pm, ps, pa, m_host=m, die_of_sm=tab, sched=sched)
         torch.cuda.synchronize()
-        decisions.append(int(sched[3]))
+        decisions.append(int(sched[1]) + int(sched[2]))
         outs.append((pm.cpu(), ps.cpu(), pa.cpu()))
-    assert decisions[1] in (1, 2)
+    assert decisions == [-(-m // 256) * S] * 2  # every unit claimed once
     for x, y in zip(*outs):
         assert torch.equal(x, y)
 
