@@ -110,7 +110,8 @@ struct Params {
   int32_t seg_splits;  // vocab segments of this many splits, processed segment-major (0 = one segment)
   const uint8_t* die_of_sm;  // die-aware dynamic schedule: SM -> L2 die (null = every pair claims from the front)
   int32_t n_sm;              // entries of die_of_sm (%smid need not be below it: treated as die 0)
-  uint32_t* sched;           // dynamic schedule: [claimed, front, back, unused] counters, zeroed per launch;
+  uint32_t* sched;           // dynamic schedule: [claimed (die split only), front, back, unused] counters,
+                             // zeroed per launch;
                              // null = static schedule (pair c takes units c, c + pairs, ...)
   int32_t policy;   // L2 policy of (A, B) loads: 0 = (normal, normal), 1 = (evict_last, normal), 2 = (normal, evict_first), 3 = (evict_last, evict_first)
   int64_t v_offset;
@@ -359,6 +360,22 @@ __global__ void __launch_bounds__(threads_for(kGather, kSample), 1)
   }
   // the n-th unit of this pair (-1: no more); `publisher`: the pair leader's
   // producer thread, which claims it and publishes it to both CTAs' rings
+  // claim: without a die map one atomic on the front counter; with it, a claim
+  // on the shared total first, then the front or back counter of this die
+  auto claim = [&]() -> int32_t {
+    if (p.die_of_sm == nullptr) {
+      const uint32_t c = atomicAdd(p.sched + 1, 1u);
+      return c < static_cast<uint32_t>(units) ? static_cast<int32_t>(c) : -1;
+    }
+    if (atomicAdd(p.sched + 0, 1u) >= static_cast<uint32_t>(units)) return -1;
+    return die == 0 ? static_cast<int32_t>(atomicAdd(p.sched + 1, 1u))
+                    : static_cast<int32_t>(units - 1 - static_cast<int64_t>(atomicAdd(p.sched + 2, 1u)));
+  };
+  // the publisher claims one unit ahead: the atomic for unit n + 1 is issued
+  // when unit n is published and its result is first used a whole unit later,
+  // so its latency never stalls the TMA stream (units of 2 tiles at 1/8 vocab
+  // shards last ~50 us)
+  int32_t claimed_next = (dyn && rank == 0 && warp == 0 && lane == 0) ? claim() : -1;
   auto unit_at = [&](int n, bool publisher) -> int64_t {
     if (!dyn) {
       const int64_t u = cluster + static_cast<int64_t>(n) * n_clusters;
@@ -366,10 +383,8 @@ __global__ void __launch_bounds__(threads_for(kGather, kSample), 1)
     }
     const int slot = n & (kURing - 1);
     if (publisher) {
-      int32_t u = -1;
-      if (atomicAdd(p.sched + 0, 1u) < static_cast<uint32_t>(units))
-        u = die == 0 ? static_cast<int32_t>(atomicAdd(p.sched + 1, 1u))
-                     : static_cast<int32_t>(units - 1 - static_cast<int64_t>(atomicAdd(p.sched + 2, 1u)));
+      const int32_t u = claimed_next;
+      claimed_next = u >= 0 ? claim() : -1;
       uring[slot] = u;
       if constexpr (CG == 2) {
         asm volatile("st.shared::cluster.s32 [%0], %1;" ::"r"(mapa_shared(smem_u32(uring + slot), 1)), "r"(u)
