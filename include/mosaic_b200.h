@@ -343,6 +343,15 @@ MOSAIC_API int mosaic_ffn_gemm(const uint16_t* A, int64_t rows_cap, int64_t lda,
 MOSAIC_API int mosaic_ffn_gemm_ex(const uint16_t* A, int64_t rows_cap, int64_t lda, const int32_t* group_off,
                                   int32_t G, int64_t m_host, const uint16_t* W, int64_t N, int64_t K,
                                   int32_t epilogue, uint16_t* C, int64_t ldc, void* stream);
+/* mosaic_ffn_gemm_ex with K3's dynamic unit schedule: sched_scratch (16
+ * caller-owned device bytes, zeroed by the call; one launch at a time per
+ * scratch) holds the counter the SM pairs claim output tiles from, so the
+ * tiles in flight stay one contiguous window of the m-grouped order (null =
+ * the static order of mosaic_ffn_gemm_ex). Identical outputs.               */
+MOSAIC_API int mosaic_ffn_gemm_sched(const uint16_t* A, int64_t rows_cap, int64_t lda, const int32_t* group_off,
+                                     int32_t G, int64_t m_host, const uint16_t* W, int64_t N, int64_t K,
+                                     int32_t epilogue, uint16_t* C, int64_t ldc, uint32_t* sched_scratch,
+                                     void* stream);
 
 /* ---------------------------------------------------------------- K7 ------
  * Contiguous device workspace with lazy physical commitment (cuMem VMM):

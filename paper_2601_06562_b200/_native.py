@@ -131,6 +131,11 @@ SIGNATURES: dict[str, tuple[object, list[object]]] = {
         [c_void_p, c_int64, c_int64, c_void_p, c_int32, c_int64, c_void_p, c_int64, c_int64, c_int32, c_void_p,
          c_int64, c_void_p],
     ),
+    "mosaic_ffn_gemm_sched": (
+        c_int,
+        [c_void_p, c_int64, c_int64, c_void_p, c_int32, c_int64, c_void_p, c_int64, c_int64, c_int32, c_void_p,
+         c_int64, c_void_p, c_void_p],
+    ),
     "mosaic_arena_reserve": (c_int, [c_int32, c_uint64, POINTER(c_void_p)]),
     "mosaic_arena_commit": (c_int, [c_void_p, c_uint64]),
     "mosaic_arena_info": (c_int, [c_void_p, _u64p, _u64p, _u64p, _u64p]),

@@ -46,6 +46,7 @@ constexpr int kThreads = 192;
 constexpr int kEpiWarps = 4;
 constexpr int kMaxGroups = 256;
 constexpr int kGroupM = 16;
+constexpr int kURing = 16;  // dynamic schedule's unit ring (as K3, csrc/lmhead.cu)
 
 // CG = 2: a CTA pair computes a 256 x 256 tile (tcgen05.mma.cta_group::2),
 // each CTA staging half of the rows and half of the weight columns, as K3.
@@ -57,7 +58,8 @@ struct GCfg {
   static constexpr int B_BYTES = B_ROWS * BK * 2;
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
   static constexpr int STAGES = CG == 1 ? 4 : 6;
-  static constexpr int SMEM = STAGES * STAGE_BYTES + 1024 + 256 + 2 * (kMaxGroups + 1) * 4;
+  static constexpr int OFF_RING = STAGES * STAGE_BYTES + 256 + 2 * (kMaxGroups + 1) * 4;  // 8-byte aligned
+  static constexpr int SMEM = OFF_RING + kURing * 12 + 1024;
   static constexpr uint32_t IDESC = umma_idesc_bf16(ROWS, BN);
 };
 
@@ -72,6 +74,7 @@ struct GParams {
   int32_t residual;  // C += A W^T (read-modify-write of each output vector)
   uint16_t* C;
   int64_t ldc;
+  uint32_t* sched;  // dynamic schedule: [unused, next unit, ...], zeroed per launch; null = static schedule
 };
 
 __device__ __forceinline__ float silu(float g) { return __fdividef(g, 1.f + __expf(-g)); }
@@ -130,6 +133,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + NUM_ACC);
   int32_t* s_off = reinterpret_cast<int32_t*>(smem + STAGES * STAGE_BYTES + 256);
   int32_t* s_mbp = s_off + kMaxGroups + 1;
+  uint64_t* ufull = reinterpret_cast<uint64_t*>(smem + C::OFF_RING);  // unit ring: id published
+  int32_t* uring = reinterpret_cast<int32_t*>(ufull + kURing);
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -149,6 +154,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(&tfull[i], 1);
       mbar_init(&tempty[i], kEpiWarps * CG);
     }
+    for (int i = 0; i < kURing; ++i) mbar_init(&ufull[i], 1);
     fence_mbar_init();
     // group row offsets and the exclusive prefix of their m-block counts
     int32_t mb = 0;
@@ -171,12 +177,48 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int64_t units = static_cast<int64_t>(total_mb) * p.n_tiles;
   const int k_blocks = p.K / BK;
 
+  // Unit schedule as K3's (csrc/lmhead.cu): static striding, or -- with a
+  // sched scratch -- units claimed from a global counter by the pair leader's
+  // producer (one claim ahead) and published to both CTAs through the ring, so
+  // the tiles in flight stay one contiguous window of the m-grouped order
+  // instead of drifting apart.
+  const bool dyn = p.sched != nullptr;
+  auto claim = [&]() -> int32_t {
+    const uint32_t c = atomicAdd(p.sched + 1, 1u);
+    return c < static_cast<uint32_t>(units) ? static_cast<int32_t>(c) : -1;
+  };
+  int32_t claimed_next = (dyn && rank == 0 && warp == 0 && lane == 0) ? claim() : -1;
+  auto unit_at = [&](int n, bool publisher) -> int64_t {
+    if (!dyn) {
+      const int64_t u = cluster + static_cast<int64_t>(n) * n_clusters;
+      return u < units ? u : -1;
+    }
+    const int slot = n & (kURing - 1);
+    if (publisher) {
+      const int32_t u = claimed_next;
+      claimed_next = u >= 0 ? claim() : -1;
+      uring[slot] = u;
+      if constexpr (CG == 2) {
+        asm volatile("st.shared::cluster.s32 [%0], %1;" ::"r"(mapa_shared(smem_u32(uring + slot), 1)), "r"(u)
+                     : "memory");
+        mbar_arrive_cluster(mapa_shared(smem_u32(&ufull[slot]), 1));
+      }
+      mbar_arrive(&ufull[slot]);
+      return u;
+    }
+    if (CG == 2 && rank == 1) mbar_wait_cluster(&ufull[slot], (n / kURing) & 1);
+    else mbar_wait(&ufull[slot], (n / kURing) & 1);
+    return *reinterpret_cast<volatile int32_t*>(uring + slot);
+  };
+
   if (warp == 0) {
     if (lane == 0) {
       const uint64_t pol_a = policy_evict_last();
       const uint64_t pol_b = policy_evict_normal();
       uint32_t stage = 0, phase = 0;
-      for (int64_t u = cluster; u < units; u += n_clusters) {
+      for (int n = 0;; ++n) {
+        const int64_t u = unit_at(n, dyn && rank == 0);
+        if (u < 0) break;
         const Unit w = unit_of<C::ROWS>(u, p.n_tiles, total_mb, s_off, s_mbp, G);
         const int32_t a_row = static_cast<int32_t>(w.row0 + rank * BM);
         const int32_t b_row = static_cast<int32_t>(w.g * p.N + static_cast<int64_t>(w.nt) * BN + rank * C::B_ROWS);
@@ -200,7 +242,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   } else if (warp == 1) {
     if (lane == 0 && rank == 0) {
       uint32_t stage = 0, phase = 0, acc = 0, acc_phase = 0;
-      for (int64_t u = cluster; u < units; u += n_clusters) {
+      for (int n = 0;; ++n) {
+        if (unit_at(n, false) < 0) break;
         if constexpr (CG == 2) mbar_wait_cluster(&tempty[acc], acc_phase ^ 1);
         else mbar_wait(&tempty[acc], acc_phase ^ 1);
         tc_fence_after();
@@ -232,7 +275,11 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int row_local = q * 32 + lane;
     const uint32_t tempty_addr0 = CG == 2 ? mapa_shared(smem_u32(&tempty[0]), 0) : smem_u32(&tempty[0]);
     uint32_t acc = 0, acc_phase = 0;
-    for (int64_t u = cluster; u < units; u += n_clusters) {
+    for (int n = 0;; ++n) {
+      int64_t u = 0;
+      if (lane == 0) u = unit_at(n, false);
+      u = __shfl_sync(0xffffffffu, u, 0);
+      if (u < 0) break;
       const Unit w = unit_of<C::ROWS>(u, p.n_tiles, total_mb, s_off, s_mbp, G);
       const int64_t row = w.row0 + rank * BM + row_local;
       const bool live = row < w.row_end;
@@ -341,6 +388,7 @@ int launch_k10(const CUtensorMap& ta, const CUtensorMap& tb, const GParams& p, i
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
+  if (p.sched != nullptr) MOSAIC_CUDA(cudaMemsetAsync(p.sched, 0, 16, stream));  // counters start at zero
   MOSAIC_CUDA(cudaLaunchKernelEx(&cfg, k10_ffn_gemm<CG>, ta, tb, p));
   return MOSAIC_OK;
 }
@@ -359,6 +407,13 @@ extern "C" int mosaic_ffn_gemm(const uint16_t* A, int64_t rows_cap, int64_t lda,
 extern "C" int mosaic_ffn_gemm_ex(const uint16_t* A, int64_t rows_cap, int64_t lda, const int32_t* group_off,
                                   int32_t G, int64_t m_host, const uint16_t* W, int64_t N, int64_t K, int32_t epilogue,
                                   uint16_t* C, int64_t ldc, void* stream) {
+  return mosaic_ffn_gemm_sched(A, rows_cap, lda, group_off, G, m_host, W, N, K, epilogue, C, ldc, nullptr, stream);
+}
+
+extern "C" int mosaic_ffn_gemm_sched(const uint16_t* A, int64_t rows_cap, int64_t lda, const int32_t* group_off,
+                                     int32_t G, int64_t m_host, const uint16_t* W, int64_t N, int64_t K,
+                                     int32_t epilogue, uint16_t* C, int64_t ldc, uint32_t* sched_scratch,
+                                     void* stream) {
   MOSAIC_REQUIRE(epilogue >= 0 && epilogue <= 2, "epilogue %d not in {0 store, 1 SwiGLU, 2 residual}", epilogue);
   const int32_t swiglu = epilogue == 1;
   MOSAIC_REQUIRE(A && W && C, "null operands");
@@ -396,6 +451,11 @@ extern "C" int mosaic_ffn_gemm_ex(const uint16_t* A, int64_t rows_cap, int64_t l
   p.residual = epilogue == 2 ? 1 : 0;
   p.C = C;
   p.ldc = ldc;
+  static const int force_static = [] {
+    const char* e = getenv("MOSAIC_K10_STATIC");
+    return e ? atoi(e) : 0;
+  }();
+  p.sched = force_static ? nullptr : sched_scratch;
   st = cg == 2 ? launch_k10<2>(ta, tb, p, rows_cap, as_stream(stream))
                : launch_k10<1>(ta, tb, p, rows_cap, as_stream(stream));
   if (st) return st;

@@ -166,7 +166,8 @@ class StepExecutor:
         self._die_aware = die_aware
         self._die_table = None
         self._die_tried = False
-        self._sched = torch.zeros(4, dtype=torch.int32, device=dev)
+        self._sched = torch.zeros(4, dtype=torch.int32, device=dev)  # K3's dynamic unit schedule
+        self._sched_ffn = torch.zeros(4, dtype=torch.int32, device=dev)  # K10's
         # fused logits: runs-mode A path (K3 reads contiguous-run tiles of h by TMA, the gather op
         # compacts only the other tiles' rows); MOSAIC_A_RUNS=0 gathers every row
         self.a_runs = os.environ.get("MOSAIC_A_RUNS", "1") != "0"
@@ -440,13 +441,13 @@ class StepExecutor:
             r0, r1 = _rows(L, b["K_FFN"], op.iteration)
             f = cfg.d_ff
             hotpath.ffn_gemm(v[op.inputs[0]][r0:r1], self._layer(op.op_id)["w_gate_up"], v[op.outputs[0]][: r1 - r0],
-                             2 * f, m_host=r1 - r0, swiglu=True)
+                             2 * f, m_host=r1 - r0, swiglu=True, sched=self._sched_ffn)
         elif kind == "ffn_down_res":  # K10: h_attn[rows] += act @ w_down (down + chunk_write + residual)
             r0, r1 = _rows(L, b["K_FFN"], op.iteration)
             if r1 > r0:
                 act, h = v[op.inputs[0]], v[op.inputs[2]]
                 hotpath.ffn_gemm(act[: r1 - r0], self._layer(op.op_id)["w_down"], h[r0:r1], d, m_host=r1 - r0,
-                                 residual=True)
+                                 residual=True, sched=self._sched_ffn)
         elif kind == "identity":
             pass  # in-place output naming the mutated storage (planned as one storage group)
         elif kind in ("ffn_up", "ffn_gate"):
@@ -577,11 +578,11 @@ class StepExecutor:
         elif kind == "ffn_gate_up":  # K10 grouped over the expert segments, SwiGLU epilogue
             xin, off = v[op.inputs[0]], v[op.inputs[2]]
             hotpath.ffn_gemm(xin[: n * k], lw["w_gate_up"], v[op.outputs[0]][: n * k], 2 * cfg.d_ff,
-                             group_off=off, groups=E, swiglu=True)
+                             group_off=off, groups=E, swiglu=True, sched=self._sched_ffn)
         elif kind == "ffn_down":  # K10 grouped, written over the dispatch rows (in place)
             act, off = v[op.inputs[0]], v[op.inputs[2]]
             hotpath.ffn_gemm(act[: n * k], lw["w_down"], v[op.outputs[0]][: n * k], cfg.d_model,
-                             group_off=off, groups=E)
+                             group_off=off, groups=E, sched=self._sched_ffn)
         elif kind == "moe_combine":
             src, rpos, rw, acc = (v[key] for key in op.inputs)
             hotpath.moe_combine(src[: n * k], rpos, rw, k, acc[r0:r1])

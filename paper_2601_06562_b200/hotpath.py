@@ -470,10 +470,11 @@ def interleave_gate_up(w_gate: torch.Tensor, w_up: torch.Tensor) -> torch.Tensor
 
 def ffn_gemm(a: torch.Tensor, w: torch.Tensor, out: torch.Tensor, n: int, group_off: Optional[torch.Tensor] = None,
              groups: int = 1, m_host: int = 0, swiglu: bool = False, residual: bool = False,
-             stream=None) -> None:
+             stream=None, sched: Optional[torch.Tensor] = None) -> None:
     """K10: out[rows of group g] = a[rows of g] @ w[g].T (bf16, fp32 accumulate),
     w = [groups * n, K] K-major; with ``swiglu`` out = silu(gate) * up, n/2
-    columns; with ``residual`` out += a @ w.T in place (one bf16 rounding)."""
+    columns; with ``residual`` out += a @ w.T in place (one bf16 rounding).
+    ``sched`` (16 device bytes): the dynamic tile schedule (as K3's)."""
     if swiglu and residual:
         raise InputError("swiglu and residual epilogues are exclusive")
     if a.dtype != torch.bfloat16 or a.dim() != 2 or a.stride(1) != 1 or not a.is_cuda:
@@ -492,9 +493,11 @@ def ffn_gemm(a: torch.Tensor, w: torch.Tensor, out: torch.Tensor, n: int, group_
             raise InputError("group_off needs groups + 1 entries")
     elif groups != 1:
         raise InputError("several groups need device offsets")
-    _native.call("mosaic_ffn_gemm_ex", _p(a), min(a.shape[0], out.shape[0]), a.stride(0), _p(group_off),
+    if sched is not None and sched.numel() * sched.element_size() < 16:
+        raise InputError("the dynamic schedule needs a 16-byte sched scratch")
+    _native.call("mosaic_ffn_gemm_sched", _p(a), min(a.shape[0], out.shape[0]), a.stride(0), _p(group_off),
                  int(groups), int(m_host), _p(w), int(n), K, 2 if residual else int(bool(swiglu)), _p(out),
-                 out.stride(0), _s(stream))
+                 out.stride(0), _p(sched), _s(stream))
 
 
 # ----------------------------------------------------------------- buffers

@@ -43,9 +43,10 @@ del src, out
 x = torch.randn(32768, 4096, generator=g, device=dev).to(torch.bfloat16)
 wgu = (torch.randn(2 * 12288, 4096, generator=g, device=dev) * 0.02).to(torch.bfloat16)
 act = torch.empty(32768, 12288, device=dev, dtype=torch.bfloat16)
-hotpath.ffn_gemm(x, wgu, act, 2 * 12288, m_host=32768, swiglu=True)
+sched = torch.zeros(4, dtype=torch.int32, device=dev)  # the dynamic tile schedule the executor uses
+hotpath.ffn_gemm(x, wgu, act, 2 * 12288, m_host=32768, swiglu=True, sched=sched)
 # K10: dense down projection with the residual epilogue (h[rows] += act @ W_down)
 wd = (torch.randn(4096, 12288, generator=g, device=dev) * 0.02).to(torch.bfloat16)
-hotpath.ffn_gemm(act, wd, x, 4096, m_host=32768, residual=True)
+hotpath.ffn_gemm(act, wd, x, 4096, m_host=32768, residual=True, sched=sched)
 torch.cuda.synchronize()
 print("ok")

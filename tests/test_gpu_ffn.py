@@ -145,3 +145,40 @@ def test_residual_epilogue_vs_fp32(dev, M, K, N):
     ref = (res[:M].float() + a.float() @ w.float()).bfloat16().float()
     torch.testing.assert_close(out[:M].float(), ref, rtol=1e-2, atol=1e-2)
     assert torch.equal(out[M:], res[M:])
+
+
+@pytest.mark.parametrize("M,K,N,mode,groups", [(5000, 1024, 3072, "swiglu", 1), (4096, 2048, 512, "residual", 1),
+                                               (777, 768, 256, "store", 1), (3000, 512, 1024, "swiglu", 4),
+                                               (100, 256, 512, "store", 1)])
+def test_k10_dynamic_schedule_bit_identical(dev, M, K, N, mode, groups):
+    """K10 with the dynamic tile schedule (tiles claimed from a counter in the
+    sched scratch, published through the unit ring) equals the static order
+    bit for bit in every epilogue, dense and grouped; every tile claimed once."""
+    from paper_2601_06562_b200 import hotpath
+
+    a = _rand((M, K), dev, seed=11)
+    w = _rand((groups * N, K), dev, scale=0.05, seed=12)
+    off = None
+    if groups > 1:
+        cuts = sorted(np.random.default_rng(1).integers(0, M, groups - 1).tolist())
+        off = torch.tensor([0] + cuts + [M], dtype=torch.int32, device=dev)
+    base = _rand((M, N // 2 if mode == "swiglu" else N), dev, seed=13)
+    outs = []
+    for sched in (None, torch.full((4,), 9, dtype=torch.int32, device=dev)):
+        out = base.clone()
+        hotpath.ffn_gemm(a, w, out, N, group_off=off, groups=groups, m_host=M, swiglu=mode == "swiglu",
+                         residual=mode == "residual", sched=sched)
+        torch.cuda.synchronize()
+        outs.append(out)
+        if sched is not None:
+            rows_blk = 256 if M > 128 else 128
+            if off is None:
+                tiles = -(-M // rows_blk) * -(-N // 256)
+            else:
+                o = off.cpu().tolist()
+                tiles = sum(-(-(o[g + 1] - o[g]) // rows_blk) for g in range(groups)) * -(-N // 256)
+            cg = 2 if M > 128 else 1
+            units_cap = (-(-M // rows_blk) + groups) * -(-N // 256)  # the launch's grid bound (csrc/ffn_gemm.cu)
+            pairs = min(units_cap, torch.cuda.get_device_properties(dev).multi_processor_count // cg)
+            assert int(sched[1]) == tiles + pairs  # every tile claimed once, one failed claim per pair
+    assert torch.equal(outs[0], outs[1])
