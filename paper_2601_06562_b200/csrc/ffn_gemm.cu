@@ -455,7 +455,9 @@ extern "C" int mosaic_ffn_gemm_sched(const uint16_t* A, int64_t rows_cap, int64_
     const char* e = getenv("MOSAIC_K10_STATIC");
     return e ? atoi(e) : 0;
   }();
-  p.sched = force_static ? nullptr : sched_scratch;
+  // at most two tiles per pair: nothing to balance, keep the static order (and skip the counter memset)
+  const int64_t tiles_cap = (ceil_div(rows_cap, static_cast<int64_t>(BM) * cg) + G) * p.n_tiles;
+  p.sched = (force_static || tiles_cap <= 2 * (num_sms() / cg)) ? nullptr : sched_scratch;
   st = cg == 2 ? launch_k10<2>(ta, tb, p, rows_cap, as_stream(stream))
                : launch_k10<1>(ta, tb, p, rows_cap, as_stream(stream));
   if (st) return st;

@@ -957,7 +957,11 @@ int launch(const ASource& a, int64_t m_cap, const int32_t* m_dev, int64_t m_host
   MOSAIC_REQUIRE(p.die_of_sm == nullptr || p.sched != nullptr, "the die map needs the dynamic schedule's scratch");
   MOSAIC_REQUIRE(p.sched == nullptr || !kStore, "materialised logits use the static schedule");
   static const int force_static = env_int("MOSAIC_K3_STATIC", 0);  // experiment: the static schedule
-  if (force_static) {
+  // a launch of at most two units per pair gains nothing from claiming (and
+  // the counters' memset would cost a launch): small heads keep the static order
+  const int64_t pairs = num_sms() / cg;
+  const bool few_units = ceil_div(m_cap, static_cast<int64_t>(BM) * cg) * p.n_splits <= 2 * pairs;
+  if (force_static || few_units) {
     p.sched = nullptr;
     p.die_of_sm = nullptr;
   }

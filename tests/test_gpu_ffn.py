@@ -179,6 +179,10 @@ def test_k10_dynamic_schedule_bit_identical(dev, M, K, N, mode, groups):
                 tiles = sum(-(-(o[g + 1] - o[g]) // rows_blk) for g in range(groups)) * -(-N // 256)
             cg = 2 if M > 128 else 1
             units_cap = (-(-M // rows_blk) + groups) * -(-N // 256)  # the launch's grid bound (csrc/ffn_gemm.cu)
-            pairs = min(units_cap, torch.cuda.get_device_properties(dev).multi_processor_count // cg)
-            assert int(sched[1]) == tiles + pairs  # every tile claimed once, one failed claim per pair
+            workers = torch.cuda.get_device_properties(dev).multi_processor_count // cg
+            pairs = min(units_cap, workers)
+            if units_cap <= 2 * workers:  # small launches keep the static order: counters untouched
+                assert int(sched[1]) == 9
+            else:
+                assert int(sched[1]) == tiles + pairs  # every tile claimed once, one failed claim per pair
     assert torch.equal(outs[0], outs[1])

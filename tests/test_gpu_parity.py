@@ -576,7 +576,8 @@ def test_die_map_and_die_aware_k3(dev):
         S, _ = hotpath.lmhead_plan(m, V, d)
         cfg = hotpath.lmhead_config(m)
         units = -(-m // hotpath.lmhead_tile_rows(m)) * S
-        pairs = min(units, torch.cuda.get_device_properties(dev).multi_processor_count // cfg["cta_group"])
+        workers = torch.cuda.get_device_properties(dev).multi_processor_count // cfg["cta_group"]
+        pairs = min(units, workers)
         outs = []
         rand_tab = torch.from_numpy(rng.integers(0, 2, t.size).astype(np.uint8)).to(dev)
         for mode, tab in (("static", None), ("dynamic", None), ("die", table), ("die", torch.zeros_like(table)),
@@ -586,7 +587,9 @@ def test_die_map_and_die_aware_k3(dev):
             sched = torch.full((4,), 7, dtype=torch.int32, device=dev) if mode != "static" else None
             hotpath.lmhead_stats(Hc, W, S, pm, ps, pa, m_host=m, v_offset=3, die_of_sm=tab, sched=sched)
             torch.cuda.synchronize()
-            if sched is not None:  # one failed claim per pair ends its loop
+            if sched is not None and units <= 2 * workers:  # small launches keep the static order
+                assert int(sched[1]) == 7
+            elif sched is not None:  # one failed claim per pair ends its loop
                 claimed, front, back = (int(v) for v in sched[:3].cpu())
                 if tab is None:  # front counter only
                     assert front == units + pairs and back == 0 and claimed == 0
