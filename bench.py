@@ -359,7 +359,12 @@ def gpu_main(args):
     if not args.no_e2e:
         # Host-resident inputs (pinned), results read back every step. Steps are
         # pipelined: the H2D copy of step i+1 runs on a copy stream into the
-        # other half of a double buffer while step i computes.
+        # other half of a double buffer while step i computes. With N ranks the
+        # job's hidden states cross PCIe once: rank r copies rows
+        # [r L/N, (r+1) L/N) from its host and an all-gather over NVLink (its own
+        # communicator, so it never queues behind the step's triple exchange)
+        # assembles H on every rank -- instead of every rank pulling all 268 MB
+        # through its own PCIe link.
         xh = x0.cpu().pin_memory()
         Hh = H.cpu().pin_memory()
         xo = torch.empty_like(xh).pin_memory()
@@ -368,6 +373,10 @@ def gpu_main(args):
         copy_s = torch.cuda.Stream(device=dev)
         ready = [torch.cuda.Event(), torch.cuda.Event()]
         done = [torch.cuda.Event(), torch.cuda.Event()]
+        shard_h2d = world > 1 and SEQ % world == 0
+        h_group = dist.new_group(backend=args.backend) if shard_h2d else None
+        rows = SEQ // world
+        h_rows = slice(rank * rows, (rank + 1) * rows) if shard_h2d else slice(0, SEQ)
 
         def issue_copy(i, after=None):
             b = i % 2
@@ -377,7 +386,13 @@ def gpu_main(args):
                 if i >= 2:
                     copy_s.wait_event(done[b])  # buffer b free again
                 xd[b].copy_(xh, non_blocking=True)
-                Hd[b].copy_(Hh, non_blocking=True)
+                Hd[b][h_rows].copy_(Hh[h_rows], non_blocking=True)
+                if shard_h2d:  # the other ranks' row blocks over NVLink
+                    if args.backend == "nccl":
+                        dist.all_gather_into_tensor(Hd[b], Hd[b][h_rows], group=h_group)
+                    else:  # gloo (the shared-GPU test): list form
+                        dist.all_gather(list(Hd[b].view(world, rows, D).unbind(0)), Hd[b][h_rows].clone(),
+                                        group=h_group)
                 ready[b].record(copy_s)
 
         def run(i):
@@ -396,6 +411,10 @@ def gpu_main(args):
 
         pipeline(3)
         torch.cuda.synchronize()
+        # the assembled hidden states are this rank's full H (x is committed in place by the step),
+        # and the read-back x is a committed step
+        assert torch.equal(Hd[0], H) and torch.equal(Hd[1], H)
+        assert int((xo == MASK_ID).sum()) == M - k
         if world > 1:
             dist.barrier()
         s2, e2 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -407,10 +426,12 @@ def gpu_main(args):
         if world > 1:
             dist.all_reduce(t2, op=dist.ReduceOp.MAX)
         e2e = {"value": M * args.steps / (float(t2[0]) / 1e3), "unit": "masked tokens/s",
-               "h2d_bytes_per_step": xh.numel() * 4 + Hh.numel() * 2,
+               "h2d_bytes_per_step": xh.numel() * 4 + Hh[h_rows].numel() * 2,
                "d2h_bytes_per_step": xo.numel() * 4,
-               "note": "pinned host H and x copied in every step (double-buffered copy stream overlapping the "
-                       "previous step's compute); updated x read back every step"}
+               "note": ("pinned host H and x copied in every step (double-buffered copy stream overlapping the "
+                        "previous step's compute); updated x read back every step"
+                        + (f"; per rank: x and 1/{world} of H's rows from the host, the rest of H all-gathered "
+                           f"over NVLink (h2d_bytes_per_step is this rank's)" if shard_h2d else ""))}
 
     peaks = json.loads((ROOT / "MEASURED_PEAKS.json").read_text()) if (ROOT / "MEASURED_PEAKS.json").exists() else {}
     # Denominator by the length of the timed region: K3 runs back to back for

@@ -25,13 +25,17 @@ def _port():
         return s.getsockname()[1]
 
 
-@pytest.mark.parametrize("world,exchange", [(2, "nccl"), (2, "p2p"), (4, "nccl"), (4, "p2p"), (8, "p2p")])
-def test_bench_multi_rank(native_lib, world, exchange):
+@pytest.mark.parametrize("world,exchange,e2e", [(2, "nccl", True), (2, "p2p", False), (4, "nccl", False),
+                                                (4, "p2p", True), (8, "p2p", False)])
+def test_bench_multi_rank(native_lib, world, exchange, e2e):
+    """... and with e2e: each rank copies 1/N of H's rows from the host and the
+    all-gather assembles the rest (bench.py asserts every rank's H equals the
+    generated one and the read-back x is the committed step)."""
     env = {**os.environ, "MOSAIC_BENCH_SHARE_GPU": "1"}
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", str(world),
            "--master-addr", "127.0.0.1", "--master-port", str(_port()), str(ROOT / "bench.py"), "--gpus", str(world),
-           "--steps", "2", "--warmup", "3", "--no-cpu-baseline", "--no-e2e", "--no-activation",
-           "--backend", "gloo", "--exchange", exchange]
+           "--steps", "2", "--warmup", "3", "--no-cpu-baseline", "--no-activation",
+           "--backend", "gloo", "--exchange", exchange] + ([] if e2e else ["--no-e2e"])
     r = subprocess.run(cmd, cwd=ROOT, env=env, capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stderr[-4000:]
     lines = [json.loads(l) for l in r.stdout.splitlines() if l.startswith("{")]
@@ -40,3 +44,6 @@ def test_bench_multi_rank(native_lib, world, exchange):
     assert line["n_gpus"] == world and line["value"] > 0 and line["config"]["vocab_shard"] == 126464 // world
     assert exchange in line["config"]["parallelism"]
     assert line["gpu_launches"] > 0
+    if e2e:
+        assert line["e2e"]["value"] > 0
+        assert line["e2e"]["h2d_bytes_per_step"] == 32768 * 4 + 32768 // world * 4096 * 2
