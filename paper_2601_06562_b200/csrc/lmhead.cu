@@ -14,13 +14,15 @@
 // 4 stages) serves M <= 128.
 //
 // Work decomposition: the vocab tiles (256 columns) are cut into n_splits
-// contiguous splits; a work unit is (row block, split). Each pair loops over
-// units u = cluster, cluster + n_clusters, ... (or its die's share, see the
-// die-aware schedule) and keeps the per-row statistics of the current unit in
-// registers across the split's tiles, so the only global output is one
-// (max, sum, arg) triple per row and split. Units are numbered m-fastest inside
-// groups of `group_m` row blocks, so the ~74 units in flight share a handful of
-// W tiles and row blocks through L2.
+// contiguous splits; a work unit is (row block, split). Each pair takes the
+// units the dynamic schedule hands it (claimed from a global counter by the
+// pair leader and published to both CTAs through a shared-memory ring; the
+// static order u = cluster, cluster + n_clusters, ... without a scratch) and
+// keeps the per-row statistics of the current unit in registers across the
+// split's tiles, so the only global output is one (max, sum, arg) triple per
+// row and split. Units are numbered m-fastest inside groups of `group_m` row
+// blocks, so the ~74 units in flight share a handful of W tiles and row blocks
+// through L2.
 #include <algorithm>
 #include <cstdlib>
 
@@ -1062,7 +1064,7 @@ extern "C" int mosaic_lmhead_sample(const uint16_t* Hc, int64_t m_cap, const int
   MOSAIC_REQUIRE(part_max && part_sum && part_arg && part_y && part_x && pos, "null operands");
   MOSAIC_REQUIRE(temperature > 0.f && temperature < 1e30f, "temperature must be positive (0 = argmax: use "
                  "mosaic_lmhead_stats)");
-  MOSAIC_REQUIRE(die_of_sm == nullptr || sched_scratch != nullptr, "die-aware schedule needs its scratch");
+  MOSAIC_REQUIRE(die_of_sm == nullptr || sched_scratch != nullptr, "the die map needs the dynamic schedule's scratch");
   const int64_t n_tiles = ceil_div(V_shard, BN);
   MOSAIC_REQUIRE(n_splits >= 1 && n_splits <= n_tiles, "n_splits=%d not in [1, %lld]", n_splits,
                  (long long)n_tiles);
@@ -1140,7 +1142,7 @@ extern "C" int mosaic_lmhead_stats_runs(const uint16_t* H, int64_t n_rows, int64
                                         void* stream) {
   MOSAIC_REQUIRE(H && idx && Hc && part_max && part_sum && part_arg, "null operands");
   MOSAIC_REQUIRE(n_rows >= 1 && n_rows < (int64_t(1) << 31), "n_rows out of range");
-  MOSAIC_REQUIRE(die_of_sm == nullptr || sched_scratch != nullptr, "die-aware schedule needs its 16-byte scratch");
+  MOSAIC_REQUIRE(die_of_sm == nullptr || sched_scratch != nullptr, "the die map needs the dynamic schedule's 16-byte scratch");
   const int64_t n_tiles = ceil_div(V_shard, BN);
   MOSAIC_REQUIRE(n_splits >= 1 && n_splits <= n_tiles, "n_splits=%d not in [1, %lld]", n_splits,
                  (long long)n_tiles);

@@ -1,7 +1,9 @@
 // SM -> L2-die map of this GPU, measured (the split is per physical part on
-// B200: two dies, each L2 caching for its own SMs). Used by K3's die-aware
-// unit schedule so the gathered rows an m-group re-reads stay in ONE die's L2
-// instead of being replicated in both.
+// B200: two dies, each L2 caching for its own SMs). The optional die split of
+// K3's dynamic unit schedule uses it (die-0 pairs claim units from the front
+// of the order, die-1 pairs from the back), so each die's m-groups stay in its
+// own L2; off by default -- the undivided dynamic schedule measured better
+// (DESIGN.md §4).
 //
 // Method (validated on B200, profiles/r01_die_probe.txt): one CTA reads a
 // pool of lines (bringing each into its own die's L2 and into the line's home

@@ -161,8 +161,8 @@ class StepExecutor:
         dev = torch.device("cuda", workspace.device)
         self.device = dev
         self._side: dict[int, dict] = {}
-        # K3's die-aware unit schedule (csrc/lmhead.cu), chosen per call by
-        # problem size as in MaskOnlyHead (hotpath.die_aware_default)
+        # the optional die split of K3's dynamic unit schedule (csrc/lmhead.cu),
+        # decided as in MaskOnlyHead (hotpath.die_aware_default: off by default)
         self._die_aware = die_aware
         self._die_table = None
         self._die_tried = False

@@ -141,7 +141,8 @@ _DIE_MAPS: dict = {}
 
 def die_map(device=None) -> tuple[torch.Tensor, dict]:
     """The measured SM -> L2-die map of ``device`` (cached per process): a
-    device uint8 tensor [num SMs] for K3's die-aware schedule, plus counts."""
+    device uint8 tensor [num SMs] for the optional die split of K3's dynamic
+    schedule, plus counts."""
     if device is None or torch.device(device).index is None:
         dev = torch.device("cuda", torch.cuda.current_device())
     else:
@@ -160,7 +161,7 @@ def die_map(device=None) -> tuple[torch.Tensor, dict]:
 
 
 def die_table_or_none(device) -> Optional[torch.Tensor]:
-    """The die map for K3's die-aware schedule, or None (default schedule) if
+    """The die map for K3's die split, or None (undivided dynamic schedule) if
     the probe cannot run here -- e.g. too little free memory for its ~2x-L2
     scratch. The schedule is an optimisation only; the result is the same."""
     try:
@@ -222,7 +223,7 @@ def lmhead_stats_gather(hidden: torch.Tensor, idx: torch.Tensor, weight: torch.T
                         repeats: bool = False) -> None:
     """K3 in gather mode: the A rows come straight from ``hidden`` [n, d] at
     the masked positions ``idx`` (cp.async loader warps), no compacted
-    buffer; ``die_of_sm``/``sched`` select the die-aware schedule as in
+    buffer; ``die_of_sm``/``sched`` select the dynamic schedule (and its die split) as in
     :func:`lmhead_stats`. ``repeats``: ``idx`` may repeat a row (not strictly
     ascending), so no tile may be taken for a contiguous run."""
     if hidden.dtype != torch.bfloat16 or hidden.dim() != 2 or hidden.stride(1) != 1 or not hidden.is_cuda:
