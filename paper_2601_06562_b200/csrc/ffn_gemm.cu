@@ -75,6 +75,7 @@ struct GParams {
   uint16_t* C;
   int64_t ldc;
   uint32_t* sched;  // dynamic schedule: [unused, next unit, ...], zeroed per launch; null = static schedule
+  int32_t group_m;  // m-blocks per raster group (units m-fastest inside a group)
 };
 
 __device__ __forceinline__ float silu(float g) { return __fdividef(g, 1.f + __expf(-g)); }
@@ -94,13 +95,13 @@ struct Unit {
 
 template <int ROWS>
 __device__ __forceinline__ Unit unit_of(int64_t u, int n_tiles, int total_mb, const int32_t* s_off,
-                                        const int32_t* s_mbp, int G) {
-  const int64_t per_group = static_cast<int64_t>(kGroupM) * n_tiles;
+                                        const int32_t* s_mbp, int G, int group_m) {
+  const int64_t per_group = static_cast<int64_t>(group_m) * n_tiles;
   const int64_t gi = u / per_group;
   const int64_t rem = u - gi * per_group;
-  const int64_t gm = min(static_cast<int64_t>(kGroupM), total_mb - gi * kGroupM);
+  const int64_t gm = min(static_cast<int64_t>(group_m), total_mb - gi * group_m);
   const int nt = static_cast<int>(rem / gm);
-  const int gmb = static_cast<int>(gi * kGroupM + rem % gm);
+  const int gmb = static_cast<int>(gi * group_m + rem % gm);
   int lo = 0, hi = G - 1;  // largest g with s_mbp[g] <= gmb
   while (lo < hi) {
     const int mid = (lo + hi + 1) >> 1;
@@ -219,7 +220,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       for (int n = 0;; ++n) {
         const int64_t u = unit_at(n, dyn && rank == 0);
         if (u < 0) break;
-        const Unit w = unit_of<C::ROWS>(u, p.n_tiles, total_mb, s_off, s_mbp, G);
+        const Unit w = unit_of<C::ROWS>(u, p.n_tiles, total_mb, s_off, s_mbp, G, p.group_m);
         const int32_t a_row = static_cast<int32_t>(w.row0 + rank * BM);
         const int32_t b_row = static_cast<int32_t>(w.g * p.N + static_cast<int64_t>(w.nt) * BN + rank * C::B_ROWS);
         for (int kb = 0; kb < k_blocks; ++kb) {
@@ -280,7 +281,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (lane == 0) u = unit_at(n, false);
       u = __shfl_sync(0xffffffffu, u, 0);
       if (u < 0) break;
-      const Unit w = unit_of<C::ROWS>(u, p.n_tiles, total_mb, s_off, s_mbp, G);
+      const Unit w = unit_of<C::ROWS>(u, p.n_tiles, total_mb, s_off, s_mbp, G, p.group_m);
       const int64_t row = w.row0 + rank * BM + row_local;
       const bool live = row < w.row_end;
       mbar_wait(&tfull[acc], acc_phase);
@@ -458,6 +459,15 @@ extern "C" int mosaic_ffn_gemm_sched(const uint16_t* A, int64_t rows_cap, int64_
   // at most two tiles per pair: nothing to balance, keep the static order (and skip the counter memset)
   const int64_t tiles_cap = (ceil_div(rows_cap, static_cast<int64_t>(BM) * cg) + G) * p.n_tiles;
   p.sched = (force_static || tiles_cap <= 2 * (num_sms() / cg)) ? nullptr : sched_scratch;
+  // raster group: the ~74 tiles in flight span g m-blocks x 74/g weight tiles, (g + 74/g) x 512 x K bytes
+  // of L2. At K = 4096 the default 16 fits (41 MB); at the down projection's K = d_ff = 12288 it is 129 MB
+  // and g = 8 (the minimum of g + 74/g) measured best: DRAM 6.0 -> 4.0 GB, 2.31 -> 2.20 ms per LLaDA
+  // chunk (profiles/r02p_k10_group_m.txt; MOSAIC_K10_GROUP_M overrides)
+  static const int forced_gm = [] {
+    const char* e = getenv("MOSAIC_K10_GROUP_M");
+    return e ? atoi(e) : 0;
+  }();
+  p.group_m = forced_gm > 0 ? forced_gm : (K > 8192 ? 8 : kGroupM);
   st = cg == 2 ? launch_k10<2>(ta, tb, p, rows_cap, as_stream(stream))
                : launch_k10<1>(ta, tb, p, rows_cap, as_stream(stream));
   if (st) return st;
