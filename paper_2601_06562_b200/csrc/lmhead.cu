@@ -953,7 +953,11 @@ int launch(const ASource& a, int64_t m_cap, const int32_t* m_dev, int64_t m_host
   if (p.group_m <= 0) p.group_m = group_m_default() > 0 ? group_m_default() : 16;
   static const int seg_splits = env_int("MOSAIC_K3_SEG_SPLITS", 0);
   p.seg_splits = seg_splits;
-  static const int policy = env_int("MOSAIC_L2_POLICY", 1);  // measured best: A evict_last
+  // L2 policy of the (A, B) loads: A (the m-group's rows, re-read for every vocab tile) evict_last, B
+  // (an LM-head tile, consumed by the group's units within one wave and dead after) evict_first --
+  // measured best under the dynamic schedule (+2.2% steady over evict_last A alone,
+  // profiles/r02r_k3_l2_policy_dynamic.txt)
+  static const int policy = env_int("MOSAIC_L2_POLICY", 3);
   p.policy = policy;
   cudaStream_t s = as_stream(stream);
   MOSAIC_REQUIRE(p.die_of_sm == nullptr || p.sched != nullptr, "the die map needs the dynamic schedule's scratch");

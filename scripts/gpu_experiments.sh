@@ -150,7 +150,30 @@ for i in 1 2; do
   done
 done
 ;;
+l2_policy)
+# K3's L2 policy of the (A, B) loads under the dynamic schedule (MOSAIC_L2_POLICY 0-3): ncu DRAM of
+# one bench launch and the 100-step steady bench per policy.
+for pol in 1 0 2 3 1; do
+export MOSAIC_L2_POLICY=$pol
+d=$(timeout 300 ncu --metrics dram__bytes_read.sum --clock-control none -k regex:k3_lmhead -s 3 -c 1 \
+python bench.py --steps 1 --warmup 3 --no-cpu-baseline --no-e2e --no-activation 2>&1 | grep -E "dram__bytes_read" | awk '{print $NF$(NF-1)}')
+b=$(timeout 300 python bench.py --steps 100 --warmup 5 --no-cpu-baseline --no-activation --no-e2e 2>&1 | grep '^{' | tail -1 | \
+python -c "import json,sys; d=json.loads(sys.stdin.read()); print(round(d['value']), round(d['roofline']['k3_ms'],3), d['clocks']['sm_mhz'])")
+echo "policy=$pol dram=$d steady: $b"
+done
+;;
+l2_ab)
+# policy 1 vs 3 alternating (steady bench, 100 steps), then the K3 burst at every shape per policy
+for i in 1 2 3; do
+for pol in 1 3; do
+b=$(MOSAIC_L2_POLICY=$pol timeout 300 python bench.py --steps 100 --warmup 5 --no-cpu-baseline --no-activation --no-e2e 2>&1 | grep '^{' | tail -1 | \
+python -c "import json,sys; d=json.loads(sys.stdin.read()); print(round(d['value']), round(d['roofline']['k3_ms'],3), d['clocks']['sm_mhz'])")
+echo "policy=$pol steady: $b"
+done
+done
+for pol in 1 3; do MOSAIC_L2_POLICY=$pol timeout 900 python scripts/k3_die_ab.py --reps 2 2>&1 | sed "s/^/policy=$pol /"; done
+;;
 *)
-echo "usage: $0 runs_ab|die_ab|dyn|dyn_die|dyn_claim|sched_sweep|gm_sweep|k10_dyn|k10_gm|half_a"; exit 2
+echo "usage: $0 runs_ab|die_ab|dyn|dyn_die|dyn_claim|sched_sweep|gm_sweep|k10_dyn|k10_gm|half_a|l2_policy|l2_ab"; exit 2
 ;;
 esac
