@@ -76,6 +76,7 @@ struct GParams {
   int64_t ldc;
   uint32_t* sched;  // dynamic schedule: [unused, next unit, ...], zeroed per launch; null = static schedule
   int32_t group_m;  // m-blocks per raster group (units m-fastest inside a group)
+  int32_t b_evict_first;  // L2 policy of the weight tiles: evict_first (default) or evict_normal
 };
 
 __device__ __forceinline__ float silu(float g) { return __fdividef(g, 1.f + __expf(-g)); }
@@ -215,7 +216,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (warp == 0) {
     if (lane == 0) {
       const uint64_t pol_a = policy_evict_last();
-      const uint64_t pol_b = policy_evict_normal();
+      const uint64_t pol_b = p.b_evict_first ? policy_evict_first() : policy_evict_normal();
       uint32_t stage = 0, phase = 0;
       for (int n = 0;; ++n) {
         const int64_t u = unit_at(n, dyn && rank == 0);
@@ -468,6 +469,13 @@ extern "C" int mosaic_ffn_gemm_sched(const uint16_t* A, int64_t rows_cap, int64_
     return e ? atoi(e) : 0;
   }();
   p.group_m = forced_gm > 0 ? forced_gm : (K > 8192 ? 8 : kGroupM);
+  // weight tiles evict_first (as K3's LM-head tiles): gate/up 4.29 -> 4.24 ms, down 2.31 -> 2.25 ms per
+  // LLaDA chunk under ncu (profiles/r02s_k10_l2_policy.txt); MOSAIC_K10_B_EVICT_FIRST=0 restores evict_normal
+  static const int b_first = [] {
+    const char* e = getenv("MOSAIC_K10_B_EVICT_FIRST");
+    return e ? atoi(e) : 1;
+  }();
+  p.b_evict_first = b_first;
   st = cg == 2 ? launch_k10<2>(ta, tb, p, rows_cap, as_stream(stream))
                : launch_k10<1>(ta, tb, p, rows_cap, as_stream(stream));
   if (st) return st;

@@ -173,7 +173,16 @@ done
 done
 for pol in 1 3; do MOSAIC_L2_POLICY=$pol timeout 900 python scripts/k3_die_ab.py --reps 2 2>&1 | sed "s/^/policy=$pol /"; done
 ;;
+k10_policy)
+# K10 weight-tile L2 policy (MOSAIC_K10_B_EVICT_FIRST), ncu per launch on the LLaDA chunk, alternating
+for i in 1 2; do
+for bf in 0 1; do
+MOSAIC_K10_B_EVICT_FIRST=$bf timeout 600 ncu --metrics dram__bytes_read.sum,gpu__time_duration.sum,sm__cycles_elapsed.avg.per_second --clock-control none -k regex:k10_ \
+python scripts/ncu_targets.py 2>&1 | grep -E "dram__|duration|per_second" | sed "s/^/k10_b_evict_first=$bf /"
+done
+done
+;;
 *)
-echo "usage: $0 runs_ab|die_ab|dyn|dyn_die|dyn_claim|sched_sweep|gm_sweep|k10_dyn|k10_gm|half_a|l2_policy|l2_ab"; exit 2
+echo "usage: $0 runs_ab|die_ab|dyn|dyn_die|dyn_claim|sched_sweep|gm_sweep|k10_dyn|k10_gm|half_a|l2_policy|l2_ab|k10_policy"; exit 2
 ;;
 esac
