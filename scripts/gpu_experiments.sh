@@ -182,7 +182,17 @@ python scripts/ncu_targets.py 2>&1 | grep -E "dram__|duration|per_second" | sed 
 done
 done
 ;;
+k3_knobs)
+# K3 knob sweep under the current defaults: steady bench (100 steps) per setting, each beside a baseline run
+for kv in "MOSAIC_K3_TPS=10" "MOSAIC_K3_TPS=16" "MOSAIC_K3_TPS=19" "MOSAIC_K3_TPS=26" "MOSAIC_TMA_L2_PROMOTION=0" "MOSAIC_TMA_L2_PROMOTION=3" "MOSAIC_GROUP_M=12"; do
+for arm in base "$kv"; do
+b=$( ( [ "$arm" != base ] && export $arm; timeout 300 python bench.py --steps 100 --warmup 5 --no-cpu-baseline --no-activation --no-e2e ) 2>&1 | grep '^{' | tail -1 | \
+python -c "import json,sys; d=json.loads(sys.stdin.read()); print(round(d['value']), round(d['roofline']['k3_ms'],3), d['clocks']['sm_mhz'], d['config']['n_splits'])")
+echo "$arm steady: $b"
+done
+done
+;;
 *)
-echo "usage: $0 runs_ab|die_ab|dyn|dyn_die|dyn_claim|sched_sweep|gm_sweep|k10_dyn|k10_gm|half_a|l2_policy|l2_ab|k10_policy"; exit 2
+echo "usage: $0 runs_ab|die_ab|dyn|dyn_die|dyn_claim|sched_sweep|gm_sweep|k10_dyn|k10_gm|half_a|l2_policy|l2_ab|k10_policy|k3_knobs"; exit 2
 ;;
 esac
