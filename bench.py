@@ -478,6 +478,7 @@ def gpu_main(args):
                                       if "bf16_tflops" in peaks else "fallback 1590 (burst)")),
                      "peak_burst": burst, "frac_of_burst": achieved / burst,
                      "peak_sustained": sustained, "frac_of_sustained": achieved / sustained,
+                     "peak_datasheet": 2250.0, "frac_of_datasheet": achieved / 2250.0,  # dense bf16, NVIDIA spec
                      "k3_ms": k3_ms, "k3_share_of_step": k3_ms / ms_per_step,
                      "flops_per_launch": flops, "traffic": traffic, "traffic_source": traffic_src},
         "gpu_launches": launches_per_step * args.steps,
