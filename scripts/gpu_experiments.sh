@@ -192,7 +192,23 @@ echo "$arm steady: $b"
 done
 done
 ;;
+stages)
+# K3 ring depth (compile-time MOSAIC_K3_STAGES2, default 6) on a copy of the tree, steady bench alternating
+R=$(pwd)
+for st in 5 7; do
+rm -rf /tmp/exp$st && cp -r "$R" /tmp/exp$st && rm -f /tmp/exp$st/paper_2601_06562_b200/libmosaic_b200.so
+(cd /tmp/exp$st && MOSAIC_NVCC_DEFINES="MOSAIC_K3_STAGES2=$st" timeout 300 python -c "import __graft_entry__ as g; g.build()" > /dev/null 2>&1) || echo "build $st failed"
+done
+for i in 1 2; do
+for v in 6 5 7; do
+d=$R; [ $v != 6 ] && d=/tmp/exp$v
+b=$( (cd $d && timeout 300 python bench.py --steps 100 --warmup 5 --no-cpu-baseline --no-activation --no-e2e) 2>&1 | grep '^{' | tail -1 | \
+python -c "import json,sys; d=json.loads(sys.stdin.read()); print(round(d['value']), round(d['roofline']['k3_ms'],3), d['clocks']['sm_mhz'])")
+echo "stages=$v steady: $b"
+done
+done
+;;
 *)
-echo "usage: $0 runs_ab|die_ab|dyn|dyn_die|dyn_claim|sched_sweep|gm_sweep|k10_dyn|k10_gm|half_a|l2_policy|l2_ab|k10_policy|k3_knobs"; exit 2
+echo "usage: $0 runs_ab|die_ab|dyn|dyn_die|dyn_claim|sched_sweep|gm_sweep|k10_dyn|k10_gm|half_a|l2_policy|l2_ab|k10_policy|k3_knobs|stages"; exit 2
 ;;
 esac
