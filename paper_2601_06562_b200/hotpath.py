@@ -126,7 +126,7 @@ def lmhead_sample(hc: torch.Tensor, weight: torch.Tensor, n_splits: int, pos: to
     _native.call("mosaic_lmhead_sample", _p(hc), m_cap, _p(m_dev), int(m_host), _p(weight), weight.shape[0], d,
                  int(v_offset), int(n_splits), _p(pos), ctypes.c_float(float(temperature)),
                  ctypes.c_uint32(int(seed) & 0xFFFFFFFF), _p(part_max), _p(part_sum), _p(part_arg), _p(part_y),
-                 _p(part_x), _p(die_of_sm), _p(sched if die_of_sm is not None else None), _s(stream))
+                 _p(part_x), _p(die_of_sm), _p(sched), _s(stream))
 
 
 def sample_merge(part_max, part_sum, part_arg, part_y, part_x, S: int, stride: int, m_cap: int, token, conf,

@@ -1031,3 +1031,48 @@ def test_sampling_keys_batch_of_one_equals_step(dev):
     ref = orc.sample_stats(orc.logits_f64(H[src], W), q, _step_seed(3, 0), T)
     ok = ref["margin"] > 1e-3
     assert np.array_equal(outs[0][1][ok], ref["arg"][ok])
+
+
+@pytest.mark.parametrize("variant", ["gather", "runs", "sample"])
+def test_dynamic_schedule_every_k3_variant(dev, variant):
+    """Every K3 variant under the dynamic unit schedule equals its static-order
+    launch bit for bit, and claims every unit exactly once (front counter ends
+    at units + pairs: one failed claim per pair)."""
+    from paper_2601_06562_b200 import hotpath
+
+    rng = np.random.default_rng(31)
+    L, d, V, m = 12000, 1024, 30000, 6000
+    H = bf16_tensor(rng.standard_normal((L, d)), dev)
+    W = bf16_tensor(rng.standard_normal((V, d)) * 0.03, dev)
+    pos = np.sort(rng.choice(L, m, replace=False))
+    pos[:2000] = np.arange(3000, 5000)  # a long run: contiguous tiles beside scattered ones
+    pos = np.sort(np.unique(pos))
+    m = pos.size
+    idx = torch.from_numpy(pos.astype(np.int32)).to(dev)
+    S, _ = hotpath.lmhead_plan(m, V, d)
+    S2 = 2 * S
+    units = -(-m // hotpath.lmhead_tile_rows(m)) * S
+    workers = torch.cuda.get_device_properties(dev).multi_processor_count // 2
+    assert units > 2 * workers  # large enough to claim dynamically
+    outs = []
+    for sched in (None, torch.full((4,), 5, dtype=torch.int32, device=dev)):
+        planes = S2 if variant == "sample" else S
+        pm, ps = torch.empty(planes, m, device=dev), torch.empty(planes, m, device=dev)
+        pa = torch.empty(planes, m, dtype=torch.int32, device=dev)
+        if variant == "gather":
+            hotpath.lmhead_stats_gather(H, idx, W, S, pm, ps, pa, m, m_host=m, sched=sched)
+        elif variant == "runs":
+            hc = torch.empty(m, d, dtype=torch.bfloat16, device=dev)
+            hotpath.gather_rows_scattered(H, idx, hc, m, m_host=m)
+            hotpath.lmhead_stats_runs(H, idx, hc, W, S, pm, ps, pa, m, m_host=m, sched=sched)
+        else:
+            hc = torch.empty(m, d, dtype=torch.bfloat16, device=dev)
+            hotpath.gather_rows(H, idx, hc, m_host=m)
+            py, px = torch.empty(S2, m, device=dev), torch.empty(S2, m, device=dev)
+            hotpath.lmhead_sample(hc, W, S, idx, 0.8, 1234, pm, ps, pa, py, px, m_host=m, sched=sched)
+        torch.cuda.synchronize()
+        outs.append((pm.cpu(), ps.cpu(), pa.cpu()))
+        if sched is not None:
+            assert int(sched[1]) == units + min(units, workers)
+    for a, b in zip(*outs):
+        assert torch.equal(a, b)
