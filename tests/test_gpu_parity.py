@@ -1076,3 +1076,27 @@ def test_dynamic_schedule_every_k3_variant(dev, variant):
             assert int(sched[1]) == units + min(units, workers)
     for a, b in zip(*outs):
         assert torch.equal(a, b)
+
+
+@pytest.mark.parametrize("temperature", [0.0, 0.7])
+def test_head_uses_the_dynamic_schedule(dev, temperature):
+    """MaskOnlyHead's K3 launch claims its units dynamically (the product
+    default): after a step the head's schedule counter shows every unit
+    claimed once plus one failed claim per SM pair -- argmax and sampling."""
+    from paper_2601_06562_b200 import MaskOnlyHead, hotpath
+
+    rng = np.random.default_rng(8)
+    L, d, V = 16384, 512, 32768
+    mask_id = V - 1
+    x = rng.integers(0, V - 1, size=L).astype(np.int32)
+    x[L // 2:] = mask_id
+    H = bf16_tensor(rng.standard_normal((L, d)), dev)
+    W = bf16_tensor(rng.standard_normal((V, d)) * 0.03, dev)
+    head = MaskOnlyHead(W, seq_len=L, mask_id=mask_id, m_cap=L // 2, temperature=temperature, seed=1)
+    head.step(torch.from_numpy(x).to(dev), H, 64)
+    torch.cuda.synchronize()
+    m = L // 2
+    units = -(-m // hotpath.lmhead_tile_rows(m)) * head.n_splits
+    workers = torch.cuda.get_device_properties(dev).multi_processor_count // 2
+    assert units > 2 * workers
+    assert int(head.buf["sched"][1]) == units + min(units, workers)
