@@ -21,8 +21,8 @@
 // (mosaic/workload.py:261-272) in one epilogue, so neither the chunk's `down`
 // rows nor the [L, d] `ffn_acc` accumulator is ever written.
 //
-// Structure as K3 (csrc/lmhead.cu): warp 0 TMA producer, warp 1 TMEM
-// allocator + single-thread tcgen05.mma issuer (cta_group::2 256x256 tiles over
+// Structure as K3 (csrc/lmhead.cu): warp 0 TMEM allocator + TMA producer, warp 1
+// single-thread tcgen05.mma issuer (cta_group::2 256x256 tiles over
 // an SM pair by default, cta_group::1 128x256 for tiny row counts; BF16 ->
 // FP32), warps 2-5 epilogue draining a double-buffered TMEM accumulator;
 // persistent CTAs walk (m-block, n-tile) units rasterised in groups of
@@ -170,7 +170,14 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
     }
   }
-  if (warp == 1) tmem_alloc<CG>(tmem_slot, TMEM_COLS);
+  // TMEM is allocated (and freed) by warp 0, the warp that also runs the block's
+  // prologue: allocating from warp 1 showed up in compute-sanitizer racecheck as a
+  // RAW hazard on the allocator's reserved shared word (1025 reports per launch,
+  // 0 with warp 0; profiles/r02w_racecheck_tmem_alloc.txt)
+  if (warp == 0) {
+    __syncwarp();  // lane 0 initialised the barriers above; tcgen05.alloc is .sync.aligned
+    tmem_alloc<CG>(tmem_slot, TMEM_COLS);
+  }
   tc_fence_before();
   if constexpr (CG == 2) cluster_sync(); else __syncthreads();
   tc_fence_after();
@@ -360,7 +367,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   tc_fence_before();
   if constexpr (CG == 2) cluster_sync(); else __syncthreads();
-  if (warp == 1) {
+  if (warp == 0) {  // the allocating warp frees
     tc_fence_after();
     tmem_dealloc<CG>(tmem_base, TMEM_COLS);
   }

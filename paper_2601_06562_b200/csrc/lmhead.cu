@@ -37,7 +37,7 @@ constexpr int BK = 64;           // K per stage: one 128-byte swizzle atom of bf
 constexpr int UK = 16;           // K per tcgen05.mma (kind::f16)
 constexpr int NUM_ACC = 2;       // TMEM accumulator double buffer
 constexpr int TMEM_COLS = 512;   // 2 x 256 fp32 columns
-constexpr int kThreads = 192;    // warp0 TMA, warp1 MMA+TMEM, warps 2..5 epilogue
+constexpr int kThreads = 192;    // warp0 TMEM alloc + TMA, warp1 MMA, warps 2..5 epilogue
 #ifndef MOSAIC_K3_AWARPS
 #define MOSAIC_K3_AWARPS 4  // measured: 4 >= 8 once the per-stage sync is CTA-scope
 #endif
@@ -326,7 +326,14 @@ __global__ void __launch_bounds__(threads_for(kGather, kSample), 1)
     for (int i = 0; i < kURing; ++i) mbar_init(&ufull[i], 1);
     fence_mbar_init();
   }
-  if (warp == 1) tmem_alloc<CG>(tmem_slot, TMEM_COLS);
+  // TMEM is allocated (and freed) by warp 0, the warp that also runs the block's
+  // prologue: allocating from warp 1 showed up in compute-sanitizer racecheck as a
+  // RAW hazard on the allocator's reserved shared word (1025 reports per launch,
+  // 0 with warp 0; profiles/r02w_racecheck_tmem_alloc.txt)
+  if (warp == 0) {
+    __syncwarp();  // lane 0 initialised the barriers above; tcgen05.alloc is .sync.aligned
+    tmem_alloc<CG>(tmem_slot, TMEM_COLS);
+  }
   tc_fence_before();
   if constexpr (CG == 2) cluster_sync(); else __syncthreads();
   tc_fence_after();
@@ -788,7 +795,7 @@ __global__ void __launch_bounds__(threads_for(kGather, kSample), 1)
 
   tc_fence_before();
   if constexpr (CG == 2) cluster_sync(); else __syncthreads();
-  if (warp == 1) {
+  if (warp == 0) {  // the allocating warp frees
     tc_fence_after();
     tmem_dealloc<CG>(tmem_base, TMEM_COLS);
   }
